@@ -1,0 +1,240 @@
+"""CPU oracle for the SentenceKV hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2504_00970_b200``) never imports it and shares no code with it.
+
+The arithmetic lives in plain C (``oracle/skvref.c``, one function per step of the paper,
+each citing its passage); this module only marshals numpy arrays into those functions and
+sequences them in the order of Algorithm 1.  bf16 tensors are passed
+as their raw ``uint16`` bit patterns.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "skvref.c")
+_LIB = os.path.join(_HERE, "libskvref.so")
+
+# -O2, IEEE semantics: no -ffast-math, no fp contraction (the canonical fp32 order of the
+# selection arithmetic is written out explicitly, fmaf where the order says fma).
+CFLAGS = ["-O2", "-fPIC", "-shared", "-std=c11", "-ffp-contract=off", "-fno-fast-math"]
+
+
+def build(force: bool = False) -> str:
+    """Compile ``skvref.c`` into ``libskvref.so`` (gcc).  Returns the library path."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        i32, i64, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+        L.skvref_segment.argtypes = [P, i32, P, i32, i32, P]
+        L.skvref_segment.restype = i32
+        L.skvref_embed.argtypes = [P, i32, P, i32, P]
+        L.skvref_embed.restype = None
+        L.skvref_qs_append_mean.argtypes = [P, P, P, i32, i32, P]
+        L.skvref_qs_append_mean.restype = None
+        L.skvref_qs_reset.argtypes = [P, P, i32, i32]
+        L.skvref_qs_reset.restype = None
+        L.skvref_group_query.argtypes = [P, i32, i32, i32, P]
+        L.skvref_group_query.restype = None
+        L.skvref_score.argtypes = [P, P, i32, i32, P]
+        L.skvref_score.restype = None
+        L.skvref_select.argtypes = [P, P, i32, i32, P, P]
+        L.skvref_select.restype = i32
+        L.skvref_attend.argtypes = [P, i32, P, P, i32, P, P, i32, P]
+        L.skvref_attend.restype = None
+        L.skvref_kv_bytes.argtypes = [i64, i64, i64, i64, i64]
+        L.skvref_kv_bytes.restype = i64
+        L.skvref_f32_to_bf16.argtypes = [f32]
+        L.skvref_f32_to_bf16.restype = ctypes.c_uint16
+        L.skvref_bf16_to_f32.argtypes = [ctypes.c_uint16]
+        L.skvref_bf16_to_f32.restype = f32
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"], "oracle arrays must be C-contiguous"
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# ----------------------------------------------------------------------------- steps
+
+
+def segment(tokens, boundary_ids, tau: int) -> np.ndarray:
+    """P1: sentence offsets ``off[S+1]`` of one prompt (int32)."""
+    tokens = _c(tokens, np.int32)
+    bset = _c(boundary_ids, np.int32)
+    off = np.zeros(len(tokens) + 1, dtype=np.int32)
+    S = lib().skvref_segment(_p(tokens), len(tokens), _p(bset), len(bset), int(tau), _p(off))
+    return off[: S + 1].copy()
+
+
+def embed(K_bits, off) -> np.ndarray:
+    """P2, Eq. 1: mean key per sentence of one (b, g) unit.  K_bits uint16 [L][d]."""
+    K_bits = _c(K_bits, np.uint16)
+    off = _c(off, np.int32)
+    S = len(off) - 1
+    d = K_bits.shape[1]
+    E = np.zeros((S, d), dtype=np.uint16)
+    lib().skvref_embed(_p(K_bits), d, _p(off), S, _p(E))
+    return E
+
+
+def qs_append_mean(Sq, cnt, q_bits):
+    """D1, Eq. 2: Sq += q, cnt += 1, returns qbar = Sq / cnt.  In-place on Sq/cnt."""
+    Hq, d = q_bits.shape
+    q_bits = _c(q_bits, np.uint16)
+    qbar = np.zeros((Hq, d), dtype=np.float32)
+    lib().skvref_qs_append_mean(_p(Sq), _p(cnt), _p(q_bits), Hq, d, _p(qbar))
+    return qbar
+
+
+def qs_reset(Sq, cnt):
+    """D1 reset at a sentence boundary (Alg. 1 l.19-21)."""
+    lib().skvref_qs_reset(_p(Sq), _p(cnt), Sq.shape[0], Sq.shape[1])
+
+
+def group_query(qbar, grp: int, g: int) -> np.ndarray:
+    """GQA group query qt_g = sum of the group's mean queries (reading A9)."""
+    qbar = _c(qbar, np.float32)
+    qt = np.zeros(qbar.shape[1], dtype=np.float32)
+    lib().skvref_group_query(_p(qbar), grp, qbar.shape[1], g, _p(qt))
+    return qt
+
+
+def score(qt, E_bits) -> np.ndarray:
+    """D1 similarity qbar^T kbar, canonical fp32 order."""
+    qt = _c(qt, np.float32)
+    E_bits = _c(E_bits, np.uint16)
+    S, d = E_bits.shape
+    out = np.zeros(S, dtype=np.float32)
+    lib().skvref_score(_p(qt), _p(E_bits), S, d, _p(out))
+    return out
+
+
+def select(scores, off, tau: int):
+    """D2: ascending selected ids and the number of selected tokens."""
+    scores = _c(scores, np.float32)
+    off = _c(off, np.int32)
+    S = len(off) - 1
+    ids = np.zeros(max(S, 1), dtype=np.int32)
+    ntok = np.zeros(1, dtype=np.int32)
+    n = lib().skvref_select(_p(scores), _p(off), S, int(tau), _p(ids), _p(ntok))
+    return ids[:n].copy(), int(ntok[0])
+
+
+def attend(q_bits, K_bits, V_bits, off, ids) -> np.ndarray:
+    """D4, Eq. 3 in fp64 over the selected sentences' tokens.  q_bits [grp][d]."""
+    q_bits = _c(q_bits, np.uint16)
+    K_bits = _c(K_bits, np.uint16)
+    V_bits = _c(V_bits, np.uint16)
+    off = _c(off, np.int32)
+    ids = _c(ids, np.int32)
+    grp, d = q_bits.shape
+    out = np.zeros((grp, d), dtype=np.float64)
+    lib().skvref_attend(_p(q_bits), grp, _p(K_bits), _p(V_bits), d, _p(off), _p(ids), len(ids), _p(out))
+    return out
+
+
+def full_attend(q_bits, K_bits, V_bits) -> np.ndarray:
+    """O-FULL: Eq. 3 over all L tokens (the Full-KV baseline) -- one sentence [0, L)."""
+    L = K_bits.shape[0]
+    return attend(q_bits, K_bits, V_bits, np.array([0, L], np.int32), np.array([0], np.int32))
+
+
+def kv_bytes(M, H, d, tokens, elem_bytes=2) -> int:
+    """App. Cost(t) written out: M*H*(L+t)*d*2*elem_bytes."""
+    return int(lib().skvref_kv_bytes(M, H, d, tokens, elem_bytes))
+
+
+def f32_to_bf16_bits(x: float) -> int:
+    return int(lib().skvref_f32_to_bf16(float(x)))
+
+
+# ------------------------------------------------------------------- Algorithm 1 driver
+
+
+class Oracle:
+    """Algorithm 1 for the hot path, one object per prompt batch.
+
+    Shapes follow the ABI: tokens [B][L]; per layer K, V bf16 bits [B][G][L][d];
+    per decode step and layer q bf16 bits [B][Hq][d] and the input token ids [B].
+    """
+
+    def __init__(self, tokens, boundary_ids, tau: int, layers: int, q_heads: int, kv_heads: int, d: int):
+        self.tokens = np.asarray(tokens, dtype=np.int32)
+        self.B = self.tokens.shape[0]
+        self.bset = np.asarray(boundary_ids, dtype=np.int32)
+        self.tau = int(tau)
+        self.M, self.Hq, self.G, self.d = layers, q_heads, kv_heads, d
+        self.grp = q_heads // kv_heads
+        # P1: segmentation, shared by all layers and heads (Alg. 1 line 2).
+        self.off = [segment(self.tokens[b], self.bset, self.tau) for b in range(self.B)]
+        self.E = {}  # layer -> list[b][g] of E bits
+        self.K = {}
+        self.V = {}
+        self.Sq = np.zeros((layers, self.B, q_heads, d), dtype=np.float32)
+        self.cnt = np.zeros((layers, self.B), dtype=np.int32)
+
+    def prefill_layer(self, layer: int, K_bits, V_bits):
+        """Alg. 1 lines 3-8 for one layer: Eq. 1 mean keys; K/V kept whole (A6, A19)."""
+        self.K[layer], self.V[layer] = K_bits, V_bits
+        self.E[layer] = [[embed(K_bits[b, g], self.off[b]) for g in range(self.G)] for b in range(self.B)]
+
+    def decode_select(self, layer: int, q_bits, input_token):
+        """Alg. 1 lines 14-17: append q_t, qbar (Eq. 2), similarity, budgeted retrieval.
+
+        Returns (scores[b][g], ids[b][g], ntok[b][g]); applies the boundary reset (A11)
+        after the step."""
+        scores, ids, ntok = [], [], []
+        for b in range(self.B):
+            Sq = self.Sq[layer, b]
+            cnt = self.cnt[layer, b : b + 1]
+            qbar = qs_append_mean(Sq, cnt, q_bits[b])
+            sb, ib, nb = [], [], []
+            for g in range(self.G):
+                qt = group_query(qbar, self.grp, g)
+                sc = score(qt, self.E[layer][b][g])
+                sel, n = select(sc, self.off[b], self.tau)
+                sb.append(sc)
+                ib.append(sel)
+                nb.append(n)
+            scores.append(sb)
+            ids.append(ib)
+            ntok.append(nb)
+            if int(input_token[b]) in set(self.bset.tolist()):
+                qs_reset(Sq, cnt)
+        return scores, ids, ntok
+
+    def decode_attend(self, layer: int, q_bits, ids):
+        """Alg. 1 line 19 / Eq. 3 over the selection of this layer: O fp64 [B][Hq][d]."""
+        O = np.zeros((self.B, self.Hq, self.d), dtype=np.float64)
+        for b in range(self.B):
+            for g in range(self.G):
+                h0 = g * self.grp
+                O[b, h0 : h0 + self.grp] = attend(
+                    q_bits[b, h0 : h0 + self.grp], self.K[layer][b, g], self.V[layer][b, g], self.off[b], ids[b][g]
+                )
+        return O
