@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""bench.py -- SentenceKV decode-step benchmark on B200 (driver contract: one JSON line on rank 0).
+
+A "step" is one pass of the whole hot path for one decode token: for every layer,
+D1+D2 (sentencekv_decode_select: Eq. 2 query cache, scores over all sentence embeddings,
+budgeted whole-sentence selection) and D3+D4 (sentencekv_decode_attend: gather + Eq. 3
+attention over the selected tokens), for all sequences of the batch.  Prefill (P1 segmentation,
+P2 embeddings) runs once before the timed region.
+
+Default workload (BASELINE.json metric "decode-step latency (ms) & tokens/s at 128K ctx"):
+configs[2] = Llama-3.1-8B shapes (32 layers, 32 Q / 8 KV heads, d=128), 128K context, tau=2048,
+batch 4.  value = tokens/s = sequences decoded per second (B per step) over all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 8b-128k] [--impl ours|reference]
+
+Multi-GPU (torchrun): weak scaling by batch -- each rank decodes its own batch of sequences with
+all KV heads (independent units; no collective on the data path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (B, M layers, Hq, G, d, L, tau, median sentence length)
+    "tiny": dict(B=1, M=1, Hq=8, G=2, d=64, L=4096, tau=256, median=20.0),
+    "8b-32k": dict(B=1, M=32, Hq=32, G=8, d=128, L=32768, tau=1024, median=25.0),
+    "8b-128k": dict(B=4, M=32, Hq=32, G=8, d=128, L=131072, tau=2048, median=25.0),
+    "8b-256k": dict(B=1, M=32, Hq=32, G=8, d=128, L=262144, tau=4096, median=25.0),
+    "70b-128k": dict(B=16, M=80, Hq=64, G=8, d=128, L=131072, tau=2048, median=25.0),
+}
+METRIC = "decode-step latency (ms) & tokens/s at 128K ctx; achieved HBM GB/s vs B200 peak"
+SEED = 0
+POOL = 8  # distinct decode steps cycled through (CUDA graph per step)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="8b-128k", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML in a thread during the timed region."""
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.sm, self.reasons, self.max_sm = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML missing: record it
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            nv.nvmlClocksEventReasonGpuIdle if hasattr(nv, "nvmlClocksEventReasonGpuIdle") else 0x1: "gpu_idle",
+            0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+        }
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_sm,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
+
+
+# --------------------------------------------------------------------------- oracle timing
+
+
+def oracle_sample(cfg, toks, Kh, Vh, qs, script, units, layers_sample, n_steps):
+    """Times the CPU oracle (select + attend per unit) on host copies of the same inputs.
+    Kh/Vh: {layer: uint16 [B][G][L][d]}; qs[step][layer]: uint16 [B][Hq][d].
+    Returns (seconds per (unit, layer, step), threads used)."""
+    import concurrent.futures as cf
+
+    import oracle
+
+    G, Hq, d, tau = cfg["G"], cfg["Hq"], cfg["d"], cfg["tau"]
+    grp = Hq // G
+    B = toks.shape[0]
+    offs = {b: oracle.segment(toks[b], __import__("synth").BOUNDARY_IDS, tau) for b in set(u[0] for u in units)}
+    threads = len(os.sched_getaffinity(0))
+    E = {}
+    with cf.ThreadPoolExecutor(threads) as ex:
+        futs = {(l, b, g): ex.submit(oracle.embed, Kh[l][b, g], offs[b]) for l in layers_sample for b, g in units}
+        for k, f in futs.items():
+            E[k] = f.result()
+    Sq = {(l, b): np.zeros((Hq, d), np.float32) for l in layers_sample for b in range(B)}
+    cnt = {(l, b): np.zeros(1, np.int32) for l in layers_sample for b in range(B)}
+
+    def unit_step(l, b, g, q_bits, qbar):
+        qt = oracle.group_query(qbar, grp, g)
+        sc = oracle.score(qt, E[(l, b, g)])
+        ids, _ = oracle.select(sc, offs[b], tau)
+        oracle.attend(q_bits[b, g * grp:(g + 1) * grp], Kh[l][b, g], Vh[l][b, g], offs[b], ids)
+
+    bset = set(__import__("synth").BOUNDARY_IDS.tolist())
+    t0 = time.perf_counter()
+    work = 0
+    with cf.ThreadPoolExecutor(threads) as ex:
+        for s in range(n_steps):
+            for l in layers_sample:
+                q_bits = qs[s % len(qs)][l]
+                qbars = {b: oracle.qs_append_mean(Sq[(l, b)], cnt[(l, b)], q_bits[b]) for b in set(u[0] for u in units)}
+                list(ex.map(lambda u: unit_step(l, u[0], u[1], q_bits, qbars[u[0]]), units))
+                work += len(units)
+                for b in set(u[0] for u in units):
+                    if int(script[s % len(script)][b]) in bset:
+                        oracle.qs_reset(Sq[(l, b)], cnt[(l, b)])
+    dt = time.perf_counter() - t0
+    return dt / work, threads
+
+
+# --------------------------------------------------------------------------- main
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = dict(CONFIGS[args.config])
+    B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
+    hbm_peak, peak_kind = peaks()
+
+    import torch
+
+    import synth
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, rank, world)
+
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_2504_00970_b200 as skvlib
+
+    # ---------------- inputs (seeded, synthetic; this rank's batch shard = global b in [rank*B, rank*B+B))
+    toks, topics = zip(*(synth.token_stream(SEED, rank * B + b, L, cfg["median"]) for b in range(B)))
+    toks, topics = np.stack(toks), np.stack(topics)
+    tok_dev = torch.from_numpy(toks).to(dev)
+    top_dev = torch.from_numpy(topics).to(dev)
+    skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
+                            device=local)
+    Ks, Vs, Cs = [], [], []
+    t_gen = time.perf_counter()
+    for l in range(M):
+        K, V, c = synth.kv_layer_torch(SEED + 1000 * rank, l, top_dev, G, d, device=dev)
+        Ks.append(K)
+        Vs.append(V)
+        Cs.append(c)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+
+    # ---------------- prefill (P1 + P2), timed for information
+    skv.set_profiling(True)
+    pf0 = torch.cuda.Event(enable_timing=True)
+    pf1 = torch.cuda.Event(enable_timing=True)
+    pf0.record()
+    for l in range(M):
+        skv.prefill_compress(l, Ks[l], Vs[l], token_ids=tok_dev if l == 0 else None,
+                             boundary_ids=synth.BOUNDARY_IDS if l == 0 else None)
+    pf1.record()
+    torch.cuda.synchronize()
+    prefill_ms = pf0.elapsed_time(pf1)
+    prof_prefill = skv.profile_read()
+    skv.set_profiling(False)
+    S = skv.sentence_counts()
+
+    # ---------------- decode inputs: POOL distinct steps
+    script, target = synth.decode_script(SEED + rank, B, POOL)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    tgt = torch.from_numpy(target).to(dev)
+    qpool = [[synth.queries_torch(gen, Cs[l], tgt[p], Hq, G, d).contiguous() for l in range(M)] for p in range(POOL)]
+    itok = [torch.from_numpy(script[p]).to(dev) for p in range(POOL)]
+    outs = [torch.empty((B, Hq, d), dtype=torch.float32, device=dev) for _ in range(M)]
+    sel_tok = [torch.zeros((B, G), dtype=torch.int32, device=dev) for _ in range(M)]
+
+    def step(p, with_tokens=False):
+        for l in range(M):
+            skv.decode_select(l, qpool[p][l], itok[p], sel_tokens=sel_tok[l] if with_tokens else None)
+            skv.decode_attend(l, qpool[p][l], outs[l])
+
+    # eager warm-up, then one CUDA graph per pool step
+    for p in range(POOL):
+        step(p)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=dev)
+    graphs = []
+    with torch.cuda.stream(stream):
+        for p in range(POOL):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(p)
+            graphs.append(g)
+    torch.cuda.synchronize()
+    for w in range(args.warmup):
+        graphs[w % POOL].replay()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: K graph replays (device time, CUDA events, max over ranks)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        cur = torch.cuda.current_stream()
+        e0.record(cur)
+        for k in range(args.steps):
+            graphs[k % POOL].replay()
+        e1.record(cur)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = B * world / (ms_step / 1e3)
+
+    # ---------------- per-kernel durations (profiled eager pass, events on the launching stream)
+    skv.set_profiling(True)
+    ntok_sum = 0
+    nprof = POOL
+    for p in range(nprof):
+        step(p, with_tokens=True)
+        ntok_sum += sum(int(t.sum()) for t in sel_tok)
+    prof = skv.profile_read()
+    skv.set_profiling(False)
+    S_tot = sum(S)
+    score_bytes = G * S_tot * d * 2 + B * Hq * d * (2 + 4) + B * G * S_tot * 4  # E + q,Sq + scores
+    attend_launches = prof["attend"][1]
+    attend_bytes = ntok_sum * d * 2 * 2 / attend_launches + B * Hq * d * (2 + 4)  # selected K,V + q + O
+    select_bytes = B * G * S_tot * 4 + B * S_tot * 4 + B * Hq * d * (4 * 2 + 2)
+    kern = {}
+    for name, nbytes in (("score", score_bytes), ("attend", attend_bytes), ("select", select_bytes)):
+        ms, n = prof[name]
+        avg = ms / n
+        kern[name] = {"avg_us": round(avg * 1e3, 3), "bytes_per_launch": int(nbytes),
+                      "gbs": round(nbytes / (avg / 1e3) / 1e9, 1), "share": None}
+    tot_prof = sum(prof[k][0] for k in ("score", "select", "attend"))
+    for name in kern:
+        kern[name]["share"] = round(prof[name][0] / tot_prof, 3)
+    dom = max(("score", "attend"), key=lambda k: prof[k][0])
+    step_bytes = (score_bytes + select_bytes) * M + attend_bytes * M
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic,
+                "peak_kind": peak_kind,
+                "per_unit": "score: G*S*d*2 B (bf16 E) + q/Sq + scores; attend: sum(ntok)*d*2*2 B (K,V rows) + q + O"}
+
+    # ---------------- end to end through the public API with host buffers
+    qhost = [torch.stack(qpool[p]).cpu().pin_memory() for p in range(POOL)]  # [M][B][Hq][d]
+    thost = [t.cpu().pin_memory() for t in itok]
+    ohost = torch.empty((M, B, Hq, d), dtype=torch.float32).pin_memory()
+    qdev = torch.empty((M, B, Hq, d), dtype=torch.bfloat16, device=dev)
+    tdev = torch.empty((B,), dtype=torch.int32, device=dev)
+    odev = torch.empty((M, B, Hq, d), dtype=torch.float32, device=dev)
+
+    def e2e_step(p):
+        qdev.copy_(qhost[p], non_blocking=True)
+        tdev.copy_(thost[p], non_blocking=True)
+        for l in range(M):
+            skvlib.sentencekv_decode_select(skv.ctx, l, qdev[l], tdev)
+            skvlib.sentencekv_decode_attend(skv.ctx, l, qdev[l], odev[l])
+        ohost.copy_(odev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for p in range(3):
+        e2e_step(p)
+    if world > 1:
+        dist.barrier()
+    x0 = torch.cuda.Event(enable_timing=True)
+    x1 = torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for k in range(args.e2e_steps):
+        e2e_step(k % POOL)
+    x1.record()
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": round(B * world / (e2e_ms / 1e3), 2), "unit": "tokens/s", "ms_per_step": round(e2e_ms, 4),
+           "h2d_bytes_per_step": int(qhost[0].numel() * 2 + B * 4), "d2h_bytes_per_step": int(ohost.numel() * 4)}
+
+    # ---------------- CPU oracle baseline (rank 0, N=1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        layers_sample = [0, 1] if M > 1 else [0]
+        units = [(b, g) for b in range(B) for g in range(G)]
+        Kh = {l: Ks[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
+        Vh = {l: Vs[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
+        qs_h = [[qpool[p][l].view(torch.int16).cpu().numpy().view(np.uint16) if l in layers_sample else None
+                 for l in range(M)] for p in range(POOL)]
+        n_steps = 2
+        per_unit, threads = oracle_sample(cfg, toks, Kh, Vh, qs_h, script, units, layers_sample, n_steps)
+        step_s = per_unit * B * G * M
+        cpu = {"value": round(B / step_s, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
+               "ms_per_step": round(step_s * 1e3, 1),
+               "sample": f"{n_steps} steps x {len(layers_sample)} of {M} layers x all {B * G} (b,g) units, "
+                         f"select+attend per unit timed, extrapolated to {M} layers"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in / fp32 acc (selection canonical fp32)",
+            "data": "synthetic (seeded token streams with punctuation boundaries, topic-structured K/V/q)",
+            "config": {"workload": args.config, "batch_per_gpu": B, "global_batch": B * world, "layers": M,
+                       "q_heads": Hq, "kv_heads": G, "head_dim": d, "context": L, "token_budget": tau,
+                       "sentences": S, "residency": "device (HBM)", "parallelism": f"batch-sharded x{world}",
+                       "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB read per step (L2 126 MB)",
+                       "cuda_graph": True},
+            "roofline": roofline,
+            "kernels": kern,
+            "step_bytes": int(step_bytes),
+            "step_gbs": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
+            "e2e": e2e,
+            "gpu_launches": 3 * M * args.steps,
+            "clocks": clk.summary(),
+            "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(B * G * L * d * 2 * M),
+                        "segment_ms": round(prof_prefill["segment"][0], 3),
+                        "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4),
+                        "compress_gbs": round(B * G * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
+            "cpu_baseline": cpu,
+            "kv_gen_s": round(t_gen, 2),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, on this arm's config, metric and unit.
+    Each step = a bounded sample (4 (b,g) units of one layer, select + attend), extrapolated to
+    the full step (all units, all layers).  Rank 0 only."""
+    if rank != 0:
+        return
+    import synth
+
+    B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
+    toks, topics = synth.prompts(SEED, 1, L, cfg["median"])
+    # host K/V for one (b=0) sequence, G heads, one layer (numpy generator)
+    K, V = synth.kv_layer(SEED, 0, topics, G, d)
+    script, target = synth.decode_script(SEED, 1, max(1, args.steps + args.warmup))
+    units = [(0, g) for g in range(min(4, G))]
+    qs = [[synth.queries(SEED, 0, s, target[s], Hq, G, d)] for s in range(8)]
+    # warm-up (W steps), then K timed steps
+    per_w, threads = oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], max(1, args.warmup))
+    per_unit, threads = oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], args.steps)
+    step_s = per_unit * B * G * M
+    value = B / step_s
+    cpu = {"value": round(value, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
+           "sample": f"each step: {len(units)} (b,g) units of 1 layer (select+attend), extrapolated to "
+                     f"{B * G} units x {M} layers"}
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 canonical / fp64",
+            "data": "synthetic", "config": {"workload": args.config, "global_batch": B * world, "context": L,
+                                            "token_budget": tau},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,196 @@
+/*
+ * sentencekv.h -- C ABI of the SentenceKV hot path on B200 (sm_100a).
+ *
+ * Library: paper_2504_00970_b200/libsentencekv.so (built by __graft_entry__.build()).
+ * Paper:   "SentenceKV" (arXiv 2504.00970); "P:<n>" = line n of PAPER.md, with the section,
+ *          equation or algorithm line it falls in.  Readings A1..A23 are listed in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *   - Plain C types only; no C++ exception crosses the boundary; every call returns skv_status.
+ *   - "device" pointers are CUDA device pointers on cfg.device; "host" pointers are ordinary
+ *     host memory.  The caller owns every pointer it passes in.
+ *   - All GPU work is enqueued on the given cudaStream_t (NULL = legacy default stream);
+ *     results are valid once that stream has completed the call's work.
+ *   - Argument errors are reported synchronously (SKV_ERR_INVALID_ARGUMENT / _STATE /
+ *     _UNSUPPORTED) and leave the context unchanged.  CUDA launch or asynchronous errors are
+ *     sticky: returned as SKV_ERR_CUDA by the call that sees them or by sentencekv_sync(), with
+ *     text from sentencekv_last_error().
+ *   - Decode entry points do no host synchronisation and no allocation, so a whole decode step
+ *     (all layers) can be captured into a CUDA graph.
+ *   - One context per host thread (single writer).  Contexts are independent.
+ *   - Tensor layouts are row-major, innermost dimension last; bf16 = IEEE bfloat16 bits.
+ *   - Multi-GPU: each rank creates one context over its shard (kv_head_begin/count,
+ *     batch_begin/count); every pointer passed is shard-local ([batch_count][...]).  The
+ *     all-gather of per-head outputs is done by the caller (torch.distributed, NCCL).
+ */
+#ifndef SENTENCEKV_H
+#define SENTENCEKV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* skv_stream_t; /* == cudaStream_t */
+typedef struct skv_ctx skv_ctx;
+
+typedef enum {
+    SKV_OK = 0,
+    SKV_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, non-positive size, Hq % G != 0, shard out of range,
+                                     tau < 1, r < 1, L < 1 or L > max_context, n_boundary < 1 or > 64,
+                                     K/V not 16-byte aligned, semantic_factor/token_budget != cfg */
+    SKV_ERR_STATE = 2,            /* layer out of range, decode before that layer's prefill, prefill of
+                                     layer > 0 before layer 0 of the same prompt */
+    SKV_ERR_UNSUPPORTED = 3,      /* head_dim not in {64, 128}; obs_window != 0 (importance retention
+                                     is not built yet) */
+    SKV_ERR_CUDA = 4,             /* CUDA launch / asynchronous failure (sticky; see last_error) */
+    SKV_ERR_OUT_OF_MEMORY = 5     /* device or pinned-host allocation failed */
+} skv_status;
+
+typedef enum {
+    SKV_KV_DEVICE = 0, /* K/V stay in HBM, borrowed from the caller (kept until next prefill/destroy) */
+    SKV_KV_HOST = 1    /* P3: full K/V offloaded to ctx-owned pinned host memory */
+} skv_residency;
+
+typedef struct {
+    int32_t batch;           /* B: sequences in the global batch */
+    int32_t layers;          /* M: transformer layers */
+    int32_t q_heads;         /* Hq: query heads (global) */
+    int32_t kv_heads;        /* G: KV heads (global); grp = Hq / G query heads share one KV head */
+    int32_t head_dim;        /* d in {64, 128} */
+    int32_t max_context;     /* L_max: largest prompt length accepted */
+    int32_t token_budget;    /* tau >= 1: retrieved tokens per (sequence, layer, KV head) (A15) */
+    float semantic_factor;   /* r >= 1; host residency: HBM working set = floor(r*tau)
+                                tokens per (sequence, layer, KV head) (A19, A20) */
+    int32_t obs_window;      /* N; must be 0 -- observation-window retention is NEXT-1 */
+    int32_t residency;       /* skv_residency */
+    int32_t device;          /* CUDA device ordinal */
+    int32_t kv_head_begin;   /* this rank's KV-head shard [begin, begin+count); 0, G = all */
+    int32_t kv_head_count;
+    int32_t batch_begin;     /* this rank's batch shard [begin, begin+count); 0, B = all */
+    int32_t batch_count;
+} skv_config;
+
+/* Fills cfg with defaults (shard = everything, device residency, r = 2, obs_window = 0). */
+void sentencekv_config_default(skv_config* cfg);
+
+/* Creates a context.  Allocates the per-layer query-cache state (Sq fp32 [M][B][Hq][d]) on
+ * cfg->device.  Sentence-dependent buffers are sized at the first prefill of a prompt.
+ * Errors: INVALID_ARGUMENT (see skv_status), UNSUPPORTED, OUT_OF_MEMORY, CUDA. */
+skv_status sentencekv_create(const skv_config* cfg, skv_ctx** out);
+
+/* Frees everything the context owns.  Synchronises the device first.  NULL is a no-op. */
+skv_status sentencekv_destroy(skv_ctx* ctx);
+
+/* Text of the last error of this context ("" if none).  Valid until the next call. */
+const char* sentencekv_last_error(const skv_ctx* ctx);
+
+/* Waits for all work of this context and surfaces asynchronous CUDA errors. */
+skv_status sentencekv_sync(skv_ctx* ctx);
+
+/*
+ * Prefill, one call per layer (Alg. 1 lines 2-8).
+ *   P1 (layer 0 only): split each prompt into sentence buckets at the boundary tokens
+ *      (Sec. 4.1; readings A1-A5: membership in boundary_ids, the boundary token
+ *      ends its sentence, no merging, trailing tokens form the last sentence, tau-cap).
+ *      Calling layer 0 starts a new prompt: it resets every layer's sentence query cache and
+ *      invalidates every layer's embeddings.  This call synchronises the stream once to learn
+ *      the sentence counts (prefill is not on the per-token path).
+ *   P2: sentence embeddings kbar_{s,g} = bf16(mean of the sentence's keys) (Eq. 1, P:402-405;
+ *      A6, A7, A23), kept in HBM (ctx-owned, [B][G][S_max][d] bf16 per layer).
+ *   P3 (SKV_KV_HOST): full K and V copied to ctx-owned pinned host memory (A19)
+ *      on an internal copy stream ordered after the caller's stream; the caller may free K/V
+ *      after sentencekv_sync().  SKV_KV_DEVICE: the ctx borrows K and V (no copy).
+ *
+ * token_ids     device int32 [batch_count][L]  (layer 0 only; ignored for layer > 0, may be NULL)
+ * L             prompt length, 1 <= L <= max_context; identical for every layer of a prompt
+ * boundary_ids  host int32 [n_boundary], 1 <= n_boundary <= 64: the punctuation token-id set
+ *               (layer 0 only; ignored for layer > 0)
+ * K, V          device bf16 [batch_count][kv_head_count][L][d], contiguous, 16-byte aligned
+ * semantic_factor, token_budget  must equal cfg values (checked; the paper's REQUIRE line)
+ */
+skv_status sentencekv_prefill_compress(skv_ctx* ctx, int32_t layer, const int32_t* token_ids, int32_t L,
+                                       const int32_t* boundary_ids, int32_t n_boundary, const void* K,
+                                       const void* V, float semantic_factor, int32_t token_budget,
+                                       skv_stream_t stream);
+
+/*
+ * Decode, per layer per step: D1 + D2 (Alg. 1 lines 14-17).
+ *   D1: append q_t to the layer's sentence query cache and form qbar (Eq. 2; A10),
+ *       group query qt_g = sum of the group's qbar_h (A9), similarity qt_g^T kbar_{s,g} for every
+ *       sentence (A23 canonical fp32).  If input_token[b] is a boundary id, the cache
+ *       of sequence b is reset after this step (A11).
+ *   D2: per (sequence, KV head): the maximal prefix of the ranking (score desc, index asc)
+ *       whose token count fits tau (A13, A14); result kept in the ctx for decode_attend.
+ *
+ * q            device bf16 [batch_count][kv_head_count*grp][d]: this step's query (as cached)
+ * input_token  device int32 [batch_count]: the token whose query this is
+ * sel_ids      device int32 [batch_count][kv_head_count][tau] or NULL: selected sentence ids,
+ *              ascending, tail filled with -1
+ * sel_count    device int32 [batch_count][kv_head_count] or NULL: number of selected sentences
+ * sel_tokens   device int32 [batch_count][kv_head_count] or NULL: selected tokens (<= tau)
+ */
+skv_status sentencekv_decode_select(skv_ctx* ctx, int32_t layer, const void* q, const int32_t* input_token,
+                                    int32_t* sel_ids, int32_t* sel_count, int32_t* sel_tokens,
+                                    skv_stream_t stream);
+
+/*
+ * Decode, per layer per step: D3 + D4 (Alg. 1 lines 18-19) over the selection made
+ * by the last decode_select of the same layer.
+ *   D3: gather the selected sentences' K/V rows (contiguous runs) into shared memory with bulk
+ *       async copies (device residency: from the caller's K/V in HBM).
+ *   D4: O = softmax(q K_sel^T / sqrt(d)) V_sel (Eq. 3; A16-A18), split-K
+ *       flash-decode with fp32 online softmax, combined in-kernel.
+ *
+ * q    device bf16 [batch_count][kv_head_count*grp][d]
+ * out  device fp32 [batch_count][kv_head_count*grp][d]
+ */
+skv_status sentencekv_decode_attend(skv_ctx* ctx, int32_t layer, const void* q, float* out,
+                                    skv_stream_t stream);
+
+/* ---- introspection (tests, bench; not on the per-token path) ---- */
+
+/* Sentence counts of the current prompt: S_out host int32 [batch_count]. */
+skv_status sentencekv_sentence_counts(skv_ctx* ctx, int32_t* S_out);
+
+/* Capacity S_max of the per-(b,g) sentence arrays of the current prompt (>= every S_b). */
+int32_t sentencekv_sentence_capacity(const skv_ctx* ctx);
+
+/* Sentence offsets of the current prompt: off_out device int32 [batch_count][S_max+1]
+ * (row b holds off[0..S_b], rest unspecified).  Enqueued on stream. */
+skv_status sentencekv_copy_offsets(skv_ctx* ctx, int32_t* off_out, skv_stream_t stream);
+
+/* Layer embeddings: E_out device bf16 [batch_count][kv_head_count][S_max][d]. */
+skv_status sentencekv_copy_embeddings(skv_ctx* ctx, int32_t layer, void* E_out, skv_stream_t stream);
+
+/* Scores of the last decode_select of the layer: device fp32 [batch_count][kv_head_count][S_max]. */
+skv_status sentencekv_copy_scores(skv_ctx* ctx, int32_t layer, float* scores_out, skv_stream_t stream);
+
+/* Number of CUDA kernel launches this context has enqueued since creation. */
+int64_t sentencekv_launch_count(const skv_ctx* ctx);
+
+/* ---- kernel profiler (bench / tracing; off by default) ----
+ * When on, every kernel launch of this context is bracketed by two CUDA events recorded on the
+ * launching stream.  Not for use while a stream is being captured into a CUDA graph. */
+typedef enum {
+    SKV_K_SEGMENT = 0, /* P1 */
+    SKV_K_COMPRESS = 1, /* P2 */
+    SKV_K_SCORE = 2,   /* D1 */
+    SKV_K_SELECT = 3,  /* D2 */
+    SKV_K_ATTEND = 4,  /* D3 + D4 */
+    SKV_K_COUNT = 5
+} skv_kernel_kind;
+
+skv_status sentencekv_set_profiling(skv_ctx* ctx, int32_t on);
+
+/* Synchronises, then adds the elapsed time of every profiled launch since the last read:
+ * ms_out host double [SKV_K_COUNT] (total milliseconds per kind), n_out host int64 [SKV_K_COUNT]
+ * (launches per kind).  Both are accumulated into (not overwritten). */
+skv_status sentencekv_profile_read(skv_ctx* ctx, double* ms_out, int64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SENTENCEKV_H */

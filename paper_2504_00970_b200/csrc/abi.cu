@@ -1,0 +1,408 @@
+// abi.cu -- skv_ctx runtime and the C ABI of include/sentencekv.h.
+//
+// Host-side responsibilities: argument validation (synchronous, state unchanged on error),
+// ownership of device / pinned-host buffers, stream ordering, sticky CUDA errors.  Every step of
+// the method runs in the kernels of prefill.cu, decode_select.cu and decode_attend.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "skv_internal.cuh"
+
+#define SKV_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+skv_status fail(skv_ctx* ctx, skv_status st, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+skv_status fail(skv_ctx* ctx, skv_status st, const char* fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return st;
+}
+
+skv_status cuda_fail(skv_ctx* ctx, cudaError_t e, const char* where) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(ctx, SKV_ERR_OUT_OF_MEMORY, "%s: %s", where, cudaGetErrorString(e));
+    }
+    ctx->sticky = SKV_ERR_CUDA;
+    return fail(ctx, SKV_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define SKV_CUDA(ctx, expr)                                          \
+    do {                                                             \
+        cudaError_t e_ = (expr);                                     \
+        if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #expr);   \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) return cudaSuccess;
+    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+void free_prompt_buffers(skv_ctx* c) {
+    for (auto& ls : c->layer) {
+        dfree(ls.E);
+        dfree(ls.scores);
+        dfree(ls.sel_ids);
+        dfree(ls.sel_tokoff);
+        dfree(ls.sel_count);
+        dfree(ls.o_part);
+        dfree(ls.ml_part);
+        dfree(ls.done);
+        ls.prefilled = false;
+        ls.selected = false;
+        ls.K = ls.V = nullptr;
+    }
+    dfree(c->off);
+    c->Smax = 0;
+    c->L = 0;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- kernel profiler: events bracketing each launch on its stream ----
+cudaEvent_t prof_event(skv_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+cudaEvent_t prof_begin(skv_ctx* c, cudaStream_t st) {
+    if (!c->profiling) return nullptr;
+    cudaEvent_t a = prof_event(c);
+    cudaEventRecord(a, st);
+    return a;
+}
+
+void prof_end(skv_ctx* c, int kind, cudaEvent_t a, cudaStream_t st) {
+    if (!a) return;
+    cudaEvent_t b = prof_event(c);
+    cudaEventRecord(b, st);
+    c->prof.push_back({kind, a, b});
+}
+
+}  // namespace
+
+SKV_API void sentencekv_config_default(skv_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->semantic_factor = 2.0f;
+    cfg->residency = SKV_KV_DEVICE;
+}
+
+SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
+    if (!cfg_in || !out) return SKV_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    skv_config cfg = *cfg_in;
+    if (cfg.batch < 1 || cfg.layers < 1 || cfg.q_heads < 1 || cfg.kv_heads < 1 || cfg.head_dim < 1 ||
+        cfg.max_context < 1 || cfg.token_budget < 1 || !(cfg.semantic_factor >= 1.0f) ||
+        cfg.q_heads % cfg.kv_heads != 0 || (cfg.residency != SKV_KV_DEVICE && cfg.residency != SKV_KV_HOST))
+        return SKV_ERR_INVALID_ARGUMENT;
+    if (cfg.kv_head_count == 0) cfg.kv_head_count = cfg.kv_heads - cfg.kv_head_begin;
+    if (cfg.batch_count == 0) cfg.batch_count = cfg.batch - cfg.batch_begin;
+    if (cfg.kv_head_begin < 0 || cfg.kv_head_count < 1 || cfg.kv_head_begin + cfg.kv_head_count > cfg.kv_heads ||
+        cfg.batch_begin < 0 || cfg.batch_count < 1 || cfg.batch_begin + cfg.batch_count > cfg.batch)
+        return SKV_ERR_INVALID_ARGUMENT;
+    const int grp = cfg.q_heads / cfg.kv_heads;
+    if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
+        cfg.obs_window != 0 || cfg.residency == SKV_KV_HOST)
+        return SKV_ERR_UNSUPPORTED;
+
+    skv_ctx* c = new (std::nothrow) skv_ctx();
+    if (!c) return SKV_ERR_OUT_OF_MEMORY;
+    c->cfg = cfg;
+    c->B = cfg.batch_count;
+    c->G = cfg.kv_head_count;
+    c->grp = grp;
+    c->Hq = c->G * grp;
+    c->d = cfg.head_dim;
+    c->tau = cfg.token_budget;
+    c->chunk = skv::attend_chunk_tokens(c->d);
+    c->nsplit = (c->tau + c->chunk - 1) / c->chunk;
+    c->layer.resize(cfg.layers);
+    c->S_host.assign(c->B, 0);
+
+    DeviceGuard dg(cfg.device);
+    cudaError_t e = cudaSuccess;
+    for (auto& ls : c->layer) {
+        if (e == cudaSuccess) e = dalloc(&ls.Sq, (size_t)c->B * c->Hq * c->d);
+        if (e == cudaSuccess) e = dalloc(&ls.cnt, (size_t)c->B);
+        if (e == cudaSuccess) e = cudaMemset(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d);
+        if (e == cudaSuccess) e = cudaMemset(ls.cnt, 0, sizeof(int32_t) * c->B);
+    }
+    if (e == cudaSuccess) e = dalloc(&c->S_dev, (size_t)c->B);
+    if (e == cudaSuccess) e = dalloc(&c->bset, (size_t)skv::kMaxBoundary);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        sentencekv_destroy(c);
+        return e == cudaErrorMemoryAllocation ? SKV_ERR_OUT_OF_MEMORY : SKV_ERR_CUDA;
+    }
+    *out = c;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
+    if (!c) return SKV_OK;
+    DeviceGuard dg(c->cfg.device);
+    cudaDeviceSynchronize();
+    free_prompt_buffers(c);
+    for (auto& ls : c->layer) {
+        dfree(ls.Sq);
+        dfree(ls.cnt);
+    }
+    dfree(c->S_dev);
+    dfree(c->bset);
+    for (auto& r : c->prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->copy_event) cudaEventDestroy(c->copy_event);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    delete c;
+    return SKV_OK;
+}
+
+SKV_API const char* sentencekv_last_error(const skv_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+SKV_API skv_status sentencekv_sync(skv_ctx* c) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(c->cfg.device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "sentencekv_sync");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "sentencekv_sync");
+    return c->sticky;
+}
+
+// (Re)allocates the sentence-dependent buffers of every layer for a prompt with capacity Smax.
+static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
+    const size_t B = c->B, G = c->G, d = c->d, tau = c->tau, ns = c->nsplit, grp = c->grp;
+    for (auto& ls : c->layer) {
+        SKV_CUDA(c, dalloc(&ls.E, B * G * Smax * d));
+        SKV_CUDA(c, dalloc(&ls.scores, B * G * Smax));
+        SKV_CUDA(c, dalloc(&ls.sel_ids, B * G * tau));
+        SKV_CUDA(c, dalloc(&ls.sel_tokoff, B * G * (tau + 1)));
+        SKV_CUDA(c, dalloc(&ls.sel_count, B * G));
+        SKV_CUDA(c, dalloc(&ls.o_part, B * G * ns * grp * d));
+        SKV_CUDA(c, dalloc(&ls.ml_part, B * G * ns * grp * 2));
+        SKV_CUDA(c, dalloc(&ls.done, B * G));
+        SKV_CUDA(c, cudaMemset(ls.done, 0, sizeof(uint32_t) * B * G));
+    }
+    c->Smax = Smax;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const int32_t* token_ids, int32_t L,
+                                               const int32_t* boundary_ids, int32_t n_boundary, const void* K,
+                                               const void* V, float semantic_factor, int32_t token_budget,
+                                               skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    if (L < 1 || L > c->cfg.max_context) return fail(c, SKV_ERR_INVALID_ARGUMENT, "L=%d outside [1, %d]", L, c->cfg.max_context);
+    if (!K || !V || !aligned16(K) || !aligned16(V))
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "K/V must be non-NULL and 16-byte aligned");
+    if (semantic_factor != c->cfg.semantic_factor || token_budget != c->tau)
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "semantic_factor/token_budget differ from the context config");
+    if (layer == 0) {
+        if (!token_ids) return fail(c, SKV_ERR_INVALID_ARGUMENT, "token_ids is NULL");
+        if (!boundary_ids || n_boundary < 1 || n_boundary > skv::kMaxBoundary)
+            return fail(c, SKV_ERR_INVALID_ARGUMENT, "boundary set must hold 1..%d ids", skv::kMaxBoundary);
+    } else if (c->L != L || !c->layer[0].prefilled) {
+        return fail(c, SKV_ERR_STATE, "prefill of layer %d before layer 0 of a prompt of length %d", layer, L);
+    }
+    DeviceGuard dg(c->cfg.device);
+
+    if (layer == 0) {
+        // ---- new prompt: P1 segmentation (once; shared by all layers and heads) ----
+        if (c->L != L || !c->off) {
+            dfree(c->off);
+            SKV_CUDA(c, dalloc(&c->off, (size_t)c->B * (L + 1)));
+            c->L = L;
+            c->off_stride = L + 1;
+        }
+        SKV_CUDA(c, cudaMemcpyAsync(c->bset, boundary_ids, sizeof(int32_t) * n_boundary, cudaMemcpyHostToDevice, st));
+        c->n_bset = n_boundary;
+        cudaEvent_t pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off, c->off_stride,
+                                        c->S_dev, st));
+        prof_end(c, SKV_K_SEGMENT, pa, st);
+        c->launches += 1;
+        SKV_CUDA(c, cudaMemcpyAsync(c->S_host.data(), c->S_dev, sizeof(int32_t) * c->B, cudaMemcpyDeviceToHost, st));
+        SKV_CUDA(c, cudaStreamSynchronize(st));
+        int Smax = 1;
+        for (int b = 0; b < c->B; ++b) Smax = c->S_host[b] > Smax ? c->S_host[b] : Smax;
+        if (Smax > c->Smax || !c->layer[0].E) {
+            for (auto& ls : c->layer) {
+                dfree(ls.E); dfree(ls.scores); dfree(ls.sel_ids); dfree(ls.sel_tokoff);
+                dfree(ls.sel_count); dfree(ls.o_part); dfree(ls.ml_part); dfree(ls.done);
+            }
+            skv_status s = alloc_prompt_buffers(c, Smax);
+            if (s != SKV_OK) return s;
+        }
+        for (auto& ls : c->layer) {
+            ls.prefilled = false;
+            ls.selected = false;
+            SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
+            SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B, st));
+        }
+    }
+
+    // ---- P2: Eq. 1 sentence embeddings of this layer ----
+    skv::LayerState& ls = c->layer[layer];
+    const auto* Kb = static_cast<const __nv_bfloat16*>(K);
+    const auto* Vb = static_cast<const __nv_bfloat16*>(V);
+    cudaEvent_t pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
+    prof_end(c, SKV_K_COMPRESS, pa, st);
+    c->launches += 1;
+    ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
+    ls.V = Vb;
+    ls.prefilled = true;
+    ls.selected = false;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const void* q, const int32_t* input_token,
+                                            int32_t* sel_ids, int32_t* sel_count, int32_t* sel_tokens,
+                                            skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (!ls.prefilled) return fail(c, SKV_ERR_STATE, "decode_select before prefill of layer %d", layer);
+    if (!q || !input_token) return fail(c, SKV_ERR_INVALID_ARGUMENT, "q / input_token is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    DeviceGuard dg(c->cfg.device);
+    const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    cudaEvent_t pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
+    prof_end(c, SKV_K_SCORE, pa, st);
+    pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax,
+                                   c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt, ls.sel_ids,
+                                   ls.sel_tokoff, ls.sel_count, sel_ids, sel_count, sel_tokens, st));
+    prof_end(c, SKV_K_SELECT, pa, st);
+    c->launches += 2;
+    ls.selected = true;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const void* q, float* out,
+                                            skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (!ls.prefilled || !ls.selected)
+        return fail(c, SKV_ERR_STATE, "decode_attend of layer %d before its prefill and decode_select", layer);
+    if (!q || !out) return fail(c, SKV_ERR_INVALID_ARGUMENT, "q / out is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    DeviceGuard dg(c->cfg.device);
+    cudaEvent_t pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_attend(static_cast<const __nv_bfloat16*>(q), ls.K, ls.V, c->B, c->G, c->grp, c->d, c->L,
+                                   c->off, c->off_stride, ls.sel_ids, ls.sel_tokoff, ls.sel_count, c->tau, c->chunk,
+                                   c->nsplit, ls.o_part, ls.ml_part, ls.done, out, st));
+    prof_end(c, SKV_K_ATTEND, pa, st);
+    c->launches += 1;
+    return SKV_OK;
+}
+
+// ------------------------------------------------------------------------------ introspection
+
+SKV_API skv_status sentencekv_sentence_counts(skv_ctx* c, int32_t* S_out) {
+    if (!c || !S_out) return SKV_ERR_INVALID_ARGUMENT;
+    if (!c->layer[0].prefilled) return fail(c, SKV_ERR_STATE, "no prompt");
+    std::memcpy(S_out, c->S_host.data(), sizeof(int32_t) * c->B);
+    return SKV_OK;
+}
+
+SKV_API int32_t sentencekv_sentence_capacity(const skv_ctx* c) { return c ? c->Smax : 0; }
+
+SKV_API skv_status sentencekv_copy_offsets(skv_ctx* c, int32_t* off_out, skv_stream_t stream_) {
+    if (!c || !off_out) return SKV_ERR_INVALID_ARGUMENT;
+    if (!c->layer[0].prefilled) return fail(c, SKV_ERR_STATE, "no prompt");
+    DeviceGuard dg(c->cfg.device);
+    SKV_CUDA(c, cudaMemcpy2DAsync(off_out, sizeof(int32_t) * (c->Smax + 1), c->off, sizeof(int32_t) * c->off_stride,
+                                  sizeof(int32_t) * (c->Smax + 1), c->B, cudaMemcpyDeviceToDevice,
+                                  reinterpret_cast<cudaStream_t>(stream_)));
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_copy_embeddings(skv_ctx* c, int32_t layer, void* E_out, skv_stream_t stream_) {
+    if (!c || !E_out) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers || !c->layer[layer].prefilled) return fail(c, SKV_ERR_STATE, "layer not prefilled");
+    DeviceGuard dg(c->cfg.device);
+    SKV_CUDA(c, cudaMemcpyAsync(E_out, c->layer[layer].E, sizeof(__nv_bfloat16) * c->B * c->G * c->Smax * c->d,
+                                cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream_)));
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_copy_scores(skv_ctx* c, int32_t layer, float* out, skv_stream_t stream_) {
+    if (!c || !out) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers || !c->layer[layer].selected) return fail(c, SKV_ERR_STATE, "layer not selected");
+    DeviceGuard dg(c->cfg.device);
+    SKV_CUDA(c, cudaMemcpyAsync(out, c->layer[layer].scores, sizeof(float) * c->B * c->G * c->Smax,
+                                cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream_)));
+    return SKV_OK;
+}
+
+SKV_API int64_t sentencekv_launch_count(const skv_ctx* c) { return c ? c->launches : 0; }
+
+SKV_API skv_status sentencekv_set_profiling(skv_ctx* c, int32_t on) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    c->profiling = on != 0;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_profile_read(skv_ctx* c, double* ms_out, int64_t* n_out) {
+    if (!c || !ms_out || !n_out) return SKV_ERR_INVALID_ARGUMENT;
+    DeviceGuard dg(c->cfg.device);
+    for (auto& r : c->prof) {
+        SKV_CUDA(c, cudaEventSynchronize(r.b));
+        float ms = 0.0f;
+        SKV_CUDA(c, cudaEventElapsedTime(&ms, r.a, r.b));
+        ms_out[r.kind] += ms;
+        n_out[r.kind] += 1;
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof.clear();
+    return SKV_OK;
+}

@@ -1,0 +1,106 @@
+// skv_internal.cuh -- shared declarations of the SentenceKV sm_100a kernels and the runtime
+// context behind the C ABI (include/sentencekv.h).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sentencekv.h"
+
+namespace skv {
+
+constexpr int kMaxBoundary = 64;
+constexpr int kNumSMs = 148;
+
+// Per-layer device state.  Sizes use the ctx shard: B = batch_count, G = kv_head_count,
+// Hq = G * grp, Smax = sentence capacity of the current prompt.
+struct LayerState {
+    bool prefilled = false;
+    bool selected = false;             // a decode_select ran since the prefill
+    const __nv_bfloat16* K = nullptr;  // device residency: borrowed [B][G][L][d]
+    const __nv_bfloat16* V = nullptr;
+    __nv_bfloat16* E = nullptr;        // [B][G][Smax][d]  sentence embeddings (Eq. 1)
+    float* Sq = nullptr;               // [B][Hq][d]       running query sum of Q_s (Eq. 2)
+    int32_t* cnt = nullptr;            // [B]              |Q_s|
+    float* scores = nullptr;           // [B][G][Smax]     last step's similarity scores
+    int32_t* sel_ids = nullptr;        // [B][G][tau]      ascending selected sentence ids
+    int32_t* sel_tokoff = nullptr;     // [B][G][tau+1]    prefix sums of selected lengths
+    int32_t* sel_count = nullptr;      // [B][G]
+    // split-K attention workspace
+    float* o_part = nullptr;           // [B][G][nsplit][grp][d]
+    float* ml_part = nullptr;          // [B][G][nsplit][grp][2]  (running max (log2 domain), sum)
+    uint32_t* done = nullptr;          // [B][G]  arrival counters of the split blocks
+    // host residency (P3)
+    __nv_bfloat16* Kh = nullptr;       // pinned host [B][G][L][d]
+    __nv_bfloat16* Vh = nullptr;
+};
+
+}  // namespace skv
+
+struct skv_ctx {
+    skv_config cfg{};
+    int B = 0, G = 0, Hq = 0, grp = 0, d = 0, tau = 0;
+    std::string err;
+    skv_status sticky = SKV_OK;
+    int64_t launches = 0;
+
+    // prompt state
+    int L = 0;
+    int Smax = 0;                      // sentence capacity per (b)
+    int off_stride = 0;                // row stride of `off` (= L + 1)
+    std::vector<int32_t> S_host;       // [B]
+    int32_t* off = nullptr;            // device [B][L+1]
+    int32_t* S_dev = nullptr;          // device [B]
+    int32_t* bset = nullptr;           // device [kMaxBoundary]
+    int n_bset = 0;
+    int nsplit = 0;                    // attention splits per (b, g)
+    int chunk = 0;                     // tokens per attention split
+
+    std::vector<skv::LayerState> layer;
+
+    // kernel profiler: (kind, start, stop) event triples awaiting a read
+    bool profiling = false;
+    struct ProfRec { int kind; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_event = nullptr;
+};
+
+namespace skv {
+
+// ---- kernel launchers (each returns the cudaError_t of the launch) ----
+
+// P1: sentence offsets for B prompts.  tokens [B][L]; off [B][Smax_cap+1]; S [B].
+cudaError_t launch_segment(const int32_t* tokens, int B, int L, const int32_t* bset, int nb, int tau,
+                           int32_t* off, int off_stride, int32_t* S, cudaStream_t st);
+
+// P2: E = bf16(mean of member keys).  K [B][G][L][d]; off [B][Smax+1]; E [B][G][Smax][d].
+cudaError_t launch_compress(const __nv_bfloat16* K, int B, int G, int L, int d, const int32_t* off,
+                            int off_stride, const int32_t* S, int Smax, __nv_bfloat16* E, cudaStream_t st);
+
+// D1: scores [B][G][Smax] of qt_g against every sentence embedding.
+cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t* cnt, const __nv_bfloat16* E,
+                         const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores,
+                         cudaStream_t st);
+
+// D2: budgeted selection + Q_s state update (Sq += q or reset).
+cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B, int G, int grp,
+                          int d, int Smax, int tau, const __nv_bfloat16* q, const int32_t* input_token,
+                          const int32_t* bset, int nb, float* Sq, int32_t* cnt, int32_t* sel_ids,
+                          int32_t* sel_tokoff, int32_t* sel_count, int32_t* out_ids, int32_t* out_count,
+                          int32_t* out_tokens, cudaStream_t st);
+
+// D3 + D4: split-K attention over the selected sentences' tokens (device residency).
+cudaError_t launch_attend(const __nv_bfloat16* q, const __nv_bfloat16* K, const __nv_bfloat16* V, int B, int G,
+                          int grp, int d, int L, const int32_t* off, int off_stride, const int32_t* sel_ids,
+                          const int32_t* sel_tokoff, const int32_t* sel_count, int tau, int chunk, int nsplit,
+                          float* o_part, float* ml_part, uint32_t* done, float* out, cudaStream_t st);
+
+int attend_chunk_tokens(int d);
+
+}  // namespace skv

@@ -121,3 +121,38 @@ def queries(seed: int, layer: int, step: int, target: np.ndarray, Hq: int, G: in
         for h in range(Hq):
             q[b, h] = c[h // grp, target[b]] + rng.standard_normal(d, dtype=np.float32)
     return f32_to_bf16_bits(q)
+
+
+# ------------------------------------------------------------- GPU-side generation (bench)
+
+
+def kv_layer_torch(seed: int, layer: int, topics, G: int, d: int, device="cuda"):
+    """Same recipe as kv_layer, drawn on the GPU with a seeded torch generator (for the
+    full-size bench configs where numpy generation would take minutes).  topics: int64/int32
+    tensor [B][L] on `device`.  Returns bf16 K, V [B][G][L][d]."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed((seed * 1_000_003 + layer * 7919 + 0x4B56) & 0x7FFFFFFFFFFFFFFF)
+    B, L = topics.shape
+    c = torch.randn((G, N_TOPICS, d), generator=gen, device=device, dtype=torch.float32)
+    K = torch.empty((B, G, L, d), dtype=torch.bfloat16, device=device)
+    V = torch.empty((B, G, L, d), dtype=torch.bfloat16, device=device)
+    tl = topics.long()
+    for b in range(B):
+        for g in range(G):
+            noise = torch.randn((L, d), generator=gen, device=device, dtype=torch.float32)
+            K[b, g] = (c[g][tl[b]] + noise).to(torch.bfloat16)
+            V[b, g] = torch.randn((L, d), generator=gen, device=device, dtype=torch.float32).to(torch.bfloat16)
+    return K, V, c
+
+
+def queries_torch(gen, centroids_g, target, Hq: int, G: int, d: int):
+    """q_t bf16 [B][Hq][d] = centroid of the target topic (per KV head group) + N(0, 1)."""
+    import torch
+
+    grp = Hq // G
+    B = target.shape[0]
+    c = centroids_g[:, target.long(), :]                  # [G][B][d]
+    c = c.permute(1, 0, 2).repeat_interleave(grp, dim=1)  # [B][Hq][d]
+    return (c + torch.randn((B, Hq, d), generator=gen, device=c.device)).to(torch.bfloat16)

@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (north_star): segmentation offsets, sentence embeddings, scores and selected
+sentence ids / counts / token counts bit-exact; attention output max-abs <= 2e-3 vs the fp64
+oracle on the same selection.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.gpu_harness import ATOL, from_bits, make_case, run_parity, to_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _skv(B, M, Hq, G, d, L, tau, **kw):
+    import paper_2504_00970_b200 as skvlib
+
+    return skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L,
+                             token_budget=tau, **kw)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("Hq", [8, 2])
+def test_tiny_config_full_parity(cuda_device, seed, Hq):
+    """configs[0]: 1 layer, 2 KV heads, d=64, 4K tokens, ~20-token sentences, tau=256, B=1
+    (Hq=8 -> GQA grp=4; Hq=2 -> MHA)."""
+    B, M, G, d, L, tau, steps = 1, 1, 2, 64, 4096, 256, 40
+    toks, _, Ks, Vs, qs, script = make_case(seed, B, M, Hq, G, d, L, tau, steps, median=20.0)
+    skv = _skv(B, M, Hq, G, d, L, tau)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+    assert st["steps"] == steps and st["max_abs"] <= ATOL
+
+
+def test_multi_sequence_multi_layer_gqa8(cuda_device):
+    """B=3 prompts of different sentence counts, 2 layers, grp=8 (70B-style), d=128, ragged L."""
+    B, M, Hq, G, d, L, tau, steps = 3, 2, 16, 2, 128, 5003, 512, 12
+    toks, _, Ks, Vs, qs, script = make_case(11, B, M, Hq, G, d, L, tau, steps, median=25.0)
+    skv = _skv(B, M, Hq, G, d, L, tau)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+
+
+def test_llama8b_32k_config(cuda_device):
+    """configs[1] shapes (8 KV / 32 Q heads, d=128, 32K context, tau=1024, B=1) on 2 of the 32
+    layers, every (b, g) unit, 6 decode steps."""
+    B, M, Hq, G, d, L, tau, steps = 1, 2, 32, 8, 128, 32768, 1024, 6
+    toks, _, Ks, Vs, qs, script = make_case(5, B, M, Hq, G, d, L, tau, steps, median=25.0)
+    skv = _skv(B, 32, Hq, G, d, L, tau)  # ctx for all 32 layers; 2 exercised
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+
+
+def test_budget_at_least_context_equals_full_attention(cuda_device):
+    """tau >= L: every sentence is selected and Eq. 3 equals full attention (O-FULL)."""
+    B, M, Hq, G, d, L, tau = 2, 1, 8, 2, 128, 1500, 1500
+    toks, _, Ks, Vs, qs, script = make_case(3, B, M, Hq, G, d, L, tau, 3, median=25.0)
+    skv = _skv(B, M, Hq, G, d, L, tau)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+    assert all(t == L for t in st["sel_tokens"])
+    # and against torch's fp64 SDPA over all L tokens
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=cuda_device)
+    qd = from_bits(qs[-1][0], cuda_device)
+    skv.decode_attend(0, qd, out)
+    K = torch.from_numpy(synth.bf16_bits_to_f32(Ks[0]).astype(np.float64))
+    V = torch.from_numpy(synth.bf16_bits_to_f32(Vs[0]).astype(np.float64))
+    q = torch.from_numpy(synth.bf16_bits_to_f32(qs[-1][0]).astype(np.float64))
+    grp = Hq // G
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        q.view(B, G, grp, d), K, V)  # [B][G][grp][d]
+    assert float((out.cpu().double().view(B, G, grp, d) - ref).abs().max()) <= ATOL
+
+
+# --------------------------------------------------------------------------- edge cases
+
+
+def _custom_case(device, toks, K_bits, V_bits, q_list, script, tau, Hq, G, d, bset=synth.BOUNDARY_IDS):
+    B, L = toks.shape
+    skv = _skv(B, 1, Hq, G, d, L, tau)
+    orc = oracle.Oracle(toks, bset, tau, 1, Hq, G, d)
+    return run_parity(skv, orc, toks, [K_bits], [V_bits], [[q] for q in q_list], script, bset, device)
+
+
+def test_ties_duplicated_sentences_and_zero_query(cuda_device):
+    """Tie stress: duplicated sentences (identical E -> equal scores, lowest index first) and
+    q = 0 (all scores +0 -> document order)."""
+    B, Hq, G, d, L, tau = 1, 4, 1, 64, 2000, 200
+    toks, topics = synth.prompts(21, B, L, median=20.0)
+    K, V = synth.kv_layer(21, 0, topics, G, d)
+    off = oracle.segment(toks[0], synth.BOUNDARY_IDS, tau)
+    lens = np.diff(off)
+    # copy sentence 3's keys over every later sentence of the same length
+    for s in range(4, len(lens)):
+        if lens[s] == lens[3]:
+            K[0, 0, off[s]:off[s + 1]] = K[0, 0, off[3]:off[4]]
+    rng = np.random.default_rng(0)
+    e3 = synth.bf16_bits_to_f32(K[0, 0, off[3]:off[4]]).mean(0)
+    q_dup = synth.f32_to_bf16_bits(np.tile(e3 * 3, (B, Hq, 1)))
+    q_zero = np.zeros((B, Hq, d), np.uint16)
+    q_rand = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, d)).astype(np.float32))
+    script = np.array([[500], [13], [500], [500]], np.int32)  # reset after step 1
+    _custom_case(cuda_device, toks, K, V, [q_dup, q_zero, q_zero, q_rand], script, tau, Hq, G, d)
+
+
+def test_all_equal_keys(cuda_device):
+    B, Hq, G, d, L, tau = 2, 8, 2, 128, 777, 64
+    toks, _ = synth.prompts(4, B, L, median=20.0)
+    k = synth.f32_to_bf16_bits(np.random.default_rng(1).standard_normal(d).astype(np.float32))
+    K = np.broadcast_to(k, (B, G, L, d)).copy()
+    V = synth.f32_to_bf16_bits(np.random.default_rng(2).standard_normal((B, G, L, d)).astype(np.float32))
+    qs = [synth.f32_to_bf16_bits(np.random.default_rng(3 + i).standard_normal((B, Hq, d)).astype(np.float32))
+          for i in range(3)]
+    _custom_case(cuda_device, toks, K, V, qs, np.full((3, B), 300, np.int32), tau, Hq, G, d)
+
+
+@pytest.mark.parametrize("L,tau", [(1, 16), (5, 16), (64, 64), (65, 64), (300, 64), (1000, 1)])
+def test_tau_cap_and_tiny_prompts(cuda_device, L, tau):
+    """Sentences of exactly tau and tau+1 tokens (tau-cap, A5), L = 1, a single sentence, tau = 1."""
+    B, Hq, G, d = 1, 4, 1, 64
+    rng = np.random.default_rng(L * 7 + tau)
+    toks = rng.integers(256, 128000, size=(B, L)).astype(np.int32)
+    # boundaries at a few fixed places so that runs of exactly tau and tau+1 occur
+    for p in (tau - 1, 2 * tau, 3 * tau + 1):
+        if p < L:
+            toks[0, p] = synth.BOUNDARY_IDS[0]
+    K = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    V = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    qs = [synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, d)).astype(np.float32)) for _ in range(3)]
+    _custom_case(cuda_device, toks, K, V, qs, np.full((3, B), 300, np.int32), tau, Hq, G, d)
+
+
+def test_many_one_token_sentences(cuda_device):
+    """Every token a boundary: S = L one-token sentences (max sentence count)."""
+    B, Hq, G, d, L, tau = 1, 8, 2, 64, 3000, 100
+    toks = np.full((B, L), synth.BOUNDARY_IDS[1], np.int32)
+    rng = np.random.default_rng(9)
+    K = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    V = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    qs = [synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, d)).astype(np.float32)) for _ in range(2)]
+    _custom_case(cuda_device, toks, K, V, qs, np.full((2, B), 300, np.int32), tau, Hq, G, d)
+
+
+def test_deterministic_run_to_run(cuda_device):
+    B, M, Hq, G, d, L, tau, steps = 2, 1, 8, 2, 128, 6000, 512, 5
+    toks, _, Ks, Vs, qs, script = make_case(8, B, M, Hq, G, d, L, tau, steps, median=25.0)
+    outs = []
+    for _ in range(2):
+        skv = _skv(B, M, Hq, G, d, L, tau)
+        tok_dev = torch.from_numpy(toks).to(cuda_device)
+        skv.prefill_compress(0, from_bits(Ks[0], cuda_device), from_bits(Vs[0], cuda_device), tok_dev,
+                             synth.BOUNDARY_IDS)
+        ids = torch.empty((B, G, tau), dtype=torch.int32, device=cuda_device)
+        out = torch.empty((B, Hq, d), dtype=torch.float32, device=cuda_device)
+        res = []
+        for s in range(steps):
+            qd = from_bits(qs[s][0], cuda_device)
+            skv.decode_select(0, qd, torch.from_numpy(script[s]).to(cuda_device), ids)
+            skv.decode_attend(0, qd, out)
+            res.append((ids.cpu().numpy().copy(), out.cpu().numpy().copy()))
+        outs.append(res)
+    for (i1, o1), (i2, o2) in zip(*outs):
+        assert np.array_equal(i1, i2) and np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
