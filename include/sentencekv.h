@@ -149,6 +149,23 @@ skv_status sentencekv_decode_select(skv_ctx* ctx, int32_t layer, const void* q, 
 skv_status sentencekv_decode_attend(skv_ctx* ctx, int32_t layer, const void* q, float* out,
                                     skv_stream_t stream);
 
+/*
+ * Decode, per layer per step: D1 + D2 + D3 + D4 in one call (Alg. 1 lines 14-19).
+ * Same results as sentencekv_decode_select followed by sentencekv_decode_attend (same arithmetic,
+ * bit-identical selection).  Default: the score, select and attend kernels back to back.  With
+ * SKV_FUSED=1 in the environment the selection and the attention run fused in one thread-block
+ * cluster per (sequence, KV head), with the K/V runs selected at the previous step prefetched into
+ * L2 while the selection is computed (falls back to the unfused kernels when S > 32768 or
+ * tau > 8192).
+ *
+ * q, input_token  as in sentencekv_decode_select
+ * out             device fp32 [batch_count][kv_head_count*grp][d]
+ * sel_ids, sel_count, sel_tokens  optional outputs, as in sentencekv_decode_select (NULL allowed)
+ */
+skv_status sentencekv_decode_step(skv_ctx* ctx, int32_t layer, const void* q, const int32_t* input_token,
+                                  float* out, int32_t* sel_ids, int32_t* sel_count, int32_t* sel_tokens,
+                                  skv_stream_t stream);
+
 /* ---- introspection (tests, bench; not on the per-token path) ---- */
 
 /* Sentence counts of the current prompt: S_out host int32 [batch_count]. */
@@ -179,7 +196,8 @@ typedef enum {
     SKV_K_SCORE = 2,   /* D1 */
     SKV_K_SELECT = 3,  /* D2 */
     SKV_K_ATTEND = 4,  /* D3 + D4 */
-    SKV_K_COUNT = 5
+    SKV_K_FUSED = 5,   /* D2 + D3 + D4 fused (decode_step) */
+    SKV_K_COUNT = 6
 } skv_kernel_kind;
 
 skv_status sentencekv_set_profiling(skv_ctx* ctx, int32_t on);

@@ -20,10 +20,11 @@ import torch
 __all__ = [
     "SkvConfig", "SkvError", "SentenceKV", "lib", "LIB_PATH",
     "SKV_KV_DEVICE", "SKV_KV_HOST", "sentencekv_config_default", "sentencekv_create", "sentencekv_destroy",
-    "sentencekv_prefill_compress", "sentencekv_decode_select", "sentencekv_decode_attend", "sentencekv_sync",
+    "sentencekv_prefill_compress", "sentencekv_decode_select", "sentencekv_decode_attend", "sentencekv_decode_step",
+    "sentencekv_sync",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsentencekv.so")
+LIB_PATH = os.environ.get("SKV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsentencekv.so")
 
 SKV_OK, SKV_ERR_INVALID_ARGUMENT, SKV_ERR_STATE, SKV_ERR_UNSUPPORTED, SKV_ERR_CUDA, SKV_ERR_OUT_OF_MEMORY = range(6)
 SKV_KV_DEVICE, SKV_KV_HOST = 0, 1
@@ -64,6 +65,7 @@ def _load():
         "sentencekv_prefill_compress": (i32, [P, i32, P, i32, P, i32, P, P, f32, i32, P]),
         "sentencekv_decode_select": (i32, [P, i32, P, P, P, P, P, P]),
         "sentencekv_decode_attend": (i32, [P, i32, P, P, P]),
+        "sentencekv_decode_step": (i32, [P, i32, P, P, P, P, P, P, P]),
         "sentencekv_sentence_counts": (i32, [P, P]),
         "sentencekv_sentence_capacity": (i32, [P]),
         "sentencekv_copy_offsets": (i32, [P, P, P]),
@@ -155,6 +157,13 @@ def sentencekv_decode_attend(ctx, layer, q, out, stream=None) -> None:
     _check(ctx, lib.sentencekv_decode_attend(ctx, int(layer), _ptr(q), _ptr(out), _stream(stream)))
 
 
+def sentencekv_decode_step(ctx, layer, q, input_token, out, sel_ids=None, sel_count=None, sel_tokens=None,
+                           stream=None) -> None:
+    """D1 + D2 + D3 + D4 in one call (fused select + attend; same results as select then attend)."""
+    _check(ctx, lib.sentencekv_decode_step(ctx, int(layer), _ptr(q), _ptr(input_token), _ptr(out), _ptr(sel_ids),
+                                           _ptr(sel_count), _ptr(sel_tokens), _stream(stream)))
+
+
 # ------------------------------------------------------------------ convenience wrapper
 
 
@@ -200,6 +209,9 @@ class SentenceKV:
     def decode_attend(self, layer, q, out, stream=None):
         sentencekv_decode_attend(self.ctx, layer, q, out, stream)
 
+    def decode_step(self, layer, q, input_token, out, sel_ids=None, sel_count=None, sel_tokens=None, stream=None):
+        sentencekv_decode_step(self.ctx, layer, q, input_token, out, sel_ids, sel_count, sel_tokens, stream)
+
     def sync(self):
         sentencekv_sync(self.ctx)
 
@@ -233,14 +245,14 @@ class SentenceKV:
     def launch_count(self) -> int:
         return int(lib.sentencekv_launch_count(self.ctx))
 
-    KERNELS = ("segment", "compress", "score", "select", "attend")
+    KERNELS = ("segment", "compress", "score", "select", "attend", "fused")
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} of the profiled launches since the last read."""
-        ms = (ctypes.c_double * 5)()
-        n = (ctypes.c_int64 * 5)()
+        ms = (ctypes.c_double * 6)()
+        n = (ctypes.c_int64 * 6)()
         _check(self.ctx, lib.sentencekv_profile_read(self.ctx, ms, n))
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}

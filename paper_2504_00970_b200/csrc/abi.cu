@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -74,10 +75,8 @@ void free_prompt_buffers(skv_ctx* c) {
         dfree(ls.scores);
         dfree(ls.sel_ids);
         dfree(ls.sel_tokoff);
+        dfree(ls.sel_src);
         dfree(ls.sel_count);
-        dfree(ls.o_part);
-        dfree(ls.ml_part);
-        dfree(ls.done);
         ls.prefilled = false;
         ls.selected = false;
         ls.K = ls.V = nullptr;
@@ -117,6 +116,22 @@ void prof_end(skv_ctx* c, int kind, cudaEvent_t a, cudaStream_t st) {
 
 }  // namespace
 
+bool skv::fused_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_FUSED");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+bool skv::pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 SKV_API void sentencekv_config_default(skv_config* cfg) {
     if (!cfg) return;
     std::memset(cfg, 0, sizeof(*cfg));
@@ -151,8 +166,6 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
     c->Hq = c->G * grp;
     c->d = cfg.head_dim;
     c->tau = cfg.token_budget;
-    c->chunk = skv::attend_chunk_tokens(c->d);
-    c->nsplit = (c->tau + c->chunk - 1) / c->chunk;
     c->layer.resize(cfg.layers);
     c->S_host.assign(c->B, 0);
 
@@ -211,17 +224,14 @@ SKV_API skv_status sentencekv_sync(skv_ctx* c) {
 
 // (Re)allocates the sentence-dependent buffers of every layer for a prompt with capacity Smax.
 static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
-    const size_t B = c->B, G = c->G, d = c->d, tau = c->tau, ns = c->nsplit, grp = c->grp;
+    const size_t B = c->B, G = c->G, d = c->d, tau = c->tau;
     for (auto& ls : c->layer) {
         SKV_CUDA(c, dalloc(&ls.E, B * G * Smax * d));
         SKV_CUDA(c, dalloc(&ls.scores, B * G * Smax));
         SKV_CUDA(c, dalloc(&ls.sel_ids, B * G * tau));
         SKV_CUDA(c, dalloc(&ls.sel_tokoff, B * G * (tau + 1)));
+        SKV_CUDA(c, dalloc(&ls.sel_src, B * G * tau));
         SKV_CUDA(c, dalloc(&ls.sel_count, B * G));
-        SKV_CUDA(c, dalloc(&ls.o_part, B * G * ns * grp * d));
-        SKV_CUDA(c, dalloc(&ls.ml_part, B * G * ns * grp * 2));
-        SKV_CUDA(c, dalloc(&ls.done, B * G));
-        SKV_CUDA(c, cudaMemset(ls.done, 0, sizeof(uint32_t) * B * G));
     }
     c->Smax = Smax;
     return SKV_OK;
@@ -271,7 +281,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         if (Smax > c->Smax || !c->layer[0].E) {
             for (auto& ls : c->layer) {
                 dfree(ls.E); dfree(ls.scores); dfree(ls.sel_ids); dfree(ls.sel_tokoff);
-                dfree(ls.sel_count); dfree(ls.o_part); dfree(ls.ml_part); dfree(ls.done);
+                dfree(ls.sel_src); dfree(ls.sel_count);
             }
             skv_status s = alloc_prompt_buffers(c, Smax);
             if (s != SKV_OK) return s;
@@ -279,6 +289,8 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         for (auto& ls : c->layer) {
             ls.prefilled = false;
             ls.selected = false;
+            // no previous selection: the fused kernel's L2 prefetch of it is then empty
+            SKV_CUDA(c, cudaMemsetAsync(ls.sel_count, 0, sizeof(int32_t) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B, st));
         }
@@ -317,8 +329,39 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
     pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax,
                                    c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt, ls.sel_ids,
-                                   ls.sel_tokoff, ls.sel_count, sel_ids, sel_count, sel_tokens, st));
+                                   ls.sel_tokoff, ls.sel_src, ls.sel_count, sel_ids, sel_count, sel_tokens, st));
     prof_end(c, SKV_K_SELECT, pa, st);
+    c->launches += 2;
+    ls.selected = true;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void* q, const int32_t* input_token,
+                                          float* out, int32_t* sel_ids, int32_t* sel_count, int32_t* sel_tokens,
+                                          skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (!ls.prefilled) return fail(c, SKV_ERR_STATE, "decode_step before prefill of layer %d", layer);
+    if (!q || !input_token || !out) return fail(c, SKV_ERR_INVALID_ARGUMENT, "q / input_token / out is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    DeviceGuard dg(c->cfg.device);
+    const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    if (!skv::fused_enabled() || !skv::fused_supported(c->d, c->grp, c->Smax, c->tau)) {
+        skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
+        if (s != SKV_OK) return s;
+        return sentencekv_decode_attend(c, layer, q, out, stream_);
+    }
+    cudaEvent_t pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
+    prof_end(c, SKV_K_SCORE, pa, st);
+    pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_fused_select_attend(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d,
+                                                c->Smax, c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt,
+                                                ls.K, ls.V, c->L, ls.sel_ids, ls.sel_tokoff, ls.sel_src,
+                                                ls.sel_count, sel_ids, sel_count, sel_tokens, out, st));
+    prof_end(c, SKV_K_FUSED, pa, st);
     c->launches += 2;
     ls.selected = true;
     return SKV_OK;
@@ -337,8 +380,7 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
     DeviceGuard dg(c->cfg.device);
     cudaEvent_t pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_attend(static_cast<const __nv_bfloat16*>(q), ls.K, ls.V, c->B, c->G, c->grp, c->d, c->L,
-                                   c->off, c->off_stride, ls.sel_ids, ls.sel_tokoff, ls.sel_count, c->tau, c->chunk,
-                                   c->nsplit, ls.o_part, ls.ml_part, ls.done, out, st));
+                                   ls.sel_src, ls.sel_tokoff, ls.sel_count, c->tau, out, st));
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;
     return SKV_OK;

@@ -12,133 +12,224 @@
 
 namespace skv {
 
+SKV_TRACE_DEFINE(select)
+
 // ------------------------------------------------------------------------------ D1 scoring
 //
-// Grid (splits, G, B); each CTA scores a contiguous range of sentences of one (b, g) unit.
-// Every CTA forms qt_g = sum_h qbar_h with qbar_h = (Sq_h + q_h) / (cnt + 1) (the appended,
-// not yet stored, Q_s of this step; the state itself is written by the select kernel, which
-// runs after all scoring CTAs).  Then D/8 lanes per sentence: lane l holds qt[8l..8l+7] in
-// registers and reads one 16-byte chunk of the sentence embedding; the fp32 dot follows the
+// Grid (splits, G, B); each CTA scores a contiguous range of sentences of one (b, g) unit.  The
+// range's embeddings are contiguous in HBM ([B][G][Smax][d]), so they stream into shared memory
+// as 16 KB tiles by single bulk async copies (TMA engine) through a kScStages-deep mbarrier
+// pipeline; the first tiles are in flight while the CTA forms the group query
+// qt_g = sum_h qbar_h, qbar_h = (Sq_h + q_h) / (cnt + 1) (the appended, not yet stored, Q_s of
+// this step; the state itself is written by the select kernel, which runs after all scoring
+// CTAs).  D/8 lanes per sentence: lane l holds qt[8l..8l+7] in registers and reads one 16-byte
+// chunk of the sentence row from shared memory (conflict-free); the fp32 dot follows the
 // canonical order (mul, 7 fma, then xor-butterfly adds whose lane-0 result equals the tree of
 // A23).  E is read exactly once per step: the HBM-bound part of decode.
-template <int D>
-__global__ void __launch_bounds__(256) score_kernel(const __nv_bfloat16* __restrict__ q,
-                                                    const float* __restrict__ Sq, const int32_t* __restrict__ cnt,
-                                                    const __nv_bfloat16* __restrict__ E,
-                                                    const int32_t* __restrict__ S, int G, int grp, int Smax,
-                                                    int chunk, float* __restrict__ scores) {
-    constexpr int LPS = D / 8;
-    constexpr int GPW = 32 / LPS;  // sentence groups per warp
-    constexpr int U = 4;           // sentences in flight per lane group
+constexpr int kScThreads = 256;
+constexpr int kScTileBytes = 16384;
+constexpr int kScStages = 4;
+
+template <int D, int GRP>
+__global__ void __launch_bounds__(kScThreads) score_kernel(const __nv_bfloat16* __restrict__ q,
+                                                           const float* __restrict__ Sq,
+                                                           const int32_t* __restrict__ cnt,
+                                                           const __nv_bfloat16* __restrict__ E,
+                                                           const int32_t* __restrict__ S, int G, int Smax,
+                                                           int chunk, float* __restrict__ scores) {
+    constexpr int LPS = D / 8;                   // lanes per sentence
+    constexpr int GPW = 32 / LPS;                // sentences per warp step
+    constexpr int TS = kScTileBytes / (D * 2);   // sentences per tile (64 or 128)
+    constexpr int NW = kScThreads / 32;
+    static_assert(TS % (NW * GPW) == 0, "tile must split evenly over the warps");
+    extern __shared__ __align__(128) unsigned char sc_smem[];
+    __nv_bfloat16* tiles = reinterpret_cast<__nv_bfloat16*>(sc_smem);  // [kScStages][TS*D]
+    __shared__ uint64_t bar[kScStages];
     __shared__ float qt[D];
+
     const int b = blockIdx.z, g = blockIdx.y;
+    pdl_wait();
     const int Sb = S[b];
     const int s0 = blockIdx.x * chunk;
     if (s0 >= Sb) return;
     const int s1 = min(Sb, s0 + chunk);
-    const int Hq = G * grp;
+    const int ntiles = (s1 - s0 + TS - 1) / TS;
+    const int Hq = G * GRP;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const __nv_bfloat16* Eu = E + ((size_t)(b * G + g) * Smax) * D;
+    SKV_TRACE_POINT(24);
 
-    const float c = (float)(cnt[b] + 1);
-    for (int j = threadIdx.x; j < D; j += blockDim.x) {
-        float acc = 0.0f;
-        for (int h = 0; h < grp; ++h) {
-            const size_t idx = ((size_t)b * Hq + g * grp + h) * D + j;
-            const float v = __fadd_rn(Sq[idx], __bfloat162float(q[idx]));
-            const float qb = __fdiv_rn(v, c);
-            acc = (h == 0) ? qb : __fadd_rn(acc, qb);
+    if (tid == 0) {
+        for (int i = 0; i < kScStages; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < kScStages && i < ntiles; ++i) {
+            const int ts = s0 + i * TS, n = min(TS, s1 - ts);
+            mbar_arrive_expect_tx(&bar[i], (uint32_t)(n * D * 2));
+            bulk_g2s(tiles + (size_t)i * TS * D, Eu + (size_t)ts * D, (uint32_t)(n * D * 2), &bar[i]);
         }
-        qt[j] = acc;
+    }
+    // group query of this step (loads batched, canonical order: qbar_h by IEEE division, then
+    // ascending-h fp32 sum)
+    if (tid < D) {
+        const float c = (float)(cnt[b] + 1);
+        float sv[GRP], qv[GRP];
+#pragma unroll
+        for (int h = 0; h < GRP; ++h) {
+            const size_t idx = ((size_t)b * Hq + g * GRP + h) * D + tid;
+            sv[h] = Sq[idx];
+            qv[h] = __bfloat162float(q[idx]);
+        }
+        float acc = __fdiv_rn(__fadd_rn(sv[0], qv[0]), c);
+#pragma unroll
+        for (int h = 1; h < GRP; ++h) acc = __fadd_rn(acc, __fdiv_rn(__fadd_rn(sv[h], qv[h]), c));
+        qt[tid] = acc;
     }
     __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int l = lane % LPS, grp_in_warp = lane / LPS;
+    const int l = lane % LPS, gw = lane / LPS;
     float qr[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) qr[i] = qt[8 * l + i];
-
-    const uint4* Eu = reinterpret_cast<const uint4*>(E + (size_t)(b * G + g) * Smax * D);
     float* out = scores + (size_t)(b * G + g) * Smax;
-    const int nwarps = blockDim.x >> 5;
-    // warp-uniform loop: every lane takes part in every shuffle
-    for (int base = s0 + warp * GPW * U; base < s1; base += nwarps * GPW * U) {
-        uint4 e[U];
+    SKV_TRACE_POINT(25);
+
+    for (int it = 0; it < ntiles; ++it) {
+        const int st = it % kScStages;
+        mbar_wait(&bar[st], (it / kScStages) & 1);
+        if (it == 0) SKV_TRACE_POINT(26);
+        const __nv_bfloat16* tile = tiles + (size_t)st * TS * D;
+        const int ts = s0 + it * TS, n = min(TS, s1 - ts);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int s = base + u * GPW + grp_in_warp;
-            e[u] = s < s1 ? ld_stream(Eu + (size_t)s * LPS + l) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int j = 0; j < TS / (NW * GPW); ++j) {
+            const int r = (j * NW + warp) * GPW + gw;  // sentence row within the tile
             float f[8];
-            unpack8(e[u], f);
+            unpack8(*reinterpret_cast<const uint4*>(tile + (size_t)r * D + 8 * l), f);
             float p = __fmul_rn(qr[0], f[0]);
 #pragma unroll
             for (int i = 1; i < 8; ++i) p = __fmaf_rn(qr[i], f[i], p);
 #pragma unroll
             for (int o = LPS / 2; o >= 1; o >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
-            const int s = base + u * GPW + grp_in_warp;
-            if (l == 0 && s < s1) out[s] = p;
+            if (l == 0 && r < n) out[ts + r] = p;
+        }
+        __syncthreads();  // stage st fully read
+        if (it + 1 == ntiles) pdl_trigger();
+        if (tid == 0 && it + kScStages < ntiles) {
+            const int tn = s0 + (it + kScStages) * TS, nn = min(TS, s1 - tn);
+            mbar_arrive_expect_tx(&bar[st], (uint32_t)(nn * D * 2));
+            bulk_g2s(tiles + (size_t)st * TS * D, Eu + (size_t)tn * D, (uint32_t)(nn * D * 2), &bar[st]);
         }
     }
+}
+
+template <int D, int GRP>
+static cudaError_t launch_score_t(dim3 grid, int chunk, cudaStream_t st, const __nv_bfloat16* q, const float* Sq,
+                                  const int32_t* cnt, const __nv_bfloat16* E, const int32_t* S, int G, int Smax,
+                                  float* scores) {
+    const size_t smem = (size_t)kScStages * kScTileBytes;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(score_kernel<D, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(score_kernel<D, GRP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    return launch_pdl(score_kernel<D, GRP>, grid, dim3(kScThreads), smem, st, q, Sq, cnt, E, S, G, Smax, chunk,
+                      scores);
 }
 
 cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t* cnt, const __nv_bfloat16* E,
                          const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores,
                          cudaStream_t st) {
-    // Fill ~2 waves of 148 SMs: split each (b, g) unit's sentences into `splits` ranges.
+    // ~3 CTAs per SM: split each (b, g) unit's sentences into `splits` tile-aligned ranges.
+    const int TS = kScTileBytes / (d * 2);
     const int units = B * G;
-    int splits = (2 * kNumSMs + units - 1) / units;
+    int splits = (3 * kNumSMs + units - 1) / units;
     int chunk = (Smax + splits - 1) / splits;
-    chunk = max(64, (chunk + 63) / 64 * 64);
+    chunk = max(TS, (chunk + TS - 1) / TS * TS);
     splits = (Smax + chunk - 1) / chunk;
     dim3 grid(splits, G, B);
-    if (d == 128)
-        score_kernel<128><<<grid, 256, 0, st>>>(q, Sq, cnt, E, S, G, grp, Smax, chunk, scores);
-    else
-        score_kernel<64><<<grid, 256, 0, st>>>(q, Sq, cnt, E, S, G, grp, Smax, chunk, scores);
-    return cudaGetLastError();
+#define SKV_SC(DV, GV) return launch_score_t<DV, GV>(grid, chunk, st, q, Sq, cnt, E, S, G, Smax, scores)
+    if (d == 128) {
+        switch (grp) {
+            case 1: SKV_SC(128, 1);
+            case 2: SKV_SC(128, 2);
+            case 4: SKV_SC(128, 4);
+            case 8: SKV_SC(128, 8);
+        }
+    } else {
+        switch (grp) {
+            case 1: SKV_SC(64, 1);
+            case 2: SKV_SC(64, 2);
+            case 4: SKV_SC(64, 4);
+            case 8: SKV_SC(64, 8);
+        }
+    }
+#undef SKV_SC
+    return cudaErrorInvalidValue;
 }
 
 // ----------------------------------------------------------------------------- D2 selection
 //
 // One CTA (1024 threads) per (b, g).  The selection is the maximal prefix of the ranking by
-// key = (ordered(score), -index) whose token count fits tau (A13, A14).  Equivalently: find
-// the first sentence s* (in rank order) at which the cumulative length exceeds tau; select
-// every sentence ranked before it.  s* is found by a length-weighted radix select on the
-// 32-bit ordered score (digits 11/11/10 bits; each pass histograms the lengths of the
-// sentences whose key matches the prefix found so far, then one block scan locates the bin
-// where the cumulative length from the top crosses the remaining budget).  If that bin holds
-// one sentence it is s*; if the full 32-bit key is reached with several tied sentences, s* is
-// located among them in ascending index order (the tie rule) by an ordered block scan.  A last
-// ordered pass compacts the selected ids in ascending order with their token prefix sums.
+// key64 = (ordered(score) << 32) | (0xffffffff - index) whose token count fits tau (A13, A14):
+// find the first sentence s* in rank order at which the cumulative length exceeds tau, then
+// select every sentence with key64 > key64(s*) (all sentences if the total fits).
+//
+// s* is located by range refinement on the 32-bit ordered score key k:
+//   level: histogram (2048 bins, length-weighted and counted) of the sentences whose key lies
+//   in [lo, hi], bin = (k - lo) * 2048 / (hi - lo + 1) (monotone in k, so bins are key
+//   intervals); one block scan finds the bin where the cumulative length from the top crosses
+//   the remaining budget.  If that bin holds <= 1024 sentences they are ranked exactly by key64
+//   (one thread per candidate) and s* is found; otherwise [lo, hi] shrinks to the bin's key
+//   range and the level repeats (at most 3 times for 32-bit keys).  If lo == hi the remaining
+//   sentences tie on the score and s* is found in ascending index order (the tie rule) by one
+//   ordered block scan.
+// The ordered-key space is roughly logarithmic in the score, so bins are ~1/8 octave wide and
+// the histogram atomics see little contention.  A final ordered block scan compacts the selected
+// ids in ascending order with their token prefix sums.  Thread t owns the contiguous index range
+// [t*E, t*E+E); keys and lengths are cached in shared memory (S <= kSelSmemCap).
 //
 // The same CTA performs the deferred D1 state update of its query heads: Sq += q_t, or Sq = 0
 // when the step's input token is a boundary (A11); cnt is updated by the g == 0 CTA.
 constexpr int kSelThreads = 1024;
 constexpr int kBins = 2048;
+constexpr int kSelSmemCap = 32768;
+constexpr int kCandCap = kSelThreads;
 
+__device__ __forceinline__ unsigned long long key64_of(uint32_t k, int s) {
+    return ((unsigned long long)k << 32) | (unsigned long long)(0xffffffffu - (uint32_t)s);
+}
+
+template <bool SMEM>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ off, int off_stride,
     const int32_t* __restrict__ S, int G, int grp, int D, int Smax, int tau, const __nv_bfloat16* __restrict__ q,
     const int32_t* __restrict__ input_token, const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq,
     int32_t* __restrict__ cnt, int32_t* __restrict__ sel_ids, int32_t* __restrict__ sel_tokoff,
-    int32_t* __restrict__ sel_count, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
-    int32_t* __restrict__ out_tokens) {
+    int32_t* __restrict__ sel_src, int32_t* __restrict__ sel_count, int32_t* __restrict__ out_ids,
+    int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens) {
     __shared__ uint32_t hw[kBins];  // length-weighted histogram
     __shared__ uint32_t hc[kBins];  // count histogram
+    __shared__ unsigned long long cand_key[kCandCap];
+    __shared__ uint32_t cand_len[kCandCap];
     __shared__ uint32_t ws32[32];
     __shared__ unsigned long long ws64[32];
-    __shared__ uint32_t sh_bin, sh_rem, sh_cnt;
-    __shared__ int sh_found;
+    __shared__ uint32_t sh_bin, sh_rem, sh_cnt, sh_lo, sh_hi, sh_ncand;
+    __shared__ unsigned long long sh_thr;
+    __shared__ int sh_all;
+    extern __shared__ __align__(16) unsigned char sel_smem[];
+    uint32_t* skey = reinterpret_cast<uint32_t*>(sel_smem);                    // [Smax]
+    uint16_t* slen = reinterpret_cast<uint16_t*>(sel_smem + 4 * (size_t)Smax);  // [Smax] (len <= tau <= 65535)
 
     const int g = blockIdx.x, b = blockIdx.y;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    pdl_wait();
     const int Sb = S[b];
     const float* sc = scores + (size_t)(b * G + g) * Smax;
     const int32_t* o = off + (size_t)b * off_stride;
     const int Hq = G * grp;
 
+    SKV_TRACE_POINT(0);
     // ---- deferred D1 state update (Eq. 2 sentence cache; reset at a boundary input) ----
     {
         const bool reset = in_set(input_token[b], bset, nb);
@@ -147,121 +238,216 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
             Sq[base + i] = reset ? 0.0f : __fadd_rn(Sq[base + i], __bfloat162float(q[base + i]));
         if (g == 0 && tid == 0) cnt[b] = reset ? 0 : cnt[b] + 1;
     }
+    SKV_TRACE_POINT(1);
 
-    // ---- radix select for the crossing key ----
-    uint32_t prefix = 0, mask = 0, rem = (uint32_t)tau;
-    bool all_fit = false, resolved = false;
-    const int shifts[3] = {21, 10, 0};
-    const int widths[3] = {11, 11, 10};
-    for (int pass = 0; pass < 3 && !resolved; ++pass) {
-        const int shift = shifts[pass];
-        const uint32_t dmask = (1u << widths[pass]) - 1u;
-        for (int i = tid; i < kBins; i += blockDim.x) hw[i] = hc[i] = 0u;
-        __syncthreads();
-        // warp-uniform trip count; lanes whose sentence falls in the same bin are aggregated
-        // (match_any + reduce) so concentrated score distributions do not serialise on one
-        // shared-memory address.
-        for (int s0 = 0; s0 < Sb; s0 += blockDim.x) {
-            const int s = s0 + tid;
-            uint32_t bin = 0xffffffffu, n = 0;
-            if (s < Sb) {
-                const uint32_t k = ordered_key(sc[s]);
-                if ((k & mask) == prefix) {
-                    bin = (k >> shift) & dmask;
-                    n = (uint32_t)(o[s + 1] - o[s]);
-                }
+    if (tid == 0) {
+        sh_lo = 0xffffffffu;
+        sh_hi = 0u;
+        sh_ncand = 0u;
+        sh_all = 0;
+    }
+    if (SMEM) {
+        // coalesced fill, loads batched before use
+        for (int s0 = 0; s0 < Sb; s0 += 4 * kSelThreads) {
+            float v[4];
+            int a[4], e[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int s = s0 + u * kSelThreads + tid;
+                v[u] = s < Sb ? sc[s] : 0.0f;
+                a[u] = s < Sb ? o[s] : 0;
+                e[u] = s < Sb ? o[s + 1] : 0;
             }
-            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-            if (bin != 0xffffffffu) {
-                const uint32_t wsum = __reduce_add_sync(peers, n);
-                if ((tid & 31) == __ffs(peers) - 1) {
-                    atomicAdd(&hw[bin], wsum);
-                    atomicAdd(&hc[bin], (uint32_t)__popc(peers));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int s = s0 + u * kSelThreads + tid;
+                if (s < Sb) {
+                    skey[s] = ordered_key(v[u]);
+                    slen[s] = (uint16_t)(e[u] - a[u]);
                 }
             }
         }
+    }
+    __syncthreads();
+    SKV_TRACE_POINT(2);
+    auto key_of = [&](int s) -> uint32_t { return SMEM ? skey[s] : ordered_key(sc[s]); };
+    auto len_of = [&](int s) -> uint32_t { return SMEM ? (uint32_t)slen[s] : (uint32_t)(o[s + 1] - o[s]); };
+    const int E = (Sb + kSelThreads - 1) / kSelThreads;
+    const int i0 = min(Sb, tid * E), i1 = min(Sb, i0 + E);
+
+    // key range of all sentences
+    {
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        for (int s = i0; s < i1; ++s) {
+            const uint32_t k = key_of(s);
+            mn = min(mn, k);
+            mx = max(mx, k);
+        }
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) {
+            atomicMin(&sh_lo, mn);
+            atomicMax(&sh_hi, mx);
+        }
+    }
+    __syncthreads();
+    SKV_TRACE_POINT(3);
+    uint32_t lo = sh_lo, hi = sh_hi, rem = (uint32_t)tau;
+    bool all_fit = false;
+    unsigned long long thr = 0;  // select key64 > thr
+    for (int level = 0;; ++level) {
+        if (lo == hi) {
+            // the remaining candidates all carry key lo: index order decides (tie rule)
+            uint32_t tw = 0;
+            for (int s = i0; s < i1; ++s)
+                if (key_of(s) == lo) tw += len_of(s);
+            uint32_t ttot;
+            const uint32_t before = block_incl_sum<uint32_t>(tw, ws32, &ttot) - tw;
+            if (level == 0 && ttot <= rem) {
+                all_fit = true;
+                break;
+            }
+            if (before <= rem && before + tw > rem) {
+                uint32_t acc = before;
+                for (int s = i0; s < i1; ++s) {
+                    if (key_of(s) != lo) continue;
+                    acc += len_of(s);
+                    if (acc > rem) {
+                        sh_thr = key64_of(lo, s);
+                        break;
+                    }
+                }
+            }
+            __syncthreads();
+            thr = sh_thr;
+            break;
+        }
+        // bin(k) = (k - lo) * kBins / span, as a 32.32 fixed-point multiply (monotone in k, < kBins);
+        // spans below kBins map one key per bin.
+        const unsigned long long span = (unsigned long long)(hi - lo) + 1ull;
+        const unsigned long long mul = span >= kBins ? ((unsigned long long)kBins << 32) / span : 0ull;
+        auto bin_of = [&](uint32_t k) -> uint32_t {
+            return mul ? (uint32_t)(((unsigned long long)(k - lo) * mul) >> 32) : (k - lo);
+        };
+        for (int i = tid; i < kBins; i += blockDim.x) hw[i] = hc[i] = 0u;
         __syncthreads();
+        for (int s = i0; s < i1; ++s) {
+            const uint32_t k = key_of(s);
+            if (k < lo || k > hi) continue;
+            const uint32_t bin = bin_of(k);
+            atomicAdd(&hw[bin], len_of(s));
+            atomicAdd(&hc[bin], 1u);
+        }
+        __syncthreads();
+        SKV_TRACE_POINT(4 + 4 * level);
         // thread t owns bins 2t (lower) and 2t+1 (upper); weight above t's pair = total - incl
         const uint32_t w_lo = hw[2 * tid], w_hi = hw[2 * tid + 1];
         uint32_t total;
         const uint32_t incl = block_incl_sum<uint32_t>(w_lo + w_hi, ws32, &total);
-        if (tid == 0) sh_found = 0;
-        __syncthreads();
-        if (pass == 0 && total <= rem) {
-            all_fit = true;  // every sentence fits the budget
+        if (level == 0 && total <= rem) {
+            all_fit = true;
             break;
         }
-        const uint32_t above = total - incl;  // weight of all bins above this pair
+        const uint32_t above = total - incl;
         if (above <= rem && above + w_hi > rem) {
             sh_bin = 2 * tid + 1;
             sh_rem = rem - above;
             sh_cnt = hc[2 * tid + 1];
-            sh_found = 1;
         } else if (above + w_hi <= rem && above + w_hi + w_lo > rem) {
             sh_bin = 2 * tid;
             sh_rem = rem - above - w_hi;
             sh_cnt = hc[2 * tid];
-            sh_found = 1;
+        }
+        if (tid == 0) {
+            sh_lo = 0xffffffffu;
+            sh_hi = 0u;
+            sh_ncand = 0u;
         }
         __syncthreads();
-        prefix |= sh_bin << shift;
-        mask |= dmask << shift;
+        SKV_TRACE_POINT(5 + 4 * level);
+        const uint32_t cb = sh_bin, ncb = sh_cnt;
         rem = sh_rem;
-        // A bin holding a single sentence: that sentence is s*; everything above is selected.
-        if (sh_cnt == 1u) resolved = true;
-        __syncthreads();
-    }
-    // Sentences with (key & mask) > prefix rank above the crossing range and are selected.
-    // Inside the range (key & mask) == prefix: if resolved, the range is {s*} (not selected);
-    // otherwise the range is a set of exact ties -> in index order, select while the cumulative
-    // tied length stays <= rem.
-    const bool ties = !all_fit && !resolved;
-
-    uint32_t tie_carry = 0;
-    unsigned long long carry = 0;  // (count << 32) | tokens of selected sentences so far
-    int32_t* ids = sel_ids + (size_t)(b * G + g) * tau;
-    int32_t* tokoff = sel_tokoff + (size_t)(b * G + g) * (tau + 1);
-    for (int base = 0; base < Sb; base += blockDim.x) {
-        const int s = base + tid;
-        const bool valid = s < Sb;
-        uint32_t k = 0, n = 0;
-        if (valid) {
-            k = ordered_key(sc[s]);
-            n = (uint32_t)(o[s + 1] - o[s]);
+        if (ncb <= (uint32_t)kCandCap) {
+            // exact rank of the crossing bin's sentences by key64
+            for (int s = i0; s < i1; ++s) {
+                const uint32_t k = key_of(s);
+                if (k < lo || k > hi) continue;
+                if (bin_of(k) != cb) continue;
+                const uint32_t pos = atomicAdd(&sh_ncand, 1u);
+                cand_key[pos] = key64_of(k, s);
+                cand_len[pos] = len_of(s);
+            }
+            __syncthreads();
+            SKV_TRACE_POINT(6 + 4 * level);
+            const int nc = (int)sh_ncand;
+            if (tid < nc) {
+                const unsigned long long mk = cand_key[tid];
+                uint32_t wabove = 0;
+                for (int c = 0; c < nc; ++c)
+                    if (cand_key[c] > mk) wabove += cand_len[c];
+                if (wabove <= rem && wabove + cand_len[tid] > rem) sh_thr = mk;
+            }
+            __syncthreads();
+            SKV_TRACE_POINT(7 + 4 * level);
+            thr = sh_thr;
+            break;
         }
-        bool sel;
-        if (all_fit) {
-            sel = valid;
-        } else {
-            const uint32_t km = k & mask;
-            sel = valid && km > prefix;
-            if (ties) {
-                const uint32_t tw = (valid && km == prefix) ? n : 0u;
-                uint32_t ttot;
-                const uint32_t tincl = block_incl_sum<uint32_t>(tw, ws32, &ttot) + tie_carry;
-                tie_carry += ttot;
-                if (tw > 0u && tincl <= rem) sel = true;
+        // too many candidates: narrow [lo, hi] to the crossing bin's key range and repeat
+        {
+            uint32_t mn = 0xffffffffu, mx = 0u;
+            for (int s = i0; s < i1; ++s) {
+                const uint32_t k = key_of(s);
+                if (k < lo || k > hi) continue;
+                if (bin_of(k) != cb) continue;
+                mn = min(mn, k);
+                mx = max(mx, k);
+            }
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) {
+                atomicMin(&sh_lo, mn);
+                atomicMax(&sh_hi, mx);
             }
         }
-        const unsigned long long v = sel ? ((1ull << 32) | (unsigned long long)n) : 0ull;
-        unsigned long long vtot;
-        const unsigned long long incl = block_incl_sum<unsigned long long>(v, ws64, &vtot) + carry;
-        if (sel) {
-            const unsigned long long excl = incl - v;
-            const int pos = (int)(excl >> 32);
-            ids[pos] = s;
-            tokoff[pos] = (int32_t)(excl & 0xffffffffull);
-        }
-        carry += vtot;
+        __syncthreads();
+        lo = sh_lo;
+        hi = sh_hi;
     }
-    const int count = (int)(carry >> 32);
-    const int ntok = (int)(carry & 0xffffffffull);
+
+    pdl_trigger();
+    // ---- ordered compaction of the selected sentences (ascending ids + token offsets) ----
+    unsigned long long mine = 0;
+    for (int s = i0; s < i1; ++s)
+        if (all_fit || key64_of(key_of(s), s) > thr) mine += (1ull << 32) | len_of(s);
+    unsigned long long tot;
+    SKV_TRACE_POINT(20);
+    const unsigned long long excl = block_incl_sum<unsigned long long>(mine, ws64, &tot) - mine;
+    SKV_TRACE_POINT(21);
+    int32_t* ids = sel_ids + (size_t)(b * G + g) * tau;
+    int32_t* tokoff = sel_tokoff + (size_t)(b * G + g) * (tau + 1);
+    int32_t* src = sel_src + (size_t)(b * G + g) * tau;
+    if (mine) {
+        int pos = (int)(excl >> 32);
+        uint32_t toff = (uint32_t)(excl & 0xffffffffull);
+        for (int s = i0; s < i1; ++s) {
+            if (all_fit || key64_of(key_of(s), s) > thr) {
+                ids[pos] = s;
+                tokoff[pos] = (int32_t)toff;
+                src[pos] = o[s];
+                ++pos;
+                toff += len_of(s);
+            }
+        }
+    }
+    const int count = (int)(tot >> 32);
+    const int ntok = (int)(tot & 0xffffffffull);
     if (tid == 0) {
         tokoff[count] = ntok;
         sel_count[b * G + g] = count;
         if (out_count) out_count[b * G + g] = count;
         if (out_tokens) out_tokens[b * G + g] = ntok;
     }
+    SKV_TRACE_POINT(22);
     if (out_ids) {
         __syncthreads();
         int32_t* oi = out_ids + (size_t)(b * G + g) * tau;
@@ -272,13 +458,25 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
                           int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
                           const int32_t* input_token, const int32_t* bset, int nb, float* Sq, int32_t* cnt,
-                          int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_count, int32_t* out_ids,
-                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st) {
+                          int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count,
+                          int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, cudaStream_t st) {
     dim3 grid(G, B);
-    select_kernel<<<grid, kSelThreads, 0, st>>>(scores, off, off_stride, S, G, grp, d, Smax, tau, q, input_token,
-                                                bset, nb, Sq, cnt, sel_ids, sel_tokoff, sel_count, out_ids,
-                                                out_count, out_tokens);
-    return cudaGetLastError();
+    if (Smax <= kSelSmemCap && tau <= 65535) {
+        const size_t smem = (size_t)Smax * 6 + 16;
+        static bool configured = false;
+        if (!configured) {
+            cudaError_t e = cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(kSelSmemCap * 6 + 16));
+            if (e != cudaSuccess) return e;
+            configured = true;
+        }
+        return launch_pdl(select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, grp,
+                          d, Smax, tau, q, input_token, bset, nb, Sq, cnt, sel_ids, sel_tokoff, sel_src, sel_count,
+                          out_ids, out_count, out_tokens);
+    }
+    return launch_pdl(select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, grp, d,
+                      Smax, tau, q, input_token, bset, nb, Sq, cnt, sel_ids, sel_tokoff, sel_src, sel_count, out_ids,
+                      out_count, out_tokens);
 }
 
 }  // namespace skv

@@ -144,4 +144,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) ----
+// Every decode kernel is launched with programmatic stream serialization: it lets the next kernel
+// of the stream start launching at once (trigger) and blocks until the previous kernel of the
+// stream has completed and its writes are visible (wait) before reading any input.  Only
+// input-independent setup (barrier init, smem carve-up) happens before the wait.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace skv
+
+// ---- optional phase tracing (SKV_TRACE builds only): clock64 stamps of block (0,0,0), thread 0,
+// into a per-translation-unit array `g_trace` that the file defines and exports for debugging ----
+#ifdef SKV_TRACE
+#define SKV_TRACE_DEFINE(name)                                                                  \
+    __device__ long long g_trace[32];                                                           \
+    extern "C" __attribute__((visibility("default"))) int sentencekv_debug_trace_##name(long long* out) { \
+        return (int)cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));                         \
+    }
+#define SKV_TRACE_POINT(slot)                                                                   \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)          \
+            g_trace[(slot)] = clock64();                                                        \
+    } while (0)
+#else
+#define SKV_TRACE_DEFINE(name)
+#define SKV_TRACE_POINT(slot) \
+    do {                      \
+    } while (0)
+#endif

@@ -29,11 +29,8 @@ struct LayerState {
     float* scores = nullptr;           // [B][G][Smax]     last step's similarity scores
     int32_t* sel_ids = nullptr;        // [B][G][tau]      ascending selected sentence ids
     int32_t* sel_tokoff = nullptr;     // [B][G][tau+1]    prefix sums of selected lengths
+    int32_t* sel_src = nullptr;        // [B][G][tau]      first context token of each selected sentence
     int32_t* sel_count = nullptr;      // [B][G]
-    // split-K attention workspace
-    float* o_part = nullptr;           // [B][G][nsplit][grp][d]
-    float* ml_part = nullptr;          // [B][G][nsplit][grp][2]  (running max (log2 domain), sum)
-    uint32_t* done = nullptr;          // [B][G]  arrival counters of the split blocks
     // host residency (P3)
     __nv_bfloat16* Kh = nullptr;       // pinned host [B][G][L][d]
     __nv_bfloat16* Vh = nullptr;
@@ -57,8 +54,6 @@ struct skv_ctx {
     int32_t* S_dev = nullptr;          // device [B]
     int32_t* bset = nullptr;           // device [kMaxBoundary]
     int n_bset = 0;
-    int nsplit = 0;                    // attention splits per (b, g)
-    int chunk = 0;                     // tokens per attention split
 
     std::vector<skv::LayerState> layer;
 
@@ -72,6 +67,25 @@ struct skv_ctx {
 };
 
 namespace skv {
+
+// Launches `kernel` on `st` with programmatic stream serialization (PDL) when enabled by the
+// environment (opt-in: SKV_PDL=1).  Kernels launched this way call pdl_wait() before reading inputs.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // ---- kernel launchers (each returns the cudaError_t of the launch) ----
 
@@ -92,15 +106,27 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B, int G, int grp,
                           int d, int Smax, int tau, const __nv_bfloat16* q, const int32_t* input_token,
                           const int32_t* bset, int nb, float* Sq, int32_t* cnt, int32_t* sel_ids,
-                          int32_t* sel_tokoff, int32_t* sel_count, int32_t* out_ids, int32_t* out_count,
-                          int32_t* out_tokens, cudaStream_t st);
+                          int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count, int32_t* out_ids,
+                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
 
 // D3 + D4: split-K attention over the selected sentences' tokens (device residency).
 cudaError_t launch_attend(const __nv_bfloat16* q, const __nv_bfloat16* K, const __nv_bfloat16* V, int B, int G,
-                          int grp, int d, int L, const int32_t* off, int off_stride, const int32_t* sel_ids,
-                          const int32_t* sel_tokoff, const int32_t* sel_count, int tau, int chunk, int nsplit,
-                          float* o_part, float* ml_part, uint32_t* done, float* out, cudaStream_t st);
+                          int grp, int d, int L, const int32_t* sel_src, const int32_t* sel_tokoff,
+                          const int32_t* sel_count, int tau, float* out, cudaStream_t st);
 
 int attend_chunk_tokens(int d);
+
+// D2 + D3 + D4 fused (one cluster per unit), reading the scores of launch_score.  Opt-in
+// (SKV_FUSED=1): on B200 the cluster-wide selection phases cost more than the separate select
+// kernel (profiles/r01_notes.md).
+bool fused_enabled();
+bool fused_supported(int d, int grp, int Smax, int tau);
+cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, int off_stride, const int32_t* S,
+                                       int B, int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
+                                       const int32_t* input_token, const int32_t* bset, int nb, float* Sq,
+                                       int32_t* cnt, const __nv_bfloat16* K, const __nv_bfloat16* V, int L,
+                                       int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count,
+                                       int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, float* out,
+                                       cudaStream_t st);
 
 }  // namespace skv

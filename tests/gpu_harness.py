@@ -20,11 +20,13 @@ def from_bits(a: np.ndarray, device) -> torch.Tensor:
 
 
 def run_parity(skv, orc: oracle.Oracle, toks, Ks, Vs, qs, script_tok, bset, device, check_scores=True,
-               units=None):
+               units=None, mode="split"):
     """Prefill all layers, then decode len(qs) steps over all layers, comparing every step.
 
     Ks/Vs: per layer bf16 bits [B][G][L][d]; qs[step][layer]: bf16 bits [B][Hq][d].
     units: optional list of (b, g) to compare (default: all).
+    mode: "split" = sentencekv_decode_select + sentencekv_decode_attend; "step" =
+    sentencekv_decode_step (fused select + attend).
     Returns a dict of statistics."""
     B, G, tau = skv.B, skv.G, skv.tau
     M = len(Ks)
@@ -60,8 +62,11 @@ def run_parity(skv, orc: oracle.Oracle, toks, Ks, Vs, qs, script_tok, bset, devi
         for l in range(M):
             q_bits = qstep[l]
             qd = from_bits(q_bits, device)
-            skv.decode_select(l, qd, it, sel_ids, sel_cnt, sel_tok)
-            skv.decode_attend(l, qd, out)
+            if mode == "step":
+                skv.decode_step(l, qd, it, out, sel_ids, sel_cnt, sel_tok)
+            else:
+                skv.decode_select(l, qd, it, sel_ids, sel_cnt, sel_tok)
+                skv.decode_attend(l, qd, out)
             sc_o, ids_o, ntok_o = orc.decode_select(l, q_bits, script_tok[step])
             O_o = orc.decode_attend(l, q_bits, ids_o)
             ids_g = sel_ids.cpu().numpy()

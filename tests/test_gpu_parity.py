@@ -22,36 +22,39 @@ def _skv(B, M, Hq, G, d, L, tau, **kw):
                              token_budget=tau, **kw)
 
 
+@pytest.mark.parametrize("mode", ["split", "step"])
 @pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("Hq", [8, 2])
-def test_tiny_config_full_parity(cuda_device, seed, Hq):
+def test_tiny_config_full_parity(cuda_device, seed, Hq, mode):
     """configs[0]: 1 layer, 2 KV heads, d=64, 4K tokens, ~20-token sentences, tau=256, B=1
     (Hq=8 -> GQA grp=4; Hq=2 -> MHA)."""
     B, M, G, d, L, tau, steps = 1, 1, 2, 64, 4096, 256, 40
     toks, _, Ks, Vs, qs, script = make_case(seed, B, M, Hq, G, d, L, tau, steps, median=20.0)
     skv = _skv(B, M, Hq, G, d, L, tau)
     orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
-    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
     assert st["steps"] == steps and st["max_abs"] <= ATOL
 
 
-def test_multi_sequence_multi_layer_gqa8(cuda_device):
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_multi_sequence_multi_layer_gqa8(cuda_device, mode):
     """B=3 prompts of different sentence counts, 2 layers, grp=8 (70B-style), d=128, ragged L."""
     B, M, Hq, G, d, L, tau, steps = 3, 2, 16, 2, 128, 5003, 512, 12
     toks, _, Ks, Vs, qs, script = make_case(11, B, M, Hq, G, d, L, tau, steps, median=25.0)
     skv = _skv(B, M, Hq, G, d, L, tau)
     orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
-    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
 
 
-def test_llama8b_32k_config(cuda_device):
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_llama8b_32k_config(cuda_device, mode):
     """configs[1] shapes (8 KV / 32 Q heads, d=128, 32K context, tau=1024, B=1) on 2 of the 32
     layers, every (b, g) unit, 6 decode steps."""
     B, M, Hq, G, d, L, tau, steps = 1, 2, 32, 8, 128, 32768, 1024, 6
     toks, _, Ks, Vs, qs, script = make_case(5, B, M, Hq, G, d, L, tau, steps, median=25.0)
     skv = _skv(B, 32, Hq, G, d, L, tau)  # ctx for all 32 layers; 2 exercised
     orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
-    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device)
+    run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
 
 
 def test_budget_at_least_context_equals_full_attention(cuda_device):
@@ -79,10 +82,13 @@ def test_budget_at_least_context_equals_full_attention(cuda_device):
 
 
 def _custom_case(device, toks, K_bits, V_bits, q_list, script, tau, Hq, G, d, bset=synth.BOUNDARY_IDS):
+    """Runs the case through both the split calls and the fused decode_step."""
     B, L = toks.shape
-    skv = _skv(B, 1, Hq, G, d, L, tau)
-    orc = oracle.Oracle(toks, bset, tau, 1, Hq, G, d)
-    return run_parity(skv, orc, toks, [K_bits], [V_bits], [[q] for q in q_list], script, bset, device)
+    for mode in ("split", "step"):
+        skv = _skv(B, 1, Hq, G, d, L, tau)
+        orc = oracle.Oracle(toks, bset, tau, 1, Hq, G, d)
+        st = run_parity(skv, orc, toks, [K_bits], [V_bits], [[q] for q in q_list], script, bset, device, mode=mode)
+    return st
 
 
 def test_ties_duplicated_sentences_and_zero_query(cuda_device):
@@ -164,3 +170,19 @@ def test_deterministic_run_to_run(cuda_device):
         outs.append(res)
     for (i1, o1), (i2, o2) in zip(*outs):
         assert np.array_equal(i1, i2) and np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
+
+
+def test_fused_select_attend_kernel_parity_subprocess(cuda_device):
+    """The opt-in fused select+attend cluster kernel (SKV_FUSED=1, read once per process) must give
+    the same bit-exact selections and 2e-3 outputs: rerun the decode_step parity cases in a child
+    process with the switch on."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_FUSED="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
+                        "-k", "(step or ties or all_equal or tau_cap or many_one) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
