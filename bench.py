@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--residency", choices=["device", "host"], default=None,
+                    help="K/V residency (default: host for 8b-128k, which configs[2] specifies, else device)")
     return ap.parse_args()
 
 
@@ -169,6 +171,7 @@ def oracle_sample(cfg, toks, Kh, Vh, qs, script, units, layers_sample, n_steps):
 
 def main():
     args = parse()
+    residency = args.residency or ("host" if args.config in ("8b-128k",) else "device")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -197,32 +200,43 @@ def main():
     toks, topics = np.stack(toks), np.stack(topics)
     tok_dev = torch.from_numpy(toks).to(dev)
     top_dev = torch.from_numpy(topics).to(dev)
+    host = residency == "host"
     skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
-                            device=local)
+                            device=local, residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE)
+    # ---------------- K/V generation + prefill (P1 segmentation, P2 embeddings, P3 offload in host
+    # residency), per layer; in host residency the device K/V of a layer is freed once offloaded
+    # (layers 0, 1 are kept for the CPU-oracle baseline).
     Ks, Vs, Cs = [], [], []
-    t_gen = time.perf_counter()
-    for l in range(M):
-        K, V, c = synth.kv_layer_torch(SEED + 1000 * rank, l, top_dev, G, d, device=dev)
-        Ks.append(K)
-        Vs.append(V)
-        Cs.append(c)
-    torch.cuda.synchronize()
-    t_gen = time.perf_counter() - t_gen
-
-    # ---------------- prefill (P1 + P2), timed for information
+    t_gen = 0.0
+    prefill_ms = 0.0
+    offload_s = 0.0
     skv.set_profiling(True)
-    pf0 = torch.cuda.Event(enable_timing=True)
-    pf1 = torch.cuda.Event(enable_timing=True)
-    pf0.record()
     for l in range(M):
-        skv.prefill_compress(l, Ks[l], Vs[l], token_ids=tok_dev if l == 0 else None,
+        t0 = time.perf_counter()
+        K, V, c = synth.kv_layer_torch(SEED + 1000 * rank, l, top_dev, G, d, device=dev)
+        torch.cuda.synchronize()
+        t_gen += time.perf_counter() - t0
+        pf0 = torch.cuda.Event(enable_timing=True)
+        pf1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        pf0.record()
+        skv.prefill_compress(l, K, V, token_ids=tok_dev if l == 0 else None,
                              boundary_ids=synth.BOUNDARY_IDS if l == 0 else None)
-    pf1.record()
-    torch.cuda.synchronize()
-    prefill_ms = pf0.elapsed_time(pf1)
+        pf1.record()
+        if host:
+            skv.sync()  # D2H copies of this layer done
+            offload_s += time.perf_counter() - t0
+        torch.cuda.synchronize()
+        prefill_ms += pf0.elapsed_time(pf1)
+        keep = (not host) or l < 2
+        Ks.append(K if keep else None)
+        Vs.append(V if keep else None)
+        Cs.append(c)
+        del K, V
     prof_prefill = skv.profile_read()
     skv.set_profiling(False)
     S = skv.sentence_counts()
+    kv_bytes_total = 2 * B * G * L * d * 2 * M
 
     # ---------------- decode inputs: POOL distinct steps
     script, target = synth.decode_script(SEED + rank, B, POOL)
@@ -256,6 +270,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------- timed region: K graph replays (device time, CUDA events, max over ranks)
+    ledger0 = sum(skv.host_fetch_bytes(l) for l in range(M)) if host else 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -277,6 +292,7 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = B * world / (ms_step / 1e3)
+    host_step_bytes = (sum(skv.host_fetch_bytes(l) for l in range(M)) - ledger0) / args.steps if host else 0
 
     # ---------------- per-kernel durations (profiled eager pass, events on the launching stream)
     # A spin kernel queued first lets the host enqueue the whole profiled pass ahead of the GPU,
@@ -384,7 +400,9 @@ def main():
             "data": "synthetic (seeded token streams with punctuation boundaries, topic-structured K/V/q)",
             "config": {"workload": args.config, "batch_per_gpu": B, "global_batch": B * world, "layers": M,
                        "q_heads": Hq, "kv_heads": G, "head_dim": d, "context": L, "token_budget": tau,
-                       "sentences": S, "residency": "device (HBM)", "parallelism": f"batch-sharded x{world}",
+                       "sentences": S,
+                       "residency": "pinned host K/V + HBM working set" if host else "device (HBM)",
+                       "parallelism": f"batch-sharded x{world}",
                        "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB read per step (L2 126 MB)",
                        "cuda_graph": True},
             "roofline": roofline,
@@ -398,6 +416,10 @@ def main():
                         "segment_ms": round(prof_prefill["segment"][0], 3),
                         "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4),
                         "compress_gbs": round(B * G * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
+            "host_residency": {"host_bytes_per_step": int(host_step_bytes),
+                               "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
+                               "offload_gbs_p3": round(kv_bytes_total / offload_s / 1e9, 2) if offload_s else None,
+                               "working_set_tokens_per_unit": 2 * tau} if host else None,
             "cpu_baseline": cpu,
             "kv_gen_s": round(t_gen, 2),
         }
@@ -434,6 +456,10 @@ def reference_arm(args, cfg, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 canonical / fp64",
             "data": "synthetic", "config": {"workload": args.config, "global_batch": B * world, "context": L,
                                             "token_budget": tau},
+            "host_residency": {"host_bytes_per_step": int(host_step_bytes),
+                               "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
+                               "offload_gbs_p3": round(kv_bytes_total / offload_s / 1e9, 2) if offload_s else None,
+                               "working_set_tokens_per_unit": 2 * tau} if host else None,
             "cpu_baseline": cpu,
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

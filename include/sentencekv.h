@@ -50,7 +50,10 @@ typedef enum {
 
 typedef enum {
     SKV_KV_DEVICE = 0, /* K/V stay in HBM, borrowed from the caller (kept until next prefill/destroy) */
-    SKV_KV_HOST = 1    /* P3: full K/V offloaded to ctx-owned pinned host memory */
+    SKV_KV_HOST = 1    /* P3: full K/V offloaded to ctx-owned pinned, mapped host memory; each
+                          decode step re-reads sentences selected at the previous step from an HBM working
+                          set (2*tau tokens per (sequence, layer, KV head), needs r >= 2) and fetches the
+                          others from host memory over PCIe (D3) */
 } skv_residency;
 
 typedef struct {
@@ -61,8 +64,9 @@ typedef struct {
     int32_t head_dim;        /* d in {64, 128} */
     int32_t max_context;     /* L_max: largest prompt length accepted */
     int32_t token_budget;    /* tau >= 1: retrieved tokens per (sequence, layer, KV head) (A15) */
-    float semantic_factor;   /* r >= 1; host residency: HBM working set = floor(r*tau)
-                                tokens per (sequence, layer, KV head) (A19, A20) */
+    float semantic_factor;   /* r >= 1; host residency needs r >= 2: its HBM working set holds
+                                the previous and the current selection, 2*tau <= floor(r*tau) tokens per
+                                (sequence, layer, KV head) (A19, A20) */
     int32_t obs_window;      /* N; must be 0 -- observation-window retention is NEXT-1 */
     int32_t residency;       /* skv_residency */
     int32_t device;          /* CUDA device ordinal */
@@ -139,7 +143,9 @@ skv_status sentencekv_decode_select(skv_ctx* ctx, int32_t layer, const void* q, 
  * Decode, per layer per step: D3 + D4 (Alg. 1 lines 18-19) over the selection made
  * by the last decode_select of the same layer.
  *   D3: gather the selected sentences' K/V rows (contiguous runs) into shared memory with bulk
- *       async copies (device residency: from the caller's K/V in HBM).
+ *       async copies (device residency: from the caller's K/V in HBM; host residency: sentences
+ *       also selected at the previous step from the HBM working set, the others from the pinned
+ *       host store over PCIe, the staged rows written through to the working set).
  *   D4: O = softmax(q K_sel^T / sqrt(d)) V_sel (Eq. 3; A16-A18), split-K
  *       flash-decode with fp32 online softmax, combined in-kernel.
  *
@@ -183,6 +189,10 @@ skv_status sentencekv_copy_embeddings(skv_ctx* ctx, int32_t layer, void* E_out, 
 
 /* Scores of the last decode_select of the layer: device fp32 [batch_count][kv_head_count][S_max]. */
 skv_status sentencekv_copy_scores(skv_ctx* ctx, int32_t layer, float* scores_out, skv_stream_t stream);
+
+/* Host residency ledger: bytes of K/V fetched from host memory by the decode steps of `layer`
+ * since its prompt's prefill (synchronous).  0 in device residency. */
+skv_status sentencekv_host_fetch_bytes(skv_ctx* ctx, int32_t layer, uint64_t* bytes_out);
 
 /* Number of CUDA kernel launches this context has enqueued since creation. */
 int64_t sentencekv_launch_count(const skv_ctx* ctx);

@@ -73,6 +73,7 @@ def _load():
         "sentencekv_copy_scores": (i32, [P, i32, P, P]),
         "sentencekv_launch_count": (i64, [P]),
         "sentencekv_set_profiling": (i32, [P, i32]),
+        "sentencekv_host_fetch_bytes": (i32, [P, i32, P]),
         "sentencekv_profile_read": (i32, [P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -241,6 +242,12 @@ class SentenceKV:
         out = torch.empty((self.B, self.G, S), dtype=torch.float32, device=self.device)
         _check(self.ctx, lib.sentencekv_copy_scores(self.ctx, layer, _ptr(out), _stream(stream)))
         return out
+
+    def host_fetch_bytes(self, layer) -> int:
+        """Host residency ledger: K/V bytes fetched from host memory by the decode steps of `layer`."""
+        v = ctypes.c_uint64()
+        _check(self.ctx, lib.sentencekv_host_fetch_bytes(self.ctx, int(layer), ctypes.byref(v)))
+        return int(v.value)
 
     def launch_count(self) -> int:
         return int(lib.sentencekv_launch_count(self.ctx))

@@ -69,14 +69,33 @@ void dfree(T*& p) {
     p = nullptr;
 }
 
+void free_sel(skv::SelBufs& s) {
+    dfree(s.ids);
+    dfree(s.tokoff);
+    dfree(s.src);
+    dfree(s.count);
+    dfree(s.parity);
+}
+
+void free_layer_prompt(skv::LayerState& ls) {
+    dfree(ls.E);
+    dfree(ls.scores);
+    free_sel(ls.sel);
+    dfree(ls.wsK);
+    dfree(ls.wsV);
+}
+
+void free_host_store(skv::LayerState& ls) {
+    if (ls.Kh) cudaFreeHost(ls.Kh);
+    if (ls.Vh) cudaFreeHost(ls.Vh);
+    ls.Kh = ls.Vh = nullptr;
+    ls.host_bytes = 0;
+    ls.host_ready = false;
+}
+
 void free_prompt_buffers(skv_ctx* c) {
     for (auto& ls : c->layer) {
-        dfree(ls.E);
-        dfree(ls.scores);
-        dfree(ls.sel_ids);
-        dfree(ls.sel_tokoff);
-        dfree(ls.sel_src);
-        dfree(ls.sel_count);
+        free_layer_prompt(ls);
         ls.prefilled = false;
         ls.selected = false;
         ls.K = ls.V = nullptr;
@@ -154,8 +173,10 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         return SKV_ERR_INVALID_ARGUMENT;
     const int grp = cfg.q_heads / cfg.kv_heads;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
-        cfg.obs_window != 0 || cfg.residency == SKV_KV_HOST)
+        cfg.obs_window != 0)
         return SKV_ERR_UNSUPPORTED;
+    // host residency keeps the previous and the current selection in HBM: 2*tau <= floor(r*tau)
+    if (cfg.residency == SKV_KV_HOST && !(cfg.semantic_factor >= 2.0f)) return SKV_ERR_INVALID_ARGUMENT;
 
     skv_ctx* c = new (std::nothrow) skv_ctx();
     if (!c) return SKV_ERR_OUT_OF_MEMORY;
@@ -177,6 +198,14 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         if (e == cudaSuccess) e = cudaMemset(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d);
         if (e == cudaSuccess) e = cudaMemset(ls.cnt, 0, sizeof(int32_t) * c->B);
     }
+    if (e == cudaSuccess && cfg.residency == SKV_KV_HOST) {
+        e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+        for (auto& ls : c->layer) {
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ls.offload_done, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = dalloc(&ls.ledger, 1);
+            if (e == cudaSuccess) e = cudaMemset(ls.ledger, 0, sizeof(unsigned long long));
+        }
+    }
     if (e == cudaSuccess) e = dalloc(&c->S_dev, (size_t)c->B);
     if (e == cudaSuccess) e = dalloc(&c->bset, (size_t)skv::kMaxBoundary);
     if (e != cudaSuccess) {
@@ -196,6 +225,9 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     for (auto& ls : c->layer) {
         dfree(ls.Sq);
         dfree(ls.cnt);
+        dfree(ls.ledger);
+        free_host_store(ls);
+        if (ls.offload_done) cudaEventDestroy(ls.offload_done);
     }
     dfree(c->S_dev);
     dfree(c->bset);
@@ -224,14 +256,22 @@ SKV_API skv_status sentencekv_sync(skv_ctx* c) {
 
 // (Re)allocates the sentence-dependent buffers of every layer for a prompt with capacity Smax.
 static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
-    const size_t B = c->B, G = c->G, d = c->d, tau = c->tau;
+    const size_t B = c->B, G = c->G, d = c->d, tau = c->tau, U = B * G;
     for (auto& ls : c->layer) {
         SKV_CUDA(c, dalloc(&ls.E, B * G * Smax * d));
         SKV_CUDA(c, dalloc(&ls.scores, B * G * Smax));
-        SKV_CUDA(c, dalloc(&ls.sel_ids, B * G * tau));
-        SKV_CUDA(c, dalloc(&ls.sel_tokoff, B * G * (tau + 1)));
-        SKV_CUDA(c, dalloc(&ls.sel_src, B * G * tau));
-        SKV_CUDA(c, dalloc(&ls.sel_count, B * G));
+        skv::SelBufs& sb = ls.sel;
+        sb.units = (int)U;
+        sb.tau = (int)tau;
+        SKV_CUDA(c, dalloc(&sb.ids, 2 * U * tau));
+        SKV_CUDA(c, dalloc(&sb.tokoff, 2 * U * (tau + 1)));
+        SKV_CUDA(c, dalloc(&sb.src, 2 * U * tau));
+        SKV_CUDA(c, dalloc(&sb.count, 2 * U));
+        SKV_CUDA(c, dalloc(&sb.parity, U));
+        if (c->cfg.residency == SKV_KV_HOST) {
+            SKV_CUDA(c, dalloc(&ls.wsK, U * 2 * tau * d));
+            SKV_CUDA(c, dalloc(&ls.wsV, U * 2 * tau * d));
+        }
     }
     c->Smax = Smax;
     return SKV_OK;
@@ -279,18 +319,17 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         int Smax = 1;
         for (int b = 0; b < c->B; ++b) Smax = c->S_host[b] > Smax ? c->S_host[b] : Smax;
         if (Smax > c->Smax || !c->layer[0].E) {
-            for (auto& ls : c->layer) {
-                dfree(ls.E); dfree(ls.scores); dfree(ls.sel_ids); dfree(ls.sel_tokoff);
-                dfree(ls.sel_src); dfree(ls.sel_count);
-            }
+            for (auto& ls : c->layer) free_layer_prompt(ls);
             skv_status s = alloc_prompt_buffers(c, Smax);
             if (s != SKV_OK) return s;
         }
         for (auto& ls : c->layer) {
             ls.prefilled = false;
             ls.selected = false;
-            // no previous selection: the fused kernel's L2 prefetch of it is then empty
-            SKV_CUDA(c, cudaMemsetAsync(ls.sel_count, 0, sizeof(int32_t) * c->B * c->G, st));
+            // no previous selection (empty slot 0, parity 0): the host gather misses everything at the
+            // first step and the fused kernel's L2 prefetch is empty
+            SKV_CUDA(c, cudaMemsetAsync(ls.sel.count, 0, sizeof(int32_t) * 2 * c->B * c->G, st));
+            SKV_CUDA(c, cudaMemsetAsync(ls.sel.parity, 0, sizeof(int32_t) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B, st));
         }
@@ -304,8 +343,36 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
     SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
     prof_end(c, SKV_K_COMPRESS, pa, st);
     c->launches += 1;
-    ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
-    ls.V = Vb;
+    if (c->cfg.residency == SKV_KV_HOST) {
+        // P3: full K/V of this layer -> ctx-owned pinned, mapped host memory, on the copy stream
+        const size_t bytes = sizeof(__nv_bfloat16) * (size_t)c->B * c->G * L * c->d;
+        if (ls.host_bytes != bytes) {
+            free_host_store(ls);
+            void *hk = nullptr, *hv = nullptr;
+            if (cudaHostAlloc(&hk, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+                cudaHostAlloc(&hv, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                if (hk) cudaFreeHost(hk);
+                return fail(c, SKV_ERR_OUT_OF_MEMORY, "pinned host store of %zu bytes for layer %d", 2 * bytes, layer);
+            }
+            ls.Kh = static_cast<__nv_bfloat16*>(hk);
+            ls.Vh = static_cast<__nv_bfloat16*>(hv);
+            ls.host_bytes = bytes;
+        }
+        if (!c->copy_event) SKV_CUDA(c, cudaEventCreateWithFlags(&c->copy_event, cudaEventDisableTiming));
+        SKV_CUDA(c, cudaEventRecord(c->copy_event, st));
+        SKV_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_event, 0));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.Kh, Kb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.Vh, Vb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        SKV_CUDA(c, cudaEventRecord(ls.offload_done, c->copy_stream));
+        ls.host_ready = false;
+        ls.K = ls.V = nullptr;  // the caller may free its K/V after sentencekv_sync
+        if (layer == 0)
+            for (auto& l2 : c->layer) SKV_CUDA(c, cudaMemsetAsync(l2.ledger, 0, sizeof(unsigned long long), st));
+    } else {
+        ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
+        ls.V = Vb;
+    }
     ls.prefilled = true;
     ls.selected = false;
     return SKV_OK;
@@ -328,8 +395,8 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
     prof_end(c, SKV_K_SCORE, pa, st);
     pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax,
-                                   c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt, ls.sel_ids,
-                                   ls.sel_tokoff, ls.sel_src, ls.sel_count, sel_ids, sel_count, sel_tokens, st));
+                                   c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt, ls.sel, false,
+                                   sel_ids, sel_count, sel_tokens, st));
     prof_end(c, SKV_K_SELECT, pa, st);
     c->launches += 2;
     ls.selected = true;
@@ -348,7 +415,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
-    if (!skv::fused_enabled() || !skv::fused_supported(c->d, c->grp, c->Smax, c->tau)) {
+    if (!skv::fused_enabled() || c->cfg.residency != SKV_KV_DEVICE ||
+        !skv::fused_supported(c->d, c->grp, c->Smax, c->tau)) {
         skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
         if (s != SKV_OK) return s;
         return sentencekv_decode_attend(c, layer, q, out, stream_);
@@ -359,8 +427,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_fused_select_attend(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d,
                                                 c->Smax, c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt,
-                                                ls.K, ls.V, c->L, ls.sel_ids, ls.sel_tokoff, ls.sel_src,
-                                                ls.sel_count, sel_ids, sel_count, sel_tokens, out, st));
+                                                skv::KvSrc{ls.K, ls.V, c->L, 0}, ls.sel, sel_ids, sel_count,
+                                                sel_tokens, out, st));
     prof_end(c, SKV_K_FUSED, pa, st);
     c->launches += 2;
     ls.selected = true;
@@ -378,9 +446,20 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
     if (!q || !out) return fail(c, SKV_ERR_INVALID_ARGUMENT, "q / out is NULL");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
-    cudaEvent_t pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_attend(static_cast<const __nv_bfloat16*>(q), ls.K, ls.V, c->B, c->G, c->grp, c->d, c->L,
-                                   ls.sel_src, ls.sel_tokoff, ls.sel_count, c->tau, out, st));
+    const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    cudaEvent_t pa = nullptr;
+    if (c->cfg.residency == SKV_KV_HOST) {
+        if (!ls.host_ready) {  // first decode of the layer after its prefill: the offload must be done
+            SKV_CUDA(c, cudaEventSynchronize(ls.offload_done));
+            ls.host_ready = true;
+        }
+        pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_attend_host(qb, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV, c->B, c->G, c->grp, c->d, ls.sel,
+                                            ls.ledger, out, st));
+    } else {
+        pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_attend(qb, skv::KvSrc{ls.K, ls.V, c->L, 0}, c->B, c->G, c->grp, c->d, ls.sel, out, st));
+    }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;
     return SKV_OK;
@@ -426,6 +505,20 @@ SKV_API skv_status sentencekv_copy_scores(skv_ctx* c, int32_t layer, float* out,
 }
 
 SKV_API int64_t sentencekv_launch_count(const skv_ctx* c) { return c ? c->launches : 0; }
+
+SKV_API skv_status sentencekv_host_fetch_bytes(skv_ctx* c, int32_t layer, uint64_t* bytes_out) {
+    if (!c || !bytes_out) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    if (c->cfg.residency != SKV_KV_HOST) {
+        *bytes_out = 0;
+        return SKV_OK;
+    }
+    DeviceGuard dg(c->cfg.device);
+    unsigned long long v = 0;
+    SKV_CUDA(c, cudaMemcpy(&v, c->layer[layer].ledger, sizeof(v), cudaMemcpyDeviceToHost));
+    *bytes_out = v;
+    return SKV_OK;
+}
 
 SKV_API skv_status sentencekv_set_profiling(skv_ctx* c, int32_t on) {
     if (!c) return SKV_ERR_INVALID_ARGUMENT;

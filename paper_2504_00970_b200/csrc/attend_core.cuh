@@ -28,14 +28,38 @@ struct AttSmem {
     uint32_t done[kStages];                      // warps finished with the stage's current chunk
 };
 
+// Host residency (D3, "loaded from CPU back to the GPU memory"): where this unit's rows come
+// from and go to.  A selected sentence that was also selected at the previous step is re-read from
+// the previous working-set slot in HBM (src < 0 encodes row -(src+1) of that slot); the others are
+// read from the mapped pinned host store over PCIe (src >= 0 = context row).  Every staged chunk is
+// written through to the current slot, which becomes the next step's previous slot.
+struct HostWs {
+    const __nv_bfloat16* prevK;
+    const __nv_bfloat16* prevV;
+    __nv_bfloat16* curK;
+    __nv_bfloat16* curV;
+    unsigned long long* ledger;  // host bytes fetched (cumulative)
+};
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Issues the bulk copies of gathered chunk `c` (tokens [c*C, c*C+nc)) into stage `s`.  Called by
-// one whole warp.  Selected sentence i occupies gathered tokens [tok[i], tok[i+1]) and context
-// tokens [src[i], src[i] + tok[i+1] - tok[i]); tok / src are the shared-memory copies of the
-// selection.
-template <int D, int GRP>
-__device__ __forceinline__ void issue_chunk(AttSmem<D, GRP>& sm, int s, int c, int nc, const int32_t* tok,
-                                            const int32_t* srcs, int count, const __nv_bfloat16* Kh,
-                                            const __nv_bfloat16* Vh, int lane) {
+// one whole warp.  Selected sentence i occupies gathered tokens [tok[i], tok[i+1]) and rows
+// [src[i], src[i] + tok[i+1] - tok[i]) of the attended store (context K/V, or with HOST the host
+// store / previous working-set slot, see HostWs); tok / src are the shared-memory copies of the
+// selection.  Returns the host bytes this lane requested.
+template <int D, int GRP, bool HOST>
+__device__ __forceinline__ uint32_t issue_chunk(AttSmem<D, GRP>& sm, int s, int c, int nc, const int32_t* tok,
+                                                const int32_t* srcs, int count, const __nv_bfloat16* Kh,
+                                                const __nv_bfloat16* Vh, const HostWs& ws, int lane) {
+    uint32_t host = 0;
     const int c0 = c * kAttC;
     if (lane == 0) mbar_arrive_expect_tx(&sm.bar[s], (uint32_t)(nc * D * 2 * 2));
     __syncwarp();
@@ -50,11 +74,20 @@ __device__ __forceinline__ void issue_chunk(AttSmem<D, GRP>& sm, int s, int c, i
         if (ts >= c0 + nc) break;
         const int te = tok[i + 1];
         const int ps = max(ts, c0), pe = min(te, c0 + nc);
-        const size_t src = (size_t)(srcs[i] + (ps - ts)) * D;
         const uint32_t bytes = (uint32_t)((pe - ps) * D * 2);
-        bulk_g2s(&sm.K[s][(ps - c0) * D], Kh + src, bytes, &sm.bar[s]);
-        bulk_g2s(&sm.V[s][(ps - c0) * D], Vh + src, bytes, &sm.bar[s]);
+        const int v = srcs[i];
+        if (HOST && v < 0) {
+            const size_t src = (size_t)(-(v + 1) + (ps - ts)) * D;
+            bulk_g2s(&sm.K[s][(ps - c0) * D], ws.prevK + src, bytes, &sm.bar[s]);
+            bulk_g2s(&sm.V[s][(ps - c0) * D], ws.prevV + src, bytes, &sm.bar[s]);
+        } else {
+            const size_t src = (size_t)(v + (ps - ts)) * D;
+            bulk_g2s(&sm.K[s][(ps - c0) * D], Kh + src, bytes, &sm.bar[s]);
+            bulk_g2s(&sm.V[s][(ps - c0) * D], Vh + src, bytes, &sm.bar[s]);
+            if (HOST) host += 2 * bytes;
+        }
     }
+    return host;
 }
 
 __device__ __forceinline__ void unpack8x2(const uint4& v, float2* f) {
@@ -67,11 +100,12 @@ __device__ __forceinline__ void unpack8x2(const uint4& v, float2* f) {
 // The chunk loop, warp merge and cluster merge for one (b, g) unit, run by every CTA of the
 // unit's cluster once the selection metadata (tok[0..count], srcs[0..count)) is in its shared
 // memory, the stage barriers are initialised and mw/lw are reset.  Writes out[(b*Hq+g*GRP)*D ..].
-template <int D, int GRP>
+template <int D, int GRP, bool HOST = false>
 __device__ __forceinline__ void attend_body(AttSmem<D, GRP>& sm, const int32_t* tok, const int32_t* srcs, int count,
                                             const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                                             const __nv_bfloat16* __restrict__ q, float* __restrict__ out, int b,
-                                            int g, int G, float scale_log2, cg::cluster_group& cluster) {
+                                            int g, int G, float scale_log2, cg::cluster_group& cluster,
+                                            const HostWs& ws = HostWs{}) {
     constexpr int C = kAttC;
     constexpr int NW = kAttWarps;
     constexpr int SL = D / 8;           // 16-byte slices per row
@@ -89,10 +123,11 @@ __device__ __forceinline__ void attend_body(AttSmem<D, GRP>& sm, const int32_t* 
     const int per = (nchunk + kCL - 1) / kCL;
     const int cbeg = min(nchunk, rank * per), cend = min(nchunk, cbeg + per);
     const int mine = cend - cbeg;
+    uint32_t host_bytes = 0;
     if (warp == 0)
         for (int s = 0; s < kStages && s < mine; ++s) {
             const int c = cbeg + s;
-            issue_chunk(sm, s, c, min(C, ntok - c * C), tok, srcs, count, Kh, Vh, lane);
+            host_bytes += issue_chunk<D, GRP, HOST>(sm, s, c, min(C, ntok - c * C), tok, srcs, count, Kh, Vh, ws, lane);
         }
 
     SKV_TRACE_POINT(2);
@@ -220,10 +255,19 @@ __device__ __forceinline__ void attend_body(AttSmem<D, GRP>& sm, const int32_t* 
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
             if (lane == 0) sm.done[s] = 0u;
+            if (HOST && lane == 0) {
+                // write the staged rows through to the current working-set slot (gathered order)
+                bulk_s2g(ws.curK + (size_t)c * C * D, &sm.K[s][0], (uint32_t)(nc * D * 2));
+                bulk_s2g(ws.curV + (size_t)c * C * D, &sm.V[s][0], (uint32_t)(nc * D * 2));
+                bulk_commit();
+                bulk_wait_read();  // the stage may be refilled once the store has read it
+            }
+            __syncwarp();
             if (it + kStages < mine) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const int cn = c + kStages;
-                issue_chunk(sm, s, cn, min(C, ntok - cn * C), tok, srcs, count, Kh, Vh, lane);
+                host_bytes += issue_chunk<D, GRP, HOST>(sm, s, cn, min(C, ntok - cn * C), tok, srcs, count, Kh, Vh,
+                                                        ws, lane);
             }
         }
     }
@@ -240,6 +284,13 @@ __device__ __forceinline__ void attend_body(AttSmem<D, GRP>& sm, const int32_t* 
                 acc[h][i].y += __shfl_xor_sync(0xffffffffu, acc[h][i].y, w);
             }
     SKV_TRACE_POINT(20);
+    if (HOST) {
+        bulk_wait_all();  // write-through stores complete (no-op for threads that issued none)
+        unsigned long long hb = host_bytes;
+#pragma unroll
+        for (int o2 = 16; o2 >= 1; o2 >>= 1) hb += __shfl_xor_sync(0xffffffffu, hb, o2);
+        if (lane == 0 && hb) atomicAdd(ws.ledger, hb);
+    }
     __syncthreads();  // every warp is done with the stages
     float* red = reinterpret_cast<float*>(&sm.K[0][0]);  // [warps][GRP][D]
     if (tsub == 0) {

@@ -69,10 +69,7 @@ fused_select_attend_kernel(const float* __restrict__ scores, const int32_t* __re
                            const int32_t* __restrict__ S, int G, int Smax, int tau,
                            const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
                            const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq,
-                           int32_t* __restrict__ cnt, const __nv_bfloat16* __restrict__ K,
-                           const __nv_bfloat16* __restrict__ V, int L, int32_t* __restrict__ sel_ids,
-                           int32_t* __restrict__ sel_tokoff, int32_t* __restrict__ sel_src,
-                           int32_t* __restrict__ sel_count, int32_t* __restrict__ out_ids,
+                           int32_t* __restrict__ cnt, KvSrc kv, SelBufs sel, int32_t* __restrict__ out_ids,
                            int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens,
                            float* __restrict__ out, float scale_log2) {
     constexpr int NT = kAttThreads;
@@ -124,20 +121,24 @@ fused_select_attend_kernel(const float* __restrict__ scores, const int32_t* __re
     const int nloc = r1 - r0;
     const float* sc = scores + (size_t)unit * Smax;
     const int32_t* o = off + (size_t)b * off_stride;
-    const __nv_bfloat16* Kh = K + (size_t)unit * L * D;
-    const __nv_bfloat16* Vh = V + (size_t)unit * L * D;
-    int32_t* g_tok = sel_tokoff + (size_t)unit * (tau + 1);
-    int32_t* g_src = sel_src + (size_t)unit * tau;
-    int32_t* g_ids = sel_ids + (size_t)unit * tau;
+    // device residency only (host checks): rows are context tokens, slot_stride == 0
+    const __nv_bfloat16* Kh = kv.K + (size_t)unit * kv.unit_stride * D;
+    const __nv_bfloat16* Vh = kv.V + (size_t)unit * kv.unit_stride * D;
+    const int prev = sel.parity[unit], cur = prev ^ 1;
+    int32_t* g_tok = sel.tok_of(cur, unit);
+    int32_t* g_src = sel.src_of(cur, unit);
+    int32_t* g_ids = sel.ids_of(cur, unit);
 
     // ---- (a) L2 prefetch of the previous step's selection (this CTA's share) ----
     {
-        const int pc = sel_count[unit];
+        const int pc = *sel.count_of(prev, unit);
+        const int32_t* p_tok = sel.tok_of(prev, unit);
+        const int32_t* p_src = sel.src_of(prev, unit);
         const int pper = (pc + kCL - 1) / kCL;
         const int p0 = min(pc, rank * pper), p1 = min(pc, p0 + pper);
         for (int j = p0 + tid; j < p1; j += NT) {
-            const int n = g_tok[j + 1] - g_tok[j];
-            const size_t src = (size_t)g_src[j] * D;
+            const int n = p_tok[j + 1] - p_tok[j];
+            const size_t src = (size_t)p_src[j] * D;
             prefetch_l2(Kh + src, (uint32_t)(n * D * 2));
             prefetch_l2(Vh + src, (uint32_t)(n * D * 2));
         }
@@ -399,7 +400,7 @@ fused_select_attend_kernel(const float* __restrict__ scores, const int32_t* __re
         tok[count] = ntok;  // every CTA writes its own copy
         if (rank == 0) {
             g_tok[count] = ntok;
-            sel_count[unit] = count;
+            *sel.count_of(cur, unit) = count;
             if (out_count) out_count[unit] = count;
             if (out_tokens) out_tokens[unit] = ntok;
         }
@@ -413,15 +414,15 @@ fused_select_attend_kernel(const float* __restrict__ scores, const int32_t* __re
     cluster.sync();  // #8: every CTA holds the full selection metadata; scratch is dead
 
     attend_body<D, GRP>(sm, tok, srcs, count, Kh, Vh, q, out, b, g, G, scale_log2, cluster);
+    if (rank == 0 && tid == 0) sel.parity[unit] = cur;  // all CTAs read parity before the first barrier
 }
 
 template <int D, int GRP>
 static cudaError_t launch_fused_t(dim3 grid, cudaStream_t st, const float* scores, const int32_t* off, int off_stride,
                                   const int32_t* S, int G, int Smax, int tau, const __nv_bfloat16* q,
                                   const int32_t* input_token, const int32_t* bset, int nb, float* Sq, int32_t* cnt,
-                                  const __nv_bfloat16* K, const __nv_bfloat16* V, int L, int32_t* sel_ids,
-                                  int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count, int32_t* out_ids,
-                                  int32_t* out_count, int32_t* out_tokens, float* out, float scale_log2) {
+                                  KvSrc kv, SelBufs sel, int32_t* out_ids, int32_t* out_count, int32_t* out_tokens,
+                                  float* out, float scale_log2) {
     const size_t smem = fused_smem_bytes<D, GRP>(tau);
     static size_t configured = 0;
     if (smem > configured) {
@@ -434,8 +435,8 @@ static cudaError_t launch_fused_t(dim3 grid, cudaStream_t st, const float* score
         configured = smem;
     }
     return launch_pdl(fused_select_attend_kernel<D, GRP>, grid, dim3(kAttThreads), smem, st, scores, off, off_stride,
-                      S, G, Smax, tau, q, input_token, bset, nb, Sq, cnt, K, V, L, sel_ids, sel_tokoff, sel_src,
-                      sel_count, out_ids, out_count, out_tokens, out, scale_log2);
+                      S, G, Smax, tau, q, input_token, bset, nb, Sq, cnt, kv, sel, out_ids, out_count, out_tokens, out,
+                      scale_log2);
 }
 
 bool fused_supported(int d, int grp, int Smax, int tau) {
@@ -446,16 +447,13 @@ bool fused_supported(int d, int grp, int Smax, int tau) {
 cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, int off_stride, const int32_t* S,
                                        int B, int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
                                        const int32_t* input_token, const int32_t* bset, int nb, float* Sq,
-                                       int32_t* cnt, const __nv_bfloat16* K, const __nv_bfloat16* V, int L,
-                                       int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count,
-                                       int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, float* out,
-                                       cudaStream_t st) {
+                                       int32_t* cnt, KvSrc kv, SelBufs sel, int32_t* out_ids, int32_t* out_count,
+                                       int32_t* out_tokens, float* out, cudaStream_t st) {
     dim3 grid(kCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
 #define SKV_FU(DV, GV)                                                                                              \
     return launch_fused_t<DV, GV>(grid, st, scores, off, off_stride, S, G, Smax, tau, q, input_token, bset, nb, Sq, \
-                                  cnt, K, V, L, sel_ids, sel_tokoff, sel_src, sel_count, out_ids, out_count,       \
-                                  out_tokens, out, scale_log2)
+                                  cnt, kv, sel, out_ids, out_count, out_tokens, out, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_FU(128, 1);

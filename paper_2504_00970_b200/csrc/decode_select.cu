@@ -205,8 +205,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ off, int off_stride,
     const int32_t* __restrict__ S, int G, int grp, int D, int Smax, int tau, const __nv_bfloat16* __restrict__ q,
     const int32_t* __restrict__ input_token, const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq,
-    int32_t* __restrict__ cnt, int32_t* __restrict__ sel_ids, int32_t* __restrict__ sel_tokoff,
-    int32_t* __restrict__ sel_src, int32_t* __restrict__ sel_count, int32_t* __restrict__ out_ids,
+    int32_t* __restrict__ cnt, SelBufs sel, bool src_gathered, int32_t* __restrict__ out_ids,
     int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens) {
     __shared__ uint32_t hw[kBins];  // length-weighted histogram
     __shared__ uint32_t hc[kBins];  // count histogram
@@ -423,9 +422,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     SKV_TRACE_POINT(20);
     const unsigned long long excl = block_incl_sum<unsigned long long>(mine, ws64, &tot) - mine;
     SKV_TRACE_POINT(21);
-    int32_t* ids = sel_ids + (size_t)(b * G + g) * tau;
-    int32_t* tokoff = sel_tokoff + (size_t)(b * G + g) * (tau + 1);
-    int32_t* src = sel_src + (size_t)(b * G + g) * tau;
+    // this step's selection goes to slot parity^1 (the previous one stays readable in slot parity)
+    const int cur = sel.parity[b * G + g] ^ 1;
+    int32_t* ids = sel.ids_of(cur, b * G + g);
+    int32_t* tokoff = sel.tok_of(cur, b * G + g);
+    int32_t* src = sel.src_of(cur, b * G + g);
     if (mine) {
         int pos = (int)(excl >> 32);
         uint32_t toff = (uint32_t)(excl & 0xffffffffull);
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
             if (all_fit || key64_of(key_of(s), s) > thr) {
                 ids[pos] = s;
                 tokoff[pos] = (int32_t)toff;
-                src[pos] = o[s];
+                src[pos] = src_gathered ? (int32_t)toff : o[s];
                 ++pos;
                 toff += len_of(s);
             }
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const int ntok = (int)(tot & 0xffffffffull);
     if (tid == 0) {
         tokoff[count] = ntok;
-        sel_count[b * G + g] = count;
+        *sel.count_of(cur, b * G + g) = count;
         if (out_count) out_count[b * G + g] = count;
         if (out_tokens) out_tokens[b * G + g] = ntok;
     }
@@ -458,8 +459,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
                           int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
                           const int32_t* input_token, const int32_t* bset, int nb, float* Sq, int32_t* cnt,
-                          int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count,
-                          int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, cudaStream_t st) {
+                          SelBufs sel, bool src_gathered, int32_t* out_ids, int32_t* out_count,
+                          int32_t* out_tokens, cudaStream_t st) {
     dim3 grid(G, B);
     if (Smax <= kSelSmemCap && tau <= 65535) {
         const size_t smem = (size_t)Smax * 6 + 16;
@@ -471,12 +472,12 @@ cudaError_t launch_select(const float* scores, const int32_t* off, int off_strid
             configured = true;
         }
         return launch_pdl(select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, grp,
-                          d, Smax, tau, q, input_token, bset, nb, Sq, cnt, sel_ids, sel_tokoff, sel_src, sel_count,
-                          out_ids, out_count, out_tokens);
+                          d, Smax, tau, q, input_token, bset, nb, Sq, cnt, sel, src_gathered, out_ids, out_count,
+                          out_tokens);
     }
     return launch_pdl(select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, grp, d,
-                      Smax, tau, q, input_token, bset, nb, Sq, cnt, sel_ids, sel_tokoff, sel_src, sel_count, out_ids,
-                      out_count, out_tokens);
+                      Smax, tau, q, input_token, bset, nb, Sq, cnt, sel, src_gathered, out_ids, out_count,
+                      out_tokens);
 }
 
 }  // namespace skv

@@ -14,6 +14,33 @@
 namespace skv {
 
 constexpr int kMaxBoundary = 64;
+
+// Double-buffered selection of one layer.  Slot `parity[unit]` holds the previous step's
+// selection; decode_select writes slot parity^1; decode_attend flips parity at its end.  (The
+// previous selection is what the host-residency gather reuses and what the fused kernel
+// prefetches.)  The flip happens on the device, so replaying a captured step stays consistent.
+struct SelBufs {
+    int32_t* ids;     // [2][units][tau]    ascending selected sentence ids
+    int32_t* tokoff;  // [2][units][tau+1]  prefix sums of the selected lengths (gathered offsets)
+    int32_t* src;     // [2][units][tau]    first K/V row of each selected sentence in the attended store
+    int32_t* count;   // [2][units]         selected sentences
+    int32_t* parity;  // [units]
+    int units, tau;
+    __host__ __device__ int32_t* ids_of(int slot, int u) const { return ids + ((size_t)slot * units + u) * tau; }
+    __host__ __device__ int32_t* tok_of(int slot, int u) const { return tokoff + ((size_t)slot * units + u) * (tau + 1); }
+    __host__ __device__ int32_t* src_of(int slot, int u) const { return src + ((size_t)slot * units + u) * tau; }
+    __host__ __device__ int32_t* count_of(int slot, int u) const { return count + (size_t)slot * units + u; }
+};
+
+// Where decode_attend reads K/V rows: unit u, slot s, row r -> base + ((u * unit_stride) +
+// s * slot_stride + r) * d.  Device residency: the caller's K/V (unit_stride = L, slot_stride = 0,
+// rows = context tokens).  Host residency: the HBM working set (unit_stride = 2*tau,
+// slot_stride = tau, rows = gathered positions).
+struct KvSrc {
+    const __nv_bfloat16* K;
+    const __nv_bfloat16* V;
+    long long unit_stride, slot_stride;
+};
 constexpr int kNumSMs = 148;
 
 // Per-layer device state.  Sizes use the ctx shard: B = batch_count, G = kv_head_count,
@@ -27,13 +54,16 @@ struct LayerState {
     float* Sq = nullptr;               // [B][Hq][d]       running query sum of Q_s (Eq. 2)
     int32_t* cnt = nullptr;            // [B]              |Q_s|
     float* scores = nullptr;           // [B][G][Smax]     last step's similarity scores
-    int32_t* sel_ids = nullptr;        // [B][G][tau]      ascending selected sentence ids
-    int32_t* sel_tokoff = nullptr;     // [B][G][tau+1]    prefix sums of selected lengths
-    int32_t* sel_src = nullptr;        // [B][G][tau]      first context token of each selected sentence
-    int32_t* sel_count = nullptr;      // [B][G]
-    // host residency (P3)
-    __nv_bfloat16* Kh = nullptr;       // pinned host [B][G][L][d]
+    SelBufs sel{};                     // double-buffered selection (see SelBufs)
+    // host residency (P3 + D3)
+    __nv_bfloat16* Kh = nullptr;       // pinned, mapped host [B][G][L][d] (full K/V)
     __nv_bfloat16* Vh = nullptr;
+    size_t host_bytes = 0;             // bytes of each of Kh, Vh
+    __nv_bfloat16* wsK = nullptr;      // HBM working set [B][G][2][tau][d] (gathered rows, 2 slots)
+    __nv_bfloat16* wsV = nullptr;
+    unsigned long long* ledger = nullptr;  // device: host->HBM bytes fetched by the gathers (cumulative)
+    cudaEvent_t offload_done = nullptr;    // D2H copies of this layer completed
+    bool host_ready = false;
 };
 
 }  // namespace skv
@@ -105,14 +135,19 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
 // D2: budgeted selection + Q_s state update (Sq += q or reset).
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B, int G, int grp,
                           int d, int Smax, int tau, const __nv_bfloat16* q, const int32_t* input_token,
-                          const int32_t* bset, int nb, float* Sq, int32_t* cnt, int32_t* sel_ids,
-                          int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count, int32_t* out_ids,
-                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
+                          const int32_t* bset, int nb, float* Sq, int32_t* cnt, SelBufs sel, bool src_gathered,
+                          int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
+
+// D3 + D4 with host residency: selected sentences also selected at the previous step are re-read
+// from the previous HBM working-set slot, the others from the mapped pinned host store (PCIe); the
+// staged rows are written through to the current slot; host bytes are added to *ledger.
+cudaError_t launch_attend_host(const __nv_bfloat16* q, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L,
+                               __nv_bfloat16* wsK, __nv_bfloat16* wsV, int B, int G, int grp, int d, SelBufs sel,
+                               unsigned long long* ledger, float* out, cudaStream_t st);
 
 // D3 + D4: split-K attention over the selected sentences' tokens (device residency).
-cudaError_t launch_attend(const __nv_bfloat16* q, const __nv_bfloat16* K, const __nv_bfloat16* V, int B, int G,
-                          int grp, int d, int L, const int32_t* sel_src, const int32_t* sel_tokoff,
-                          const int32_t* sel_count, int tau, float* out, cudaStream_t st);
+cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, float* out,
+                          cudaStream_t st);
 
 int attend_chunk_tokens(int d);
 
@@ -124,9 +159,7 @@ bool fused_supported(int d, int grp, int Smax, int tau);
 cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, int off_stride, const int32_t* S,
                                        int B, int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
                                        const int32_t* input_token, const int32_t* bset, int nb, float* Sq,
-                                       int32_t* cnt, const __nv_bfloat16* K, const __nv_bfloat16* V, int L,
-                                       int32_t* sel_ids, int32_t* sel_tokoff, int32_t* sel_src, int32_t* sel_count,
-                                       int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, float* out,
-                                       cudaStream_t st);
+                                       int32_t* cnt, KvSrc kv, SelBufs sel, int32_t* out_ids, int32_t* out_count,
+                                       int32_t* out_tokens, float* out, cudaStream_t st);
 
 }  // namespace skv

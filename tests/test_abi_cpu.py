@@ -71,6 +71,7 @@ def _create_status(**kw):
     (dict(head_dim=96), 3),                    # unsupported head dim
     (dict(q_heads=24, kv_heads=2), 3),         # grp = 12 unsupported
     (dict(obs_window=32), 3),                  # NEXT-1 not built
+    (dict(residency=1, semantic_factor=1.5), 1),  # host residency needs r >= 2
 ])
 def test_create_rejects_bad_configs(kw, status):
     assert _create_status(**kw) == status

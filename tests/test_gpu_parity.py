@@ -186,3 +186,57 @@ def test_fused_select_attend_kernel_parity_subprocess(cuda_device):
                         "-k", "(step or ties or all_equal or tau_cap or many_one) and not subprocess"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# --------------------------------------------------------------------------- host residency (P3 + D3)
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+@pytest.mark.parametrize("seed,Hq,G,d,B,L,tau,median", [
+    (0, 8, 2, 64, 1, 4096, 256, 20.0),      # configs[0] shapes
+    (11, 16, 2, 128, 3, 5003, 512, 25.0),   # ragged, grp = 8
+])
+def test_host_residency_parity(cuda_device, mode, seed, Hq, G, d, B, L, tau, median):
+    """Full K/V offloaded to pinned host (P3); each step gathers from the HBM working set (previous
+    selection) and from host memory (misses).  Results must equal the oracle exactly as in device
+    residency: any stale working-set row or bad host fetch shows up in O."""
+    import paper_2504_00970_b200 as skvlib
+
+    M, steps = 2, 30
+    toks, _, Ks, Vs, qs, script = make_case(seed, B, M, Hq, G, d, L, tau, steps, median=median)
+    skv = _skv(B, M, Hq, G, d, L, tau, residency=skvlib.SKV_KV_HOST)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
+    assert st["max_abs"] <= ATOL
+
+
+def test_host_residency_transfer_ledger(cuda_device):
+    """Ledger pins (SURVEY 8(c) D3 host): the first step fetches every
+    selected byte from host memory; repeating the same query (no boundary) leaves the selection
+    unchanged, so the next step fetches 0 bytes; a different topic fetches some."""
+    import paper_2504_00970_b200 as skvlib
+
+    B, Hq, G, d, L, tau = 2, 8, 2, 128, 6000, 512
+    toks, topics = synth.prompts(2, B, L, median=25.0)
+    K, V = synth.kv_layer(2, 0, topics, G, d)
+    skv = _skv(B, 1, Hq, G, d, L, tau, residency=skvlib.SKV_KV_HOST)
+    skv.prefill_compress(0, from_bits(K, cuda_device), from_bits(V, cuda_device),
+                         torch.from_numpy(toks).to(cuda_device), synth.BOUNDARY_IDS)
+    tgt = np.array([3, 9], np.int32)
+    q1 = from_bits(synth.queries(2, 0, 0, tgt, Hq, G, d), cuda_device)
+    q2 = from_bits(synth.queries(2, 0, 1, (tgt + 20) % synth.N_TOPICS, Hq, G, d), cuda_device)
+    no_b = torch.full((B,), 300, dtype=torch.int32, device=cuda_device)
+    ntok = torch.empty((B, G), dtype=torch.int32, device=cuda_device)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=cuda_device)
+    row = d * 2 * 2  # K + V bytes per token
+    skv.decode_step(0, q1, no_b, out, sel_tokens=ntok)
+    first = skv.host_fetch_bytes(0)
+    assert first == int(ntok.sum()) * row > 0
+    ids1 = torch.empty((B, G, tau), dtype=torch.int32, device=cuda_device)
+    skv.decode_step(0, q1, no_b, out, sel_ids=ids1)  # qbar = (q1 + q1) / 2 = q1: same selection
+    assert skv.host_fetch_bytes(0) == first
+    reset = torch.full((B,), int(synth.BOUNDARY_IDS[0]), dtype=torch.int32, device=cuda_device)
+    skv.decode_step(0, q1, reset, out)  # still q1; resets Q_s afterwards
+    assert skv.host_fetch_bytes(0) == first
+    skv.decode_step(0, q2, no_b, out, sel_tokens=ntok)  # qbar = q2 (fresh sentence): new topic
+    assert skv.host_fetch_bytes(0) > first
