@@ -13,8 +13,10 @@ batch 4.  value = tokens/s = sequences decoded per second (B per step) over all 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 8b-128k] [--impl ours|reference]
 
-Multi-GPU (torchrun): weak scaling by batch -- each rank decodes its own batch of sequences with
-all KV heads (independent units; no collective on the data path).
+Multi-GPU (torchrun, one process per GPU): --shard heads (default) splits the KV heads (then the
+batch) of the fixed global batch over the ranks -- strong scaling -- with one NCCL all-gather of the
+per-head outputs per layer inside the captured step; --shard batch gives every rank its own batch
+(weak scaling, device residency only: the host store would not fit the box's RAM at 8 ranks).
 """
 from __future__ import annotations
 
@@ -53,6 +55,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--shard", choices=["heads", "batch"], default="heads")
     ap.add_argument("--residency", choices=["device", "host"], default=None,
                     help="K/V residency (default: host for 8b-128k, which configs[2] specifies, else device)")
     return ap.parse_args()
@@ -178,42 +181,46 @@ def main():
     cfg = dict(CONFIGS[args.config])
     B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
     hbm_peak, peak_kind = peaks()
-
-    import torch
-
-    import synth
-
     if args.impl == "reference":
         return reference_arm(args, cfg, rank, world)
 
+    import torch
     import torch.distributed as dist
 
+    import synth
+
+    if args.shard == "batch" and residency == "host" and world > 1:
+        raise SystemExit("--shard batch with host residency would pin world x the host store; use --shard heads")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import paper_2504_00970_b200 as skvlib
+    from paper_2504_00970_b200 import parallel
 
-    # ---------------- inputs (seeded, synthetic; this rank's batch shard = global b in [rank*B, rank*B+B))
-    toks, topics = zip(*(synth.token_stream(SEED, rank * B + b, L, cfg["median"]) for b in range(B)))
+    GB = B * world if args.shard == "batch" else B  # global batch
+    plan = parallel.plan(GB, G, Hq, world, rank, "batch" if args.shard == "batch" else "heads")
+    Bl, Gl, Hl = plan.batch_count, plan.kv_head_count, plan.q_head_count
+    b0, g0, h0 = plan.batch_begin, plan.kv_head_begin, plan.q_head_begin
+
+    # ---------------- inputs (seeded, synthetic; this rank's shard of sequences and heads)
+    toks, topics = zip(*(synth.token_stream(SEED, b0 + b, L, cfg["median"]) for b in range(Bl)))
     toks, topics = np.stack(toks), np.stack(topics)
     tok_dev = torch.from_numpy(toks).to(dev)
     top_dev = torch.from_numpy(topics).to(dev)
     host = residency == "host"
-    skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
-                            device=local, residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE)
+    skv = skvlib.SentenceKV(layers=M, head_dim=d, max_context=L, token_budget=tau, device=local,
+                            residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE, **plan.ctx_kwargs())
     # ---------------- K/V generation + prefill (P1 segmentation, P2 embeddings, P3 offload in host
     # residency), per layer; in host residency the device K/V of a layer is freed once offloaded
     # (layers 0, 1 are kept for the CPU-oracle baseline).
     Ks, Vs, Cs = [], [], []
-    t_gen = 0.0
-    prefill_ms = 0.0
-    offload_s = 0.0
+    t_gen = prefill_ms = offload_s = 0.0
     skv.set_profiling(True)
     for l in range(M):
         t0 = time.perf_counter()
-        K, V, c = synth.kv_layer_torch(SEED + 1000 * rank, l, top_dev, G, d, device=dev)
+        K, V, c = synth.kv_layer_torch(SEED, l, top_dev, G, d, device=dev, b_begin=b0, g_begin=g0, g_count=Gl)
         torch.cuda.synchronize()
         t_gen += time.perf_counter() - t0
         pf0 = torch.cuda.Event(enable_timing=True)
@@ -228,7 +235,7 @@ def main():
             offload_s += time.perf_counter() - t0
         torch.cuda.synchronize()
         prefill_ms += pf0.elapsed_time(pf1)
-        keep = (not host) or l < 2
+        keep = (not host) or (l < 2 and world == 1)
         Ks.append(K if keep else None)
         Vs.append(V if keep else None)
         Cs.append(c)
@@ -236,40 +243,61 @@ def main():
     prof_prefill = skv.profile_read()
     skv.set_profiling(False)
     S = skv.sentence_counts()
-    kv_bytes_total = 2 * B * G * L * d * 2 * M
+    kv_bytes_total = 2 * Bl * Gl * L * d * 2 * M
 
-    # ---------------- decode inputs: POOL distinct steps
-    script, target = synth.decode_script(SEED + rank, B, POOL)
+    # ---------------- decode inputs: POOL distinct steps (queries of the full head set, sliced)
+    script, target = synth.decode_script(SEED, GB, POOL)
+    script, target = script[:, b0:b0 + Bl].copy(), target[:, b0:b0 + Bl].copy()
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
     tgt = torch.from_numpy(target).to(dev)
-    qpool = [[synth.queries_torch(gen, Cs[l], tgt[p], Hq, G, d).contiguous() for l in range(M)] for p in range(POOL)]
+    qpool = []
+    for p in range(POOL):
+        row = []
+        for l in range(M):
+            gen.manual_seed(1234 + 7919 * p + 104729 * l)
+            row.append(synth.queries_torch(gen, Cs[l], tgt[p], Hq, G, d)[:, h0:h0 + Hl].contiguous())
+        qpool.append(row)
     itok = [torch.from_numpy(script[p]).to(dev) for p in range(POOL)]
-    outs = [torch.empty((B, Hq, d), dtype=torch.float32, device=dev) for _ in range(M)]
-    sel_tok = [torch.zeros((B, G), dtype=torch.int32, device=dev) for _ in range(M)]
+    outs = [torch.empty((Bl, Hl, d), dtype=torch.float32, device=dev) for _ in range(M)]
+    gath = [torch.empty((world, Bl, Hl, d), dtype=torch.float32, device=dev) for _ in range(M)] if world > 1 else None
+    sel_tok = [torch.zeros((Bl, Gl), dtype=torch.int32, device=dev) for _ in range(M)]
 
     def step(p, with_tokens=False):
         for l in range(M):
             skv.decode_step(l, qpool[p][l], itok[p], outs[l], sel_tokens=sel_tok[l] if with_tokens else None)
+            if world > 1:  # the one exchange: all-gather of the per-head outputs of the layer
+                parallel.all_gather_outputs(outs[l], plan, gathered=gath[l])
 
-    # eager warm-up, then one CUDA graph per pool step
+    # eager warm-up, then one CUDA graph per pool step (eager fallback if capture fails)
     for p in range(POOL):
         step(p)
     torch.cuda.synchronize()
-    stream = torch.cuda.Stream(device=dev)
     graphs = []
-    with torch.cuda.stream(stream):
-        for p in range(POOL):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                step(p)
-            graphs.append(g)
-    torch.cuda.synchronize()
+    try:
+        stream = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(stream):
+            for p in range(POOL):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    step(p)
+                graphs.append(g)
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001 -- report and time the eager step instead
+        print(f"[bench] CUDA graph capture failed ({type(e).__name__}: {e}); timing eager steps", file=sys.stderr)
+        graphs = []
+        torch.cuda.synchronize()
+
+    def run(k):
+        if graphs:
+            graphs[k % POOL].replay()
+        else:
+            step(k % POOL)
+
     for w in range(args.warmup):
-        graphs[w % POOL].replay()
+        run(w)
     torch.cuda.synchronize()
 
-    # ---------------- timed region: K graph replays (device time, CUDA events, max over ranks)
+    # ---------------- timed region: K steps (device time, CUDA events, max over ranks)
     ledger0 = sum(skv.host_fetch_bytes(l) for l in range(M)) if host else 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -280,7 +308,7 @@ def main():
         cur = torch.cuda.current_stream()
         e0.record(cur)
         for k in range(args.steps):
-            graphs[k % POOL].replay()
+            run(k)
         e1.record(cur)
         torch.cuda.synchronize()
     if world > 1:
@@ -291,18 +319,17 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = B * world / (ms_step / 1e3)
+    value = GB / (ms_step / 1e3)
     host_step_bytes = (sum(skv.host_fetch_bytes(l) for l in range(M)) - ledger0) / args.steps if host else 0
 
     # ---------------- per-kernel durations (profiled eager pass, events on the launching stream)
     # A spin kernel queued first lets the host enqueue the whole profiled pass ahead of the GPU,
     # so the events bracket back-to-back kernels rather than host launch gaps.
     skv.set_profiling(True)
-    nprof = POOL
     tok_hist = []
     torch.cuda.synchronize()
     torch.cuda._sleep(int(2e9 * 0.05))  # ~50 ms head start
-    for p in range(nprof):
+    for p in range(POOL):
         step(p, with_tokens=True)
         tok_hist.append(torch.stack(sel_tok).sum())
     torch.cuda.synchronize()
@@ -310,14 +337,14 @@ def main():
     prof = skv.profile_read()
     skv.set_profiling(False)
     S_tot = sum(S)
-    # algorithmic bytes per launch (one layer, all B x G units); DESIGN.md "Measurement"
-    score_bytes = G * S_tot * d * 2 + B * Hq * d * (2 + 4) + B * G * S_tot * 4  # E + q,Sq + scores written
+    # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md "Measurement"
+    score_bytes = Gl * S_tot * d * 2 + Bl * Hl * d * (2 + 4) + Bl * Gl * S_tot * 4  # E + q,Sq + scores written
     nlaunch = max(1, prof["fused"][1] or prof["attend"][1])
     kv_bytes = ntok_sum * d * 2 * 2 / nlaunch  # selected K and V rows
-    fused_bytes = kv_bytes + B * G * S_tot * (4 + 4) + B * Hq * d * (2 + 4 * 2 + 4)  # + scores/offsets, q, Sq, O
+    sel_bytes = Bl * Gl * S_tot * (4 + 4) + Bl * Hl * d * (2 + 4 * 2)  # scores + offsets read, q + Sq
     kern = {}
-    for name, nbytes in (("score", score_bytes), ("fused", fused_bytes), ("select", fused_bytes - kv_bytes),
-                         ("attend", kv_bytes)):
+    for name, nbytes in (("score", score_bytes), ("fused", kv_bytes + sel_bytes + Bl * Hl * d * 4),
+                         ("select", sel_bytes), ("attend", kv_bytes + Bl * Hl * d * (2 + 4))):
         ms, n = prof[name]
         if not n:
             continue
@@ -328,31 +355,32 @@ def main():
     for name in kern:
         kern[name]["share"] = round(prof[name][0] / tot_prof, 3)
     dom = max(kern, key=lambda k: prof[k][0])
-    step_bytes = (score_bytes + fused_bytes) * M
+    step_bytes = (score_bytes + sel_bytes + kv_bytes + Bl * Hl * d * 4) * M
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic,
-                "peak_kind": peak_kind,
-                "per_unit": "score: G*S*d*2 B (bf16 E) + q/Sq + scores; fused select+attend: sum(ntok)*d*2*2 B "
-                            "(selected K,V rows) + scores/offsets + q/Sq/O"}
+                "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "per_unit": "score: G*S*d*2 B (bf16 E) + q/Sq + scores; attend: sum(ntok)*d*2*2 B (selected K,V "
+                            "rows) + q + O; select: scores + offsets + q/Sq"}
 
     # ---------------- end to end through the public API with host buffers
-    qhost = [torch.stack(qpool[p]).cpu().pin_memory() for p in range(POOL)]  # [M][B][Hq][d]
+    qhost = [torch.stack(qpool[p]).cpu().pin_memory() for p in range(POOL)]  # [M][Bl][Hl][d]
     thost = [t.cpu().pin_memory() for t in itok]
-    ohost = torch.empty((M, B, Hq, d), dtype=torch.float32).pin_memory()
-    qdev = torch.empty((M, B, Hq, d), dtype=torch.bfloat16, device=dev)
-    tdev = torch.empty((B,), dtype=torch.int32, device=dev)
-    odev = torch.empty((M, B, Hq, d), dtype=torch.float32, device=dev)
+    ohost = torch.empty((M, Bl, Hl, d), dtype=torch.float32).pin_memory()
+    qdev = torch.empty((M, Bl, Hl, d), dtype=torch.bfloat16, device=dev)
+    tdev = torch.empty((Bl,), dtype=torch.int32, device=dev)
+    odev = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
 
     def e2e_step(p):
         qdev.copy_(qhost[p], non_blocking=True)
         tdev.copy_(thost[p], non_blocking=True)
         for l in range(M):
             skvlib.sentencekv_decode_step(skv.ctx, l, qdev[l], tdev, odev[l])
+            if world > 1:
+                parallel.all_gather_outputs(odev[l], plan, gathered=gath[l])
         ohost.copy_(odev, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
@@ -372,50 +400,50 @@ def main():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": round(B * world / (e2e_ms / 1e3), 2), "unit": "tokens/s", "ms_per_step": round(e2e_ms, 4),
-           "h2d_bytes_per_step": int(qhost[0].numel() * 2 + B * 4), "d2h_bytes_per_step": int(ohost.numel() * 4)}
+    e2e = {"value": round(GB / (e2e_ms / 1e3), 2), "unit": "tokens/s", "ms_per_step": round(e2e_ms, 4),
+           "h2d_bytes_per_step": int(qhost[0].numel() * 2 + Bl * 4), "d2h_bytes_per_step": int(ohost.numel() * 4)}
 
     # ---------------- CPU oracle baseline (rank 0, N=1 only; bounded sample)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         layers_sample = [0, 1] if M > 1 else [0]
-        units = [(b, g) for b in range(B) for g in range(G)]
+        units = [(b, g) for b in range(Bl) for g in range(Gl)]
         Kh = {l: Ks[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
         Vh = {l: Vs[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
         qs_h = [[qpool[p][l].view(torch.int16).cpu().numpy().view(np.uint16) if l in layers_sample else None
                  for l in range(M)] for p in range(POOL)]
         n_steps = 2
         per_unit, threads = oracle_sample(cfg, toks, Kh, Vh, qs_h, script, units, layers_sample, n_steps)
-        step_s = per_unit * B * G * M
-        cpu = {"value": round(B / step_s, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
+        step_s = per_unit * Bl * Gl * M
+        cpu = {"value": round(Bl / step_s, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
                "ms_per_step": round(step_s * 1e3, 1),
-               "sample": f"{n_steps} steps x {len(layers_sample)} of {M} layers x all {B * G} (b,g) units, "
+               "sample": f"{n_steps} steps x {len(layers_sample)} of {M} layers x all {Bl * Gl} (b,g) units, "
                          f"select+attend per unit timed, extrapolated to {M} layers"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in / fp32 acc (selection canonical fp32)",
+            "scaling": "weak" if args.shard == "batch" else "strong", "vs_baseline": None,
+            "dtype": "bf16 in / fp32 acc (selection canonical fp32)",
             "data": "synthetic (seeded token streams with punctuation boundaries, topic-structured K/V/q)",
-            "config": {"workload": args.config, "batch_per_gpu": B, "global_batch": B * world, "layers": M,
-                       "q_heads": Hq, "kv_heads": G, "head_dim": d, "context": L, "token_budget": tau,
-                       "sentences": S,
+            "config": {"workload": args.config, "global_batch": GB, "layers": M, "q_heads": Hq, "kv_heads": G,
+                       "head_dim": d, "context": L, "token_budget": tau, "sentences_rank0": S,
                        "residency": "pinned host K/V + HBM working set" if host else "device (HBM)",
-                       "parallelism": f"batch-sharded x{world}",
-                       "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB read per step (L2 126 MB)",
-                       "cuda_graph": True},
+                       "parallelism": f"{plan.batch_shards} batch x {plan.head_shards} KV-head shards",
+                       "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB read per step per GPU (L2 126 MB)",
+                       "cuda_graph": bool(graphs)},
             "roofline": roofline,
             "kernels": kern,
-            "step_bytes": int(step_bytes),
-            "step_gbs": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
+            "step_bytes_per_gpu": int(step_bytes),
+            "step_gbs_per_gpu": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
             "e2e": e2e,
-            "gpu_launches": 2 * M * args.steps,
+            "gpu_launches": (3 * M if prof["select"][1] else 2 * M) * args.steps,
             "clocks": clk.summary(),
-            "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(B * G * L * d * 2 * M),
+            "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(Bl * Gl * L * d * 2 * M),
                         "segment_ms": round(prof_prefill["segment"][0], 3),
                         "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4),
-                        "compress_gbs": round(B * G * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
+                        "compress_gbs": round(Bl * Gl * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
             "host_residency": {"host_bytes_per_step": int(host_step_bytes),
                                "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
                                "offload_gbs_p3": round(kv_bytes_total / offload_s / 1e9, 2) if offload_s else None,
@@ -431,35 +459,30 @@ def main():
 def reference_arm(args, cfg, rank, world):
     """--impl reference: the CPU oracle as it stands, on this arm's config, metric and unit.
     Each step = a bounded sample (4 (b,g) units of one layer, select + attend), extrapolated to
-    the full step (all units, all layers).  Rank 0 only."""
+    the full step (all units, all layers).  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
     import synth
 
     B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
     toks, topics = synth.prompts(SEED, 1, L, cfg["median"])
-    # host K/V for one (b=0) sequence, G heads, one layer (numpy generator)
-    K, V = synth.kv_layer(SEED, 0, topics, G, d)
-    script, target = synth.decode_script(SEED, 1, max(1, args.steps + args.warmup))
+    K, V = synth.kv_layer(SEED, 0, topics, G, d)  # host K/V of one sequence, one layer
+    script, target = synth.decode_script(SEED, 1, 8)
     units = [(0, g) for g in range(min(4, G))]
     qs = [[synth.queries(SEED, 0, s, target[s], Hq, G, d)] for s in range(8)]
-    # warm-up (W steps), then K timed steps
-    per_w, threads = oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], max(1, args.warmup))
+    oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], max(1, args.warmup))  # warm-up
     per_unit, threads = oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], args.steps)
-    step_s = per_unit * B * G * M
-    value = B / step_s
+    GB = B * world if args.shard == "batch" else B
+    step_s = per_unit * GB * G * M
+    value = GB / step_s
     cpu = {"value": round(value, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
            "sample": f"each step: {len(units)} (b,g) units of 1 layer (select+attend), extrapolated to "
-                     f"{B * G} units x {M} layers"}
+                     f"{GB * G} units x {M} layers"}
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 canonical / fp64",
-            "data": "synthetic", "config": {"workload": args.config, "global_batch": B * world, "context": L,
-                                            "token_budget": tau},
-            "host_residency": {"host_bytes_per_step": int(host_step_bytes),
-                               "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
-                               "offload_gbs_p3": round(kv_bytes_total / offload_s / 1e9, 2) if offload_s else None,
-                               "working_set_tokens_per_unit": 2 * tau} if host else None,
+            "higher_is_better": True, "scaling": "weak" if args.shard == "batch" else "strong",
+            "vs_baseline": None, "dtype": "fp32 canonical / fp64", "data": "synthetic",
+            "config": {"workload": args.config, "global_batch": GB, "context": L, "token_budget": tau},
             "cpu_baseline": cpu,
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

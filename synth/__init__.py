@@ -126,24 +126,29 @@ def queries(seed: int, layer: int, step: int, target: np.ndarray, Hq: int, G: in
 # ------------------------------------------------------------- GPU-side generation (bench)
 
 
-def kv_layer_torch(seed: int, layer: int, topics, G: int, d: int, device="cuda"):
-    """Same recipe as kv_layer, drawn on the GPU with a seeded torch generator (for the
-    full-size bench configs where numpy generation would take minutes).  topics: int64/int32
-    tensor [B][L] on `device`.  Returns bf16 K, V [B][G][L][d]."""
+def kv_layer_torch(seed: int, layer: int, topics, G: int, d: int, device="cuda", b_begin: int = 0,
+                   g_begin: int = 0, g_count: int = None):
+    """Same recipe as kv_layer, drawn on the GPU with seeded torch generators (for the full-size
+    bench configs where numpy generation would take minutes).  topics: int tensor [B_loc][L] of the
+    global sequences b_begin .. b_begin + B_loc; returns bf16 K, V [B_loc][g_count][L][d] for KV
+    heads g_begin .. g_begin + g_count and the layer's centroids [G][T][d].  Every (layer, b, g)
+    has its own generator, so any shard layout draws the same numbers."""
     import torch
 
+    g_count = G - g_begin if g_count is None else g_count
     gen = torch.Generator(device=device)
-    gen.manual_seed((seed * 1_000_003 + layer * 7919 + 0x4B56) & 0x7FFFFFFFFFFFFFFF)
-    B, L = topics.shape
+    gen.manual_seed((seed * 1_000_003 + layer * 7919 + 0xCE27) & 0x7FFFFFFFFFFFFFFF)
     c = torch.randn((G, N_TOPICS, d), generator=gen, device=device, dtype=torch.float32)
-    K = torch.empty((B, G, L, d), dtype=torch.bfloat16, device=device)
-    V = torch.empty((B, G, L, d), dtype=torch.bfloat16, device=device)
+    B, L = topics.shape
+    K = torch.empty((B, g_count, L, d), dtype=torch.bfloat16, device=device)
+    V = torch.empty((B, g_count, L, d), dtype=torch.bfloat16, device=device)
     tl = topics.long()
-    for b in range(B):
-        for g in range(G):
-            noise = torch.randn((L, d), generator=gen, device=device, dtype=torch.float32)
-            K[b, g] = (c[g][tl[b]] + noise).to(torch.bfloat16)
-            V[b, g] = torch.randn((L, d), generator=gen, device=device, dtype=torch.float32).to(torch.bfloat16)
+    for bi in range(B):
+        for gi in range(g_count):
+            b, g = b_begin + bi, g_begin + gi
+            gen.manual_seed((seed * 1_000_003 + layer * 7919 + b * 131 + g * 17 + 0x4B56) & 0x7FFFFFFFFFFFFFFF)
+            K[bi, gi] = (c[g][tl[bi]] + torch.randn((L, d), generator=gen, device=device)).to(torch.bfloat16)
+            V[bi, gi] = torch.randn((L, d), generator=gen, device=device).to(torch.bfloat16)
     return K, V, c
 
 
