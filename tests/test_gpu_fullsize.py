@@ -1,0 +1,78 @@
+"""Full-size parity at BASELINE.json configs[2] (Llama-3.1-8B shapes, 128K context, tau=2048, batch 4,
+K/V offloaded to pinned host) in the launch configuration bench.py times (sentencekv_decode_step):
+every sequence's segmentation is compared in full; embeddings, scores, selections and attention
+outputs on a seeded sample of (b, g) units that the oracle computes one by one."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.gpu_harness import ATOL, to_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("residency", ["host", "device"])
+def test_config2_sampled_units(cuda_device, residency):
+    import paper_2504_00970_b200 as skvlib
+
+    B, Hq, G, d, L, tau, steps, layer = 4, 32, 8, 128, 131072, 2048, 3, 1
+    grp = Hq // G
+    dev = cuda_device
+    toks, topics = synth.prompts(0, B, L, 25.0)
+    skv = skvlib.SentenceKV(batch=B, layers=2, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L,
+                            token_budget=tau,
+                            residency=skvlib.SKV_KV_HOST if residency == "host" else skvlib.SKV_KV_DEVICE)
+    top = torch.from_numpy(topics).to(dev)
+    KV = [synth.kv_layer_torch(0, l, top, G, d, device=dev) for l in range(2)]
+    for l in range(2):
+        skv.prefill_compress(l, KV[l][0], KV[l][1], torch.from_numpy(toks).to(dev) if l == 0 else None,
+                             synth.BOUNDARY_IDS if l == 0 else None)
+    skv.sync()
+    units = [(0, 0), (1, 3), (2, 5), (3, 7)]
+    Kh = {u: to_bits(KV[layer][0][u[0], u[1]]) for u in units}
+    Vh = {u: to_bits(KV[layer][1][u[0], u[1]]) for u in units}
+
+    # P1: every prompt, bit-exact
+    S = skv.sentence_counts()
+    offs = skv.offsets().cpu().numpy()
+    off_o = [oracle.segment(toks[b], synth.BOUNDARY_IDS, tau) for b in range(B)]
+    for b in range(B):
+        assert np.array_equal(offs[b, : S[b] + 1], off_o[b])
+    # P2: sampled units, bit-exact
+    E = to_bits(skv.embeddings(layer))
+    E_o = {u: oracle.embed(Kh[u], off_o[u[0]]) for u in units}
+    for (b, g) in units:
+        assert np.array_equal(E[b, g, : S[b]], E_o[(b, g)])
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    script, target = synth.decode_script(0, B, steps)
+    Sq = np.zeros((B, Hq, d), np.float32)
+    cnt = np.zeros((B, 1), np.int32)
+    ids = torch.empty((B, G, tau), dtype=torch.int32, device=dev)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+    bset = set(synth.BOUNDARY_IDS.tolist())
+    for s in range(steps):
+        q = synth.queries_torch(gen, KV[layer][2], torch.from_numpy(target[s]).to(dev), Hq, G, d).contiguous()
+        it = torch.from_numpy(script[s]).to(dev)
+        skv.decode_step(0, synth.queries_torch(gen, KV[0][2], torch.from_numpy(target[s]).to(dev), Hq, G, d)
+                        .contiguous(), it, torch.empty_like(out))  # layer 0 runs too, as in a real step
+        skv.decode_step(layer, q, it, out, sel_ids=ids)
+        qb = to_bits(q)
+        sc = skv.scores(layer).cpu().numpy()
+        got_ids = ids.cpu().numpy()
+        O = out.cpu().numpy()
+        for b in sorted({u[0] for u in units}):
+            qbar = oracle.qs_append_mean(Sq[b], cnt[b], qb[b])
+            for g in [u[1] for u in units if u[0] == b]:
+                qt = oracle.group_query(qbar, grp, g)
+                sc_o = oracle.score(qt, E_o[(b, g)])
+                assert np.array_equal(sc[b, g, : S[b]].view(np.uint32), sc_o.view(np.uint32)), (s, b, g)
+                sel, _ = oracle.select(sc_o, off_o[b], tau)
+                assert np.array_equal(got_ids[b, g, : len(sel)], sel) and np.all(got_ids[b, g, len(sel):] == -1)
+                O_o = oracle.attend(qb[b, g * grp:(g + 1) * grp], Kh[(b, g)], Vh[(b, g)], off_o[b], sel)
+                assert np.max(np.abs(O[b, g * grp:(g + 1) * grp] - O_o)) <= ATOL, (s, b, g)
+            if int(script[s, b]) in bset:
+                oracle.qs_reset(Sq[b], cnt[b])
