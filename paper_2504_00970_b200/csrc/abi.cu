@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -83,6 +84,11 @@ void free_layer_prompt(skv::LayerState& ls) {
     free_sel(ls.sel);
     dfree(ls.wsK);
     dfree(ls.wsV);
+    dfree(ls.lk_counters);
+    dfree(ls.lk_part_ml);
+    dfree(ls.lk_part_o);
+    dfree(ls.lk_cand);
+    dfree(ls.lk_cand_count);
 }
 
 void free_host_store(skv::LayerState& ls) {
@@ -134,6 +140,22 @@ void prof_end(skv_ctx* c, int kind, cudaEvent_t a, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool skv::layer_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_LAYER");  // opt-in: slower than the three kernels on B200
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+static int layer_group() {
+    static const int gsz = [] {
+        const char* e = getenv("SKV_LAYER_GROUP");
+        return e ? std::max(1, atoi(e)) : 8;
+    }();
+    return gsz;
+}
 
 bool skv::fused_enabled() {
     static const bool on = [] {
@@ -194,9 +216,9 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
     cudaError_t e = cudaSuccess;
     for (auto& ls : c->layer) {
         if (e == cudaSuccess) e = dalloc(&ls.Sq, (size_t)c->B * c->Hq * c->d);
-        if (e == cudaSuccess) e = dalloc(&ls.cnt, (size_t)c->B);
+        if (e == cudaSuccess) e = dalloc(&ls.cnt, (size_t)c->B * c->G);
         if (e == cudaSuccess) e = cudaMemset(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d);
-        if (e == cudaSuccess) e = cudaMemset(ls.cnt, 0, sizeof(int32_t) * c->B);
+        if (e == cudaSuccess) e = cudaMemset(ls.cnt, 0, sizeof(int32_t) * c->B * c->G);
     }
     if (e == cudaSuccess && cfg.residency == SKV_KV_HOST) {
         e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
@@ -231,6 +253,7 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     }
     dfree(c->S_dev);
     dfree(c->bset);
+    dfree(c->lk_items);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -272,6 +295,14 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
             SKV_CUDA(c, dalloc(&ls.wsK, U * 2 * tau * d));
             SKV_CUDA(c, dalloc(&ls.wsV, U * 2 * tau * d));
         }
+        const size_t n_att = (size_t)skv::layer_attend_items((int)tau);
+        SKV_CUDA(c, dalloc(&ls.lk_counters, 3 + 3 * U));
+        SKV_CUDA(c, cudaMemset(ls.lk_counters, 0, sizeof(uint32_t) * (3 + 3 * U)));
+        SKV_CUDA(c, dalloc(&ls.lk_part_ml, U * n_att * 16));
+        SKV_CUDA(c, dalloc(&ls.lk_part_o, U * n_att * 8 * d));
+        const size_t nsm = (size_t)c->lk_n_score_max;
+        SKV_CUDA(c, dalloc(&ls.lk_cand, U * nsm * (size_t)skv::layer_item_sentences((int)d)));
+        SKV_CUDA(c, dalloc(&ls.lk_cand_count, U * nsm));
     }
     c->Smax = Smax;
     return SKV_OK;
@@ -318,10 +349,20 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         SKV_CUDA(c, cudaStreamSynchronize(st));
         int Smax = 1;
         for (int b = 0; b < c->B; ++b) Smax = c->S_host[b] > Smax ? c->S_host[b] : Smax;
-        if (Smax > c->Smax || !c->layer[0].E) {
+        const int nsm = skv::layer_score_items(c->d, Smax);
+        const bool grow = nsm > c->lk_n_score_max;
+        c->lk_n_score_max = std::max(nsm, c->lk_n_score_max);
+        if (Smax > c->Smax || !c->layer[0].E || grow) {
             for (auto& ls : c->layer) free_layer_prompt(ls);
             skv_status s = alloc_prompt_buffers(c, Smax);
             if (s != SKV_OK) return s;
+        }
+        {  // work queue of the per-layer kernel for this prompt's sentence counts
+            const std::vector<int2> items = skv::layer_schedule(c->S_host, c->G, c->d, c->tau, layer_group());
+            dfree(c->lk_items);
+            SKV_CUDA(c, dalloc(&c->lk_items, items.size()));
+            SKV_CUDA(c, cudaMemcpy(c->lk_items, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice));
+            c->lk_n_items = (int)items.size();
         }
         for (auto& ls : c->layer) {
             ls.prefilled = false;
@@ -331,7 +372,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             SKV_CUDA(c, cudaMemsetAsync(ls.sel.count, 0, sizeof(int32_t) * 2 * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.sel.parity, 0, sizeof(int32_t) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
-            SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B, st));
+            SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B * c->G, st));
         }
     }
 
@@ -415,6 +456,53 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    if (skv::layer_enabled() && c->cfg.residency == SKV_KV_DEVICE &&
+        skv::layer_smem_bytes(c->d, c->Smax, c->tau) <= 200 * 1024) {
+        // persistent per-layer kernel: D1-D4 of every unit in one launch
+        skv::LayerArgs a{};
+        a.q = qb;
+        a.input_token = input_token;
+        a.bset = c->bset;
+        a.nb = c->n_bset;
+        a.Sq = ls.Sq;
+        a.cnt = ls.cnt;
+        a.E = ls.E;
+        a.S = c->S_dev;
+        a.off = c->off;
+        a.off_stride = c->off_stride;
+        a.scores = ls.scores;
+        a.sel = ls.sel;
+        a.kv = skv::KvSrc{ls.K, ls.V, c->L, 0};
+        a.out = out;
+        a.out_ids = sel_ids;
+        a.out_count = sel_count;
+        a.out_tokens = sel_tokens;
+        a.items = c->lk_items;
+        a.n_items = c->lk_n_items;
+        a.B = c->B;
+        a.G = c->G;
+        a.Smax = c->Smax;
+        a.tau = c->tau;
+        a.scale_log2 = (float)(1.0 / std::sqrt((double)c->d) * 1.4426950408889634);
+        const int U = c->B * c->G;
+        a.ticket = ls.lk_counters;
+        a.exit_count = ls.lk_counters + 1;
+        a.score_done = ls.lk_counters + 3;
+        a.select_done = ls.lk_counters + 3 + U;
+        a.attend_done = ls.lk_counters + 3 + 2 * U;
+        a.part_ml = ls.lk_part_ml;
+        a.part_o = ls.lk_part_o;
+        a.n_att = skv::layer_attend_items(c->tau);
+        a.cand = ls.lk_cand;
+        a.cand_count = ls.lk_cand_count;
+        a.n_score_max = c->lk_n_score_max;
+        cudaEvent_t pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_layer(a, c->grp, c->d, st));
+        prof_end(c, SKV_K_FUSED, pa, st);
+        c->launches += 1;
+        ls.selected = true;
+        return SKV_OK;
+    }
     if (!skv::fused_enabled() || c->cfg.residency != SKV_KV_DEVICE ||
         !skv::fused_supported(c->d, c->grp, c->Smax, c->tau)) {
         skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
@@ -454,11 +542,20 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
             ls.host_ready = true;
         }
         pa = prof_begin(c, st);
-        SKV_CUDA(c, skv::launch_attend_host(qb, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV, c->B, c->G, c->grp, c->d, ls.sel,
-                                            ls.ledger, out, st));
+        if (skv::mma_enabled())
+            SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
+                                               true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, out, st));
+        else
+            SKV_CUDA(c, skv::launch_attend_host(qb, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV, c->B, c->G, c->grp, c->d,
+                                                ls.sel, ls.ledger, out, st));
     } else {
         pa = prof_begin(c, st);
-        SKV_CUDA(c, skv::launch_attend(qb, skv::KvSrc{ls.K, ls.V, c->L, 0}, c->B, c->G, c->grp, c->d, ls.sel, out, st));
+        const skv::KvSrc kv{ls.K, ls.V, c->L, 0};
+        if (skv::mma_enabled())
+            SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, c->L, nullptr, nullptr, false, c->B, c->G,
+                                               c->grp, c->d, ls.sel, nullptr, out, st));
+        else
+            SKV_CUDA(c, skv::launch_attend(qb, kv, c->B, c->G, c->grp, c->d, ls.sel, out, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;

@@ -150,7 +150,7 @@ fused_select_attend_kernel(const float* __restrict__ scores, const int32_t* __re
         constexpr int E = (GRP * D + kCL - 1) / kCL;
         for (int i = rank * E + tid; i < min(GRP * D, rank * E + E); i += NT)
             Sq[base + i] = reset ? 0.0f : __fadd_rn(Sq[base + i], __bfloat162float(q[base + i]));
-        if (g == 0 && rank == 0 && tid == 0) cnt[b] = reset ? 0 : cnt[b] + 1;
+        if (rank == 0 && tid == 0) cnt[unit] = reset ? 0 : cnt[unit] + 1;
     }
     // ---- (c) keys and lengths of this CTA's sentences -> shared memory; local key range ----
     {

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kScThreads) score_kernel(const __nv_bfloat16* 
     // group query of this step (loads batched, canonical order: qbar_h by IEEE division, then
     // ascending-h fp32 sum)
     if (tid < D) {
-        const float c = (float)(cnt[b] + 1);
+        const float c = (float)(cnt[b * G + g] + 1);
         float sv[GRP], qv[GRP];
 #pragma unroll
         for (int h = 0; h < GRP; ++h) {
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         const size_t base = ((size_t)b * Hq + (size_t)g * grp) * D;
         for (int i = tid; i < grp * D; i += blockDim.x)
             Sq[base + i] = reset ? 0.0f : __fadd_rn(Sq[base + i], __bfloat162float(q[base + i]));
-        if (g == 0 && tid == 0) cnt[b] = reset ? 0 : cnt[b] + 1;
+        if (tid == 0) cnt[b * G + g] = reset ? 0 : cnt[b * G + g] + 1;
     }
     SKV_TRACE_POINT(1);
 

@@ -52,7 +52,7 @@ struct LayerState {
     const __nv_bfloat16* V = nullptr;
     __nv_bfloat16* E = nullptr;        // [B][G][Smax][d]  sentence embeddings (Eq. 1)
     float* Sq = nullptr;               // [B][Hq][d]       running query sum of Q_s (Eq. 2)
-    int32_t* cnt = nullptr;            // [B]              |Q_s|
+    int32_t* cnt = nullptr;            // [B][G]           |Q_s| (one copy per KV-head unit)
     float* scores = nullptr;           // [B][G][Smax]     last step's similarity scores
     SelBufs sel{};                     // double-buffered selection (see SelBufs)
     // host residency (P3 + D3)
@@ -64,6 +64,12 @@ struct LayerState {
     unsigned long long* ledger = nullptr;  // device: host->HBM bytes fetched by the gathers (cumulative)
     cudaEvent_t offload_done = nullptr;    // D2H copies of this layer completed
     bool host_ready = false;
+    // persistent per-layer kernel: work queue + dependency counters + merge workspace
+    uint32_t* lk_counters = nullptr;   // [3 + 3 * units]: ticket, exit_count, pad, score/select/attend done
+    float* lk_part_ml = nullptr;       // [units][n_att][8][2]
+    float* lk_part_o = nullptr;        // [units][n_att][8][d]
+    int4* lk_cand = nullptr;           // [units][n_score_max][NL] local selection candidates
+    int32_t* lk_cand_count = nullptr;  // [units][n_score_max]
 };
 
 }  // namespace skv
@@ -86,6 +92,9 @@ struct skv_ctx {
     int n_bset = 0;
 
     std::vector<skv::LayerState> layer;
+    int2* lk_items = nullptr;          // device work queue of the per-layer kernel (per prompt)
+    int lk_n_items = 0;
+    int lk_n_score_max = 0;            // SCORE items of the longest sequence (per-layer candidate lists)
 
     // kernel profiler: (kind, start, stop) event triples awaiting a read
     bool profiling = false;
@@ -150,6 +159,61 @@ cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int gr
                           cudaStream_t st);
 
 int attend_chunk_tokens(int d);
+
+// ---- persistent per-layer kernel (decode_layer.cu): D1-D4 for every unit in one launch ----
+struct LayerArgs {  // kernel parameter of layer_kernel
+    // inputs / state (device residency)
+    const __nv_bfloat16* q;        // [B][Hq][d]
+    const int32_t* input_token;    // [B]
+    const int32_t* bset;
+    int nb;
+    float* Sq;                     // [B][Hq][d]
+    int32_t* cnt;                  // [B][G]
+    const __nv_bfloat16* E;        // [B][G][Smax][d]
+    const int32_t* S;              // [B]
+    const int32_t* off;            // [B][off_stride]
+    int off_stride;
+    float* scores;                 // [B][G][Smax]
+    SelBufs sel;
+    KvSrc kv;
+    float* out;                    // [B][Hq][d]
+    int32_t* out_ids;              // optional [B][G][tau]
+    int32_t* out_count;            // optional [B][G]
+    int32_t* out_tokens;           // optional [B][G]
+    // schedule
+    const int2* items;             // (kind, unit | index << 16)
+    int n_items;
+    int B, G, Smax, tau;
+    float scale_log2;
+    // scratch (zeroed once; every launch returns it to zero)
+    uint32_t* ticket;
+    uint32_t* exit_count;
+    uint32_t* score_done;          // [units]
+    uint32_t* select_done;         // [units]
+    uint32_t* attend_done;         // [units]
+    float* part_ml;                // [units][n_att][8][2]
+    float* part_o;                 // [units][n_att][8][D]
+    int n_att;                     // ATTEND items per unit
+    int4* cand;                    // [units][n_score_max][NL] (id, key, len, -) local candidates
+    int32_t* cand_count;           // [units][n_score_max]
+    int n_score_max;               // SCORE items of the unit with the most sentences
+};
+
+bool layer_enabled();
+int layer_score_items(int d, int S_b);
+int layer_attend_items(int tau);
+int layer_item_sentences(int d);
+std::vector<int2> layer_schedule(const std::vector<int>& S_host, int G, int d, int tau, int group);
+size_t layer_smem_bytes(int d, int Smax, int tau);
+cudaError_t launch_layer(const LayerArgs& a, int grp, int d, cudaStream_t st);
+
+
+// D3 + D4 on tensor cores (mma.sync m16n8k16, decode_attend_mma.cu), both residencies; default
+// (SKV_ATTEND=fma selects the fp32-FMA kernels above).
+bool mma_enabled();
+cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
+                              int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
+                              SelBufs sel, unsigned long long* ledger, float* out, cudaStream_t st);
 
 // D2 + D3 + D4 fused (one cluster per unit), reading the scores of launch_score.  Opt-in
 // (SKV_FUSED=1): on B200 the cluster-wide selection phases cost more than the separate select

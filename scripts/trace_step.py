@@ -32,12 +32,11 @@ for step in range(4):
         skv.decode_select(l, q, it)
         torch.cuda.synchronize()
         sel = rd("select")
-        skv.decode_attend(l, q, out)
-        torch.cuda.synchronize()
-        att = rd("attend")
+
+        att = [0] * 32
         skv.decode_step(l, q, it, out)
         torch.cuda.synchronize()
-        fus = rd("fused")
+        mma = rd("mma")
     ghz = 1.965
     def show(name, t, slots):
         t0 = t[slots[0]]
@@ -45,5 +44,5 @@ for step in range(4):
     print(f"--- step {step} (us since first stamp)")
     show("score ", sel, [24, 25, 26])
     show("select", sel, [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 20, 21, 22])
-    show("attend", att, [0, 1, 2] + list(range(3, 20)) + [20, 21, 22, 23, 24])
-    show("fused ", fus, [0, 1, 25, 26, 27, 28, 29, 2] + list(range(3, 20)) + [20, 21, 22, 23, 24])
+
+    show("mma   ", mma, list(range(0, 13)))

@@ -180,7 +180,7 @@ def test_fused_select_attend_kernel_parity_subprocess(cuda_device):
     import subprocess
     import sys
 
-    env = dict(os.environ, SKV_FUSED="1")
+    env = dict(os.environ, SKV_FUSED="1", SKV_LAYER="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
                         "-k", "(step or ties or all_equal or tau_cap or many_one) and not subprocess"],
@@ -240,3 +240,34 @@ def test_host_residency_transfer_ledger(cuda_device):
     assert skv.host_fetch_bytes(0) == first
     skv.decode_step(0, q2, no_b, out, sel_tokens=ntok)  # qbar = q2 (fresh sentence): new topic
     assert skv.host_fetch_bytes(0) > first
+
+
+def test_fma_attend_kernels_parity_subprocess(cuda_device):
+    """The fp32-FMA attend kernels (SKV_ATTEND=fma; default is the tensor-core kernel) must pass the
+    same parity cases in both residencies."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_ATTEND="fma")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
+                        "-k", "(tiny_config or host_residency or ties or tau_cap or many_one) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_persistent_layer_kernel_parity_subprocess(cuda_device):
+    """The opt-in persistent per-layer kernel (SKV_LAYER=1; work queue of SCORE / SELECT / ATTEND
+    items with per-unit dependency counters) must reproduce the decode_step parity cases."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_LAYER="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
+                        "tests/test_gpu_fullsize.py",
+                        "-k", "(step or ties or all_equal or tau_cap or many_one or config2) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
