@@ -124,12 +124,14 @@ skv_status sentencekv_prefill_compress(skv_ctx* ctx, int32_t layer, const int32_
  *   D1: append q_t to the layer's sentence query cache and form qbar (Eq. 2; A10),
  *       group query qt_g = sum of the group's qbar_h (A9), similarity qt_g^T kbar_{s,g} for every
  *       sentence (A23 canonical fp32).  If input_token[b] is a boundary id, the cache
- *       of sequence b is reset after this step (A11).
+ *       of sequence b is reset after this step (A11).  The cache update itself (append or
+ *       reset) is applied by the decode_attend of the same layer and step, which must follow.
  *   D2: per (sequence, KV head): the maximal prefix of the ranking (score desc, index asc)
  *       whose token count fits tau (A13, A14); result kept in the ctx for decode_attend.
  *
  * q            device bf16 [batch_count][kv_head_count*grp][d]: this step's query (as cached)
- * input_token  device int32 [batch_count]: the token whose query this is
+ * input_token  device int32 [batch_count]: the token whose query this is; it must stay valid until the
+ *              decode_attend of the same layer has executed (that call applies the Eq. 2 update)
  * sel_ids      device int32 [batch_count][kv_head_count][tau] or NULL: selected sentence ids,
  *              ascending, tail filled with -1
  * sel_count    device int32 [batch_count][kv_head_count] or NULL: number of selected sentences

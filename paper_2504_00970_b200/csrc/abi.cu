@@ -435,12 +435,12 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
     SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
     prof_end(c, SKV_K_SCORE, pa, st);
     pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax,
-                                   c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt, ls.sel, false,
-                                   sel_ids, sel_count, sel_tokens, st));
+    SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->Smax, c->tau, ls.sel,
+                                   false, sel_ids, sel_count, sel_tokens, st));
     prof_end(c, SKV_K_SELECT, pa, st);
     c->launches += 2;
     ls.selected = true;
+    ls.input_token = input_token;
     return SKV_OK;
 }
 
@@ -535,6 +535,7 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    const skv::QsState qs{ls.input_token, c->bset, c->n_bset, ls.Sq, ls.cnt};
     cudaEvent_t pa = nullptr;
     if (c->cfg.residency == SKV_KV_HOST) {
         if (!ls.host_ready) {  // first decode of the layer after its prefill: the offload must be done
@@ -544,18 +545,18 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
         pa = prof_begin(c, st);
         if (skv::mma_enabled())
             SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
-                                               true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, out, st));
+                                               true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, st));
         else
             SKV_CUDA(c, skv::launch_attend_host(qb, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV, c->B, c->G, c->grp, c->d,
-                                                ls.sel, ls.ledger, out, st));
+                                                ls.sel, ls.ledger, qs, out, st));
     } else {
         pa = prof_begin(c, st);
         const skv::KvSrc kv{ls.K, ls.V, c->L, 0};
         if (skv::mma_enabled())
             SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, c->L, nullptr, nullptr, false, c->B, c->G,
-                                               c->grp, c->d, ls.sel, nullptr, out, st));
+                                               c->grp, c->d, ls.sel, nullptr, qs, out, st));
         else
-            SKV_CUDA(c, skv::launch_attend(qb, kv, c->B, c->G, c->grp, c->d, ls.sel, out, st));
+            SKV_CUDA(c, skv::launch_attend(qb, kv, c->B, c->G, c->grp, c->d, ls.sel, qs, out, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;

@@ -30,8 +30,8 @@ int attend_chunk_tokens(int) { return kAttC; }
 
 template <int D, int GRP>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kAttThreads, GRP <= 4 ? 2 : 1)
-attend_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, int G, SelBufs sel, float* __restrict__ out,
-              float scale_log2) {
+attend_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, int G, SelBufs sel, QsState qs,
+              float* __restrict__ out, float scale_log2) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     AttSmem<D, GRP>& sm = *reinterpret_cast<AttSmem<D, GRP>*>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
@@ -51,6 +51,7 @@ attend_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, int G, SelBufs sel,
         (&sm.lw[0][0])[tid] = 0.0f;
     }
     pdl_wait();
+    if (cluster.block_rank() == 0) qs_update_unit(q, qs.input_token, qs.bset, qs.nb, qs.Sq, qs.cnt, b, g, G, GRP, D, tid, kAttThreads);
     const int cur = sel.parity[unit] ^ 1;  // the selection made by this step's decode_select
     const int count = *sel.count_of(cur, unit);
     const size_t base = (size_t)unit * kv.unit_stride + (size_t)cur * kv.slot_stride;
@@ -82,7 +83,7 @@ template <int D, int GRP>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kAttThreads, GRP <= 4 ? 2 : 1)
 attend_host_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* Khost, const __nv_bfloat16* Vhost,
                    int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, int G, SelBufs sel,
-                   unsigned long long* __restrict__ ledger, float* __restrict__ out, float scale_log2) {
+                   unsigned long long* __restrict__ ledger, QsState qs, float* __restrict__ out, float scale_log2) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     AttSmem<D, GRP>& sm = *reinterpret_cast<AttSmem<D, GRP>*>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
@@ -100,6 +101,7 @@ attend_host_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* Kho
         (&sm.lw[0][0])[tid] = 0.0f;
     }
     pdl_wait();
+    if (cluster.block_rank() == 0) qs_update_unit(q, qs.input_token, qs.bset, qs.nb, qs.Sq, qs.cnt, b, g, G, GRP, D, tid, kAttThreads);
     const int prev = sel.parity[unit], cur = prev ^ 1;
     const int count = *sel.count_of(cur, unit);
     const int pcount = *sel.count_of(prev, unit);
@@ -147,7 +149,7 @@ attend_host_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* Kho
 template <int D, int GRP>
 static cudaError_t launch_host_one(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, const __nv_bfloat16* Kh,
                                    const __nv_bfloat16* Vh, int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, int G,
-                                   SelBufs sel, unsigned long long* ledger, float* out, float scale_log2) {
+                                   SelBufs sel, unsigned long long* ledger, QsState qs, float* out, float scale_log2) {
     const size_t smem = sizeof(AttSmem<D, GRP>) + sizeof(int32_t) * (4 * (size_t)sel.tau + 2);
     static size_t configured = 0;
     if (smem > configured) {
@@ -160,15 +162,15 @@ static cudaError_t launch_host_one(dim3 grid, cudaStream_t st, const __nv_bfloat
         configured = smem;
     }
     return launch_pdl(attend_host_kernel<D, GRP>, grid, dim3(kAttThreads), smem, st, q, Kh, Vh, L, wsK, wsV, G, sel,
-                      ledger, out, scale_log2);
+                      ledger, qs, out, scale_log2);
 }
 
 cudaError_t launch_attend_host(const __nv_bfloat16* q, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L,
                                __nv_bfloat16* wsK, __nv_bfloat16* wsV, int B, int G, int grp, int d, SelBufs sel,
-                               unsigned long long* ledger, float* out, cudaStream_t st) {
+                               unsigned long long* ledger, QsState qs, float* out, cudaStream_t st) {
     dim3 grid(kCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
-#define SKV_ATH(DV, GV) return launch_host_one<DV, GV>(grid, st, q, Kh, Vh, L, wsK, wsV, G, sel, ledger, out, scale_log2)
+#define SKV_ATH(DV, GV) return launch_host_one<DV, GV>(grid, st, q, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_ATH(128, 1);
@@ -190,7 +192,7 @@ cudaError_t launch_attend_host(const __nv_bfloat16* q, const __nv_bfloat16* Kh, 
 
 template <int D, int GRP>
 static cudaError_t launch_one(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, KvSrc kv, int G, SelBufs sel,
-                              float* out, float scale_log2) {
+                              QsState qs, float* out, float scale_log2) {
     const size_t smem = sizeof(AttSmem<D, GRP>) + sizeof(int32_t) * (2 * (size_t)sel.tau + 1);
     static size_t configured = 0;
     if (smem > configured) {
@@ -202,14 +204,14 @@ static cudaError_t launch_one(dim3 grid, cudaStream_t st, const __nv_bfloat16* q
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    return launch_pdl(attend_kernel<D, GRP>, grid, dim3(kAttThreads), smem, st, q, kv, G, sel, out, scale_log2);
+    return launch_pdl(attend_kernel<D, GRP>, grid, dim3(kAttThreads), smem, st, q, kv, G, sel, qs, out, scale_log2);
 }
 
-cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, float* out,
-                          cudaStream_t st) {
+cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, QsState qs,
+                          float* out, cudaStream_t st) {
     dim3 grid(kCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
-#define SKV_ATT(DV, GV) return launch_one<DV, GV>(grid, st, q, kv, G, sel, out, scale_log2)
+#define SKV_ATT(DV, GV) return launch_one<DV, GV>(grid, st, q, kv, G, sel, qs, out, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_ATT(128, 1);

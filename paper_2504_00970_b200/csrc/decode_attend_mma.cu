@@ -73,7 +73,7 @@ template <int D, int GRP, bool HOST>
 __global__ void __cluster_dims__(kMCL, 1, 1) __launch_bounds__(kMT, 2)
 attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bfloat16* Khost,
                   const __nv_bfloat16* Vhost, int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, int G, SelBufs sel,
-                  unsigned long long* __restrict__ ledger, float* __restrict__ out, float scale_log2) {
+                  unsigned long long* __restrict__ ledger, QsState qs, float* __restrict__ out, float scale_log2) {
     constexpr int NKS = D / 16;   // k-steps of QK (and m-tiles of PV)
     constexpr int NU = D / 32;    // 16-byte K segments per lane per row
     constexpr int NVP = D / 64;   // 16-byte V segments per lane per token (D = 64: 1, D = 128: 2)
@@ -97,6 +97,7 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
 
     SKV_TRACE_POINT(0);
     pdl_wait();
+    if (rank == 0) qs_update_unit(q, qs.input_token, qs.bset, qs.nb, qs.Sq, qs.cnt, b, g, G, GRP, D, tid, kMT);
     const int prev = sel.parity[unit], cur = prev ^ 1;
     const int count = *sel.count_of(cur, unit);
     SKV_TRACE_POINT(1);
@@ -392,8 +393,8 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, KvSrc kv,
                                 const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L, __nv_bfloat16* wsK,
-                                __nv_bfloat16* wsV, int G, SelBufs sel, unsigned long long* ledger, float* out,
-                                float scale_log2) {
+                                __nv_bfloat16* wsV, int G, SelBufs sel, unsigned long long* ledger, QsState qs,
+                                float* out, float scale_log2) {
     // metadata: tok[tau+1] + srcs[tau] (+ pids[tau] + ptok[tau+1]) + rowtab[per-CTA tokens]
     const size_t tiles = ((size_t)sel.tau + kTile - 1) / kTile;
     const size_t rows = ((tiles + kMCL - 1) / kMCL) * kTile;
@@ -410,7 +411,7 @@ static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16*
         configured = smem;
     }
     return launch_pdl(attend_mma_kernel<D, GRP, HOST>, grid, dim3(kMT), smem, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel,
-                      ledger, out, scale_log2);
+                      ledger, qs, out, scale_log2);
 }
 
 bool mma_enabled() {
@@ -423,12 +424,12 @@ bool mma_enabled() {
 
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
-                              SelBufs sel, unsigned long long* ledger, float* out, cudaStream_t st) {
+                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, cudaStream_t st) {
     dim3 grid(kMCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
 #define SKV_MM(DV, GV)                                                                                          \
-    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, out, scale_log2) \
-                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, out, scale_log2)
+    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, scale_log2) \
+                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_MM(128, 1);

@@ -189,11 +189,11 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
 // ids in ascending order with their token prefix sums.  Thread t owns the contiguous index range
 // [t*E, t*E+E); keys and lengths are cached in shared memory (S <= kSelSmemCap).
 //
-// The same CTA performs the deferred D1 state update of its query heads: Sq += q_t, or Sq = 0
-// when the step's input token is a boundary (A11); cnt is updated by the g == 0 CTA.
+// The deferred D1 state update (Sq += q_t, or reset at a boundary, A11) is done afterwards by the
+// attend kernel (qs_update_unit), off the selection's critical path.
 constexpr int kSelThreads = 1024;
 constexpr int kBins = 2048;
-constexpr int kSelSmemCap = 32768;
+constexpr int kSelSmemCap = 19000;  // 10 B per sentence of dynamic shared memory
 constexpr int kCandCap = kSelThreads;
 
 __device__ __forceinline__ unsigned long long key64_of(uint32_t k, int s) {
@@ -203,22 +203,19 @@ __device__ __forceinline__ unsigned long long key64_of(uint32_t k, int s) {
 template <bool SMEM>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ off, int off_stride,
-    const int32_t* __restrict__ S, int G, int grp, int D, int Smax, int tau, const __nv_bfloat16* __restrict__ q,
-    const int32_t* __restrict__ input_token, const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq,
-    int32_t* __restrict__ cnt, SelBufs sel, bool src_gathered, int32_t* __restrict__ out_ids,
-    int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens) {
-    __shared__ uint32_t hw[kBins];  // length-weighted histogram
-    __shared__ uint32_t hc[kBins];  // count histogram
+    const int32_t* __restrict__ S, int G, int Smax, int tau, SelBufs sel, bool src_gathered,
+    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens) {
+    __shared__ uint32_t hist[kBins];  // length-weighted histogram
     __shared__ unsigned long long cand_key[kCandCap];
     __shared__ uint32_t cand_len[kCandCap];
     __shared__ uint32_t ws32[32];
     __shared__ unsigned long long ws64[32];
-    __shared__ uint32_t sh_bin, sh_rem, sh_cnt, sh_lo, sh_hi, sh_ncand;
+    __shared__ uint32_t sh_bin, sh_rem, sh_lo, sh_hi, sh_ncand;
     __shared__ unsigned long long sh_thr;
-    __shared__ int sh_all;
     extern __shared__ __align__(16) unsigned char sel_smem[];
-    uint32_t* skey = reinterpret_cast<uint32_t*>(sel_smem);                    // [Smax]
-    uint16_t* slen = reinterpret_cast<uint16_t*>(sel_smem + 4 * (size_t)Smax);  // [Smax] (len <= tau <= 65535)
+    uint32_t* skey = reinterpret_cast<uint32_t*>(sel_smem);                    // [Smax] ordered keys
+    int32_t* soff = reinterpret_cast<int32_t*>(sel_smem + 4 * (size_t)Smax);   // [Smax] first token
+    uint16_t* slen = reinterpret_cast<uint16_t*>(sel_smem + 8 * (size_t)Smax);  // [Smax] (len <= tau <= 65535)
 
     const int g = blockIdx.x, b = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -226,61 +223,42 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const int Sb = S[b];
     const float* sc = scores + (size_t)(b * G + g) * Smax;
     const int32_t* o = off + (size_t)b * off_stride;
-    const int Hq = G * grp;
 
     SKV_TRACE_POINT(0);
-    // ---- deferred D1 state update (Eq. 2 sentence cache; reset at a boundary input) ----
-    {
-        const bool reset = in_set(input_token[b], bset, nb);
-        const size_t base = ((size_t)b * Hq + (size_t)g * grp) * D;
-        for (int i = tid; i < grp * D; i += blockDim.x)
-            Sq[base + i] = reset ? 0.0f : __fadd_rn(Sq[base + i], __bfloat162float(q[base + i]));
-        if (tid == 0) cnt[b * G + g] = reset ? 0 : cnt[b * G + g] + 1;
-    }
-    SKV_TRACE_POINT(1);
-
     if (tid == 0) {
         sh_lo = 0xffffffffu;
         sh_hi = 0u;
         sh_ncand = 0u;
-        sh_all = 0;
-    }
-    if (SMEM) {
-        // coalesced fill, loads batched before use
-        for (int s0 = 0; s0 < Sb; s0 += 4 * kSelThreads) {
-            float v[4];
-            int a[4], e[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int s = s0 + u * kSelThreads + tid;
-                v[u] = s < Sb ? sc[s] : 0.0f;
-                a[u] = s < Sb ? o[s] : 0;
-                e[u] = s < Sb ? o[s + 1] : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int s = s0 + u * kSelThreads + tid;
-                if (s < Sb) {
-                    skey[s] = ordered_key(v[u]);
-                    slen[s] = (uint16_t)(e[u] - a[u]);
-                }
-            }
-        }
     }
     __syncthreads();
-    SKV_TRACE_POINT(2);
-    auto key_of = [&](int s) -> uint32_t { return SMEM ? skey[s] : ordered_key(sc[s]); };
-    auto len_of = [&](int s) -> uint32_t { return SMEM ? (uint32_t)slen[s] : (uint32_t)(o[s + 1] - o[s]); };
-    const int E = (Sb + kSelThreads - 1) / kSelThreads;
-    const int i0 = min(Sb, tid * E), i1 = min(Sb, i0 + E);
-
-    // key range of all sentences
+    // ---- keys, lengths and offsets -> shared memory (one batched pass) + the key range ----
     {
         uint32_t mn = 0xffffffffu, mx = 0u;
-        for (int s = i0; s < i1; ++s) {
-            const uint32_t k = key_of(s);
-            mn = min(mn, k);
-            mx = max(mx, k);
+        constexpr int U = 8;
+        for (int s0 = 0; s0 < Sb; s0 += U * kSelThreads) {
+            float v[U];
+            int a0[U], a1[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int s = s0 + j * kSelThreads + tid;
+                v[j] = s < Sb ? sc[s] : 0.0f;
+                a0[j] = s < Sb ? o[s] : 0;
+                a1[j] = s < Sb ? o[s + 1] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int s = s0 + j * kSelThreads + tid;
+                if (s < Sb) {
+                    const uint32_t k = ordered_key(v[j]);
+                    mn = min(mn, k);
+                    mx = max(mx, k);
+                    if (SMEM) {
+                        skey[s] = k;
+                        soff[s] = a0[j];
+                        slen[s] = (uint16_t)(a1[j] - a0[j]);
+                    }
+                }
+            }
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
         mx = __reduce_max_sync(0xffffffffu, mx);
@@ -290,6 +268,12 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         }
     }
     __syncthreads();
+    SKV_TRACE_POINT(2);
+    auto key_of = [&](int s) -> uint32_t { return SMEM ? skey[s] : ordered_key(sc[s]); };
+    auto len_of = [&](int s) -> uint32_t { return SMEM ? (uint32_t)slen[s] : (uint32_t)(o[s + 1] - o[s]); };
+    auto off_of = [&](int s) -> int32_t { return SMEM ? soff[s] : o[s]; };
+    const int E = (Sb + kSelThreads - 1) / kSelThreads;
+    const int i0 = min(Sb, tid * E), i1 = min(Sb, i0 + E);
     SKV_TRACE_POINT(3);
     uint32_t lo = sh_lo, hi = sh_hi, rem = (uint32_t)tau;
     bool all_fit = false;
@@ -328,19 +312,17 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         auto bin_of = [&](uint32_t k) -> uint32_t {
             return mul ? (uint32_t)(((unsigned long long)(k - lo) * mul) >> 32) : (k - lo);
         };
-        for (int i = tid; i < kBins; i += blockDim.x) hw[i] = hc[i] = 0u;
+        for (int i = tid; i < kBins; i += blockDim.x) hist[i] = 0u;
         __syncthreads();
         for (int s = i0; s < i1; ++s) {
             const uint32_t k = key_of(s);
             if (k < lo || k > hi) continue;
-            const uint32_t bin = bin_of(k);
-            atomicAdd(&hw[bin], len_of(s));
-            atomicAdd(&hc[bin], 1u);
+            atomicAdd(&hist[bin_of(k)], len_of(s));
         }
         __syncthreads();
         SKV_TRACE_POINT(4 + 4 * level);
         // thread t owns bins 2t (lower) and 2t+1 (upper); weight above t's pair = total - incl
-        const uint32_t w_lo = hw[2 * tid], w_hi = hw[2 * tid + 1];
+        const uint32_t w_lo = hist[2 * tid], w_hi = hist[2 * tid + 1];
         uint32_t total;
         const uint32_t incl = block_incl_sum<uint32_t>(w_lo + w_hi, ws32, &total);
         if (level == 0 && total <= rem) {
@@ -351,11 +333,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         if (above <= rem && above + w_hi > rem) {
             sh_bin = 2 * tid + 1;
             sh_rem = rem - above;
-            sh_cnt = hc[2 * tid + 1];
         } else if (above + w_hi <= rem && above + w_hi + w_lo > rem) {
             sh_bin = 2 * tid;
             sh_rem = rem - above - w_hi;
-            sh_cnt = hc[2 * tid];
         }
         if (tid == 0) {
             sh_lo = 0xffffffffu;
@@ -364,20 +344,33 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         }
         __syncthreads();
         SKV_TRACE_POINT(5 + 4 * level);
-        const uint32_t cb = sh_bin, ncb = sh_cnt;
+        const uint32_t cb = sh_bin;
         rem = sh_rem;
-        if (ncb <= (uint32_t)kCandCap) {
-            // exact rank of the crossing bin's sentences by key64
+        // gather the crossing bin's sentences (at most kCandCap) and its key range in one pass
+        {
+            uint32_t mn = 0xffffffffu, mx = 0u;
             for (int s = i0; s < i1; ++s) {
                 const uint32_t k = key_of(s);
-                if (k < lo || k > hi) continue;
-                if (bin_of(k) != cb) continue;
+                if (k < lo || k > hi || bin_of(k) != cb) continue;
+                mn = min(mn, k);
+                mx = max(mx, k);
                 const uint32_t pos = atomicAdd(&sh_ncand, 1u);
-                cand_key[pos] = key64_of(k, s);
-                cand_len[pos] = len_of(s);
+                if (pos < (uint32_t)kCandCap) {
+                    cand_key[pos] = key64_of(k, s);
+                    cand_len[pos] = len_of(s);
+                }
             }
-            __syncthreads();
-            SKV_TRACE_POINT(6 + 4 * level);
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) {
+                atomicMin(&sh_lo, mn);
+                atomicMax(&sh_hi, mx);
+            }
+        }
+        __syncthreads();
+        SKV_TRACE_POINT(6 + 4 * level);
+        if (sh_ncand <= (uint32_t)kCandCap) {
+            // exact rank of the crossing bin's sentences by key64
             const int nc = (int)sh_ncand;
             if (tid < nc) {
                 const unsigned long long mk = cand_key[tid];
@@ -392,27 +385,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
             break;
         }
         // too many candidates: narrow [lo, hi] to the crossing bin's key range and repeat
-        {
-            uint32_t mn = 0xffffffffu, mx = 0u;
-            for (int s = i0; s < i1; ++s) {
-                const uint32_t k = key_of(s);
-                if (k < lo || k > hi) continue;
-                if (bin_of(k) != cb) continue;
-                mn = min(mn, k);
-                mx = max(mx, k);
-            }
-            mn = __reduce_min_sync(0xffffffffu, mn);
-            mx = __reduce_max_sync(0xffffffffu, mx);
-            if (lane == 0) {
-                atomicMin(&sh_lo, mn);
-                atomicMax(&sh_hi, mx);
-            }
-        }
-        __syncthreads();
         lo = sh_lo;
         hi = sh_hi;
+        __syncthreads();
     }
-
     pdl_trigger();
     // ---- ordered compaction of the selected sentences (ascending ids + token offsets) ----
     unsigned long long mine = 0;
@@ -434,7 +410,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
             if (all_fit || key64_of(key_of(s), s) > thr) {
                 ids[pos] = s;
                 tokoff[pos] = (int32_t)toff;
-                src[pos] = src_gathered ? (int32_t)toff : o[s];
+                src[pos] = src_gathered ? (int32_t)toff : off_of(s);
+                if (out_ids) out_ids[(size_t)(b * G + g) * tau + pos] = s;
                 ++pos;
                 toff += len_of(s);
             }
@@ -449,35 +426,28 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
         if (out_tokens) out_tokens[b * G + g] = ntok;
     }
     SKV_TRACE_POINT(22);
-    if (out_ids) {
-        __syncthreads();
-        int32_t* oi = out_ids + (size_t)(b * G + g) * tau;
-        for (int i = tid; i < tau; i += blockDim.x) oi[i] = i < count ? ids[i] : -1;
-    }
+    if (out_ids)
+        for (int i = count + tid; i < tau; i += blockDim.x) out_ids[(size_t)(b * G + g) * tau + i] = -1;
 }
 
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
-                          int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
-                          const int32_t* input_token, const int32_t* bset, int nb, float* Sq, int32_t* cnt,
-                          SelBufs sel, bool src_gathered, int32_t* out_ids, int32_t* out_count,
-                          int32_t* out_tokens, cudaStream_t st) {
+                          int G, int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids,
+                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st) {
     dim3 grid(G, B);
     if (Smax <= kSelSmemCap && tau <= 65535) {
-        const size_t smem = (size_t)Smax * 6 + 16;
+        const size_t smem = (size_t)Smax * 10 + 16;
         static bool configured = false;
         if (!configured) {
             cudaError_t e = cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(kSelSmemCap * 6 + 16));
+                                                 (int)(kSelSmemCap * 10 + 16));
             if (e != cudaSuccess) return e;
             configured = true;
         }
-        return launch_pdl(select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, grp,
-                          d, Smax, tau, q, input_token, bset, nb, Sq, cnt, sel, src_gathered, out_ids, out_count,
-                          out_tokens);
+        return launch_pdl(select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, Smax,
+                          tau, sel, src_gathered, out_ids, out_count, out_tokens);
     }
-    return launch_pdl(select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, grp, d,
-                      Smax, tau, q, input_token, bset, nb, Sq, cnt, sel, src_gathered, out_ids, out_count,
-                      out_tokens);
+    return launch_pdl(select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, Smax, tau,
+                      sel, src_gathered, out_ids, out_count, out_tokens);
 }
 
 }  // namespace skv

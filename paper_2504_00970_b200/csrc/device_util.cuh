@@ -144,6 +144,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// ---- deferred D1 state update (Eq. 2 sentence cache; reset at a boundary input, A11) ----
+// Sq += q_t (or Sq = 0 when the step's input token is a boundary) for the grp query heads of unit
+// (b, g), and its count.  Called by one CTA per unit after that unit's scoring and selection.
+__device__ __forceinline__ void qs_update_unit(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
+                               const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq,
+                               int32_t* __restrict__ cnt, int b, int g, int G, int grp, int D, int tid, int nthreads) {
+    const bool reset = in_set(input_token[b], bset, nb);
+    const size_t base = ((size_t)b * G * grp + (size_t)g * grp) * D;
+    for (int i = tid; i < grp * D; i += nthreads)
+        Sq[base + i] = reset ? 0.0f : __fadd_rn(Sq[base + i], __bfloat162float(q[base + i]));
+    if (tid == 0) cnt[b * G + g] = reset ? 0 : cnt[b * G + g] + 1;
+}
+
 // ---- programmatic dependent launch (PDL) ----
 // Every decode kernel is launched with programmatic stream serialization: it lets the next kernel
 // of the stream start launching at once (trigger) and blocks until the previous kernel of the

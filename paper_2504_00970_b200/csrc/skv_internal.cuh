@@ -32,6 +32,16 @@ struct SelBufs {
     __host__ __device__ int32_t* count_of(int slot, int u) const { return count + (size_t)slot * units + u; }
 };
 
+// The deferred Eq. 2 state update of a layer (Sq += q_t or reset), done by the attend kernels
+// after the step's scoring and selection (qs_update_unit in device_util.cuh).
+struct QsState {
+    const int32_t* input_token;  // [B]
+    const int32_t* bset;
+    int nb;
+    float* Sq;                   // [B][Hq][d]
+    int32_t* cnt;                // [B][G]
+};
+
 // Where decode_attend reads K/V rows: unit u, slot s, row r -> base + ((u * unit_stride) +
 // s * slot_stride + r) * d.  Device residency: the caller's K/V (unit_stride = L, slot_stride = 0,
 // rows = context tokens).  Host residency: the HBM working set (unit_stride = 2*tau,
@@ -48,6 +58,7 @@ constexpr int kNumSMs = 148;
 struct LayerState {
     bool prefilled = false;
     bool selected = false;             // a decode_select ran since the prefill
+    const int32_t* input_token = nullptr;  // of the last decode_select (its Eq. 2 update runs in attend)
     const __nv_bfloat16* K = nullptr;  // device residency: borrowed [B][G][L][d]
     const __nv_bfloat16* V = nullptr;
     __nv_bfloat16* E = nullptr;        // [B][G][Smax][d]  sentence embeddings (Eq. 1)
@@ -142,21 +153,20 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
                          cudaStream_t st);
 
 // D2: budgeted selection + Q_s state update (Sq += q or reset).
-cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B, int G, int grp,
-                          int d, int Smax, int tau, const __nv_bfloat16* q, const int32_t* input_token,
-                          const int32_t* bset, int nb, float* Sq, int32_t* cnt, SelBufs sel, bool src_gathered,
-                          int32_t* out_ids, int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
+cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
+                          int G, int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids,
+                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
 
 // D3 + D4 with host residency: selected sentences also selected at the previous step are re-read
 // from the previous HBM working-set slot, the others from the mapped pinned host store (PCIe); the
 // staged rows are written through to the current slot; host bytes are added to *ledger.
 cudaError_t launch_attend_host(const __nv_bfloat16* q, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L,
                                __nv_bfloat16* wsK, __nv_bfloat16* wsV, int B, int G, int grp, int d, SelBufs sel,
-                               unsigned long long* ledger, float* out, cudaStream_t st);
+                               unsigned long long* ledger, QsState qs, float* out, cudaStream_t st);
 
 // D3 + D4: split-K attention over the selected sentences' tokens (device residency).
-cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, float* out,
-                          cudaStream_t st);
+cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, QsState qs,
+                          float* out, cudaStream_t st);
 
 int attend_chunk_tokens(int d);
 
@@ -213,7 +223,7 @@ cudaError_t launch_layer(const LayerArgs& a, int grp, int d, cudaStream_t st);
 bool mma_enabled();
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
-                              SelBufs sel, unsigned long long* ledger, float* out, cudaStream_t st);
+                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, cudaStream_t st);
 
 // D2 + D3 + D4 fused (one cluster per unit), reading the scores of launch_score.  Opt-in
 // (SKV_FUSED=1): on B200 the cluster-wide selection phases cost more than the separate select
