@@ -339,11 +339,13 @@ def main():
     S_tot = sum(S)
     # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md "Measurement"
     score_bytes = Gl * S_tot * d * 2 + Bl * Hl * d * (2 + 4) + Bl * Gl * S_tot * 4  # E + q,Sq + scores written
-    nlaunch = max(1, prof["fused"][1] or prof["attend"][1])
+    nlaunch = max(1, prof["step"][1] or prof["fused"][1] or prof["attend"][1])
     kv_bytes = ntok_sum * d * 2 * 2 / nlaunch  # selected K and V rows
     sel_bytes = Bl * Gl * S_tot * (4 + 4) + Bl * Hl * d * (2 + 4 * 2)  # scores + offsets read, q + Sq
     kern = {}
-    for name, nbytes in (("score", score_bytes), ("fused", kv_bytes + sel_bytes + Bl * Hl * d * 4),
+    # one-launch step (decode_unit.cu): E + q/Sq + scores written, offsets read, selected K/V, Sq update, O
+    unit_bytes = score_bytes + Bl * Gl * S_tot * 4 + kv_bytes + Bl * Hl * d * (4 + 4)
+    for name, nbytes in (("step", unit_bytes), ("score", score_bytes), ("fused", kv_bytes + sel_bytes + Bl * Hl * d * 4),
                          ("select", sel_bytes), ("attend", kv_bytes + Bl * Hl * d * (2 + 4))):
         ms, n = prof[name]
         if not n:
@@ -363,8 +365,9 @@ def main():
             traffic = json.load(f).get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "per_unit": "score: G*S*d*2 B (bf16 E) + q/Sq + scores; attend: sum(ntok)*d*2*2 B (selected K,V "
-                            "rows) + q + O; select: scores + offsets + q/Sq"}
+                "per_unit": "step (one launch per layer): G*S*d*2 B (bf16 E) + sum(ntok)*d*2*2 B (selected K,V rows) "
+                            "+ scores/offsets/q/Sq/O; score: E + q/Sq + scores; attend: selected K,V + q + O; "
+                            "select: scores + offsets + q/Sq"}
 
     # ---------------- end to end through the public API with host buffers
     qhost = [torch.stack(qpool[p]).cpu().pin_memory() for p in range(POOL)]  # [M][Bl][Hl][d]

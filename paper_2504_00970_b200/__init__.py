@@ -252,14 +252,14 @@ class SentenceKV:
     def launch_count(self) -> int:
         return int(lib.sentencekv_launch_count(self.ctx))
 
-    KERNELS = ("segment", "compress", "score", "select", "attend", "fused")
+    KERNELS = ("segment", "compress", "score", "select", "attend", "fused", "step")
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} of the profiled launches since the last read."""
-        ms = (ctypes.c_double * 6)()
-        n = (ctypes.c_int64 * 6)()
+        ms = (ctypes.c_double * len(self.KERNELS))()
+        n = (ctypes.c_int64 * len(self.KERNELS))()
         _check(self.ctx, lib.sentencekv_profile_read(self.ctx, ms, n))
         return {k: (ms[i], n[i]) for i, k in enumerate(self.KERNELS)}

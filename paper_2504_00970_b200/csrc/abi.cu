@@ -89,6 +89,7 @@ void free_layer_prompt(skv::LayerState& ls) {
     dfree(ls.lk_part_o);
     dfree(ls.lk_cand);
     dfree(ls.lk_cand_count);
+    dfree(ls.unit_hint);
 }
 
 void free_host_store(skv::LayerState& ls) {
@@ -254,6 +255,7 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     dfree(c->S_dev);
     dfree(c->bset);
     dfree(c->lk_items);
+    dfree(c->unit_cand);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -303,7 +305,10 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
         const size_t nsm = (size_t)c->lk_n_score_max;
         SKV_CUDA(c, dalloc(&ls.lk_cand, U * nsm * (size_t)skv::layer_item_sentences((int)d)));
         SKV_CUDA(c, dalloc(&ls.lk_cand_count, U * nsm));
+        SKV_CUDA(c, dalloc(&ls.unit_hint, U));
     }
+    dfree(c->unit_cand);
+    SKV_CUDA(c, dalloc(&c->unit_cand, skv::unit_cand_entries((int)U)));
     c->Smax = Smax;
     return SKV_OK;
 }
@@ -373,6 +378,9 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             SKV_CUDA(c, cudaMemsetAsync(ls.sel.parity, 0, sizeof(int32_t) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.cnt, 0, sizeof(int32_t) * c->B * c->G, st));
+            // no band yet (klo = 0, khi = max: everything is in the band)
+            SKV_CUDA(c, cudaMemsetAsync(ls.unit_hint, 0xff, sizeof(uint2) * c->B * c->G, st));
+            SKV_CUDA(c, cudaMemset2DAsync(ls.unit_hint, sizeof(uint2), 0, sizeof(uint32_t), (size_t)c->B * c->G, st));
         }
     }
 
@@ -456,6 +464,41 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    if (skv::unit_enabled() && c->cfg.residency == SKV_KV_DEVICE &&
+        skv::unit_supported(c->d, c->grp, c->Smax, c->tau)) {
+        // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
+        skv::UnitArgs a{};
+        a.q = qb;
+        a.input_token = input_token;
+        a.bset = c->bset;
+        a.nb = c->n_bset;
+        a.Sq = ls.Sq;
+        a.cnt = ls.cnt;
+        a.E = ls.E;
+        a.S = c->S_dev;
+        a.off = c->off;
+        a.off_stride = c->off_stride;
+        a.B = c->B;
+        a.G = c->G;
+        a.Smax = c->Smax;
+        a.scores = ls.scores;
+        a.sel = ls.sel;
+        a.kv = skv::KvSrc{ls.K, ls.V, c->L, 0};
+        a.cand = c->unit_cand;
+        a.hint = ls.unit_hint;
+        a.prefetch = 1;
+        a.out = out;
+        a.out_ids = sel_ids;
+        a.out_count = sel_count;
+        a.out_tokens = sel_tokens;
+        cudaEvent_t pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_unit(a, c->grp, c->d, st));
+        prof_end(c, SKV_K_STEP, pa, st);
+        c->launches += 1;
+        ls.selected = true;
+        ls.input_token = input_token;
+        return SKV_OK;
+    }
     if (skv::layer_enabled() && c->cfg.residency == SKV_KV_DEVICE &&
         skv::layer_smem_bytes(c->d, c->Smax, c->tau) <= 200 * 1024) {
         // persistent per-layer kernel: D1-D4 of every unit in one launch

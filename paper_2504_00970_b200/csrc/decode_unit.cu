@@ -1,0 +1,896 @@
+// decode_unit.cu -- one decode step of one layer, D1 + D2 + D3 + D4, in ONE launch: a
+// thread-block cluster of kUC CTAs per (b, g) unit (device residency).
+//
+// Same arithmetic and results as score_kernel + select_kernel + attend_mma_kernel; this file only
+// changes where the work runs so that a layer costs one launch and two cluster barriers:
+//
+//   1. score (D1; Eq. 2, S = qbar^T kbar P:440-442, Alg. 1 l.14-16): CTA r streams the
+//      embeddings of its contiguous sentence range [r*chunk, (r+1)*chunk) through a TMA bulk-copy
+//      ring (cp.async.bulk + mbarrier, L2 evict-first) and keeps the ordered 32-bit keys in shared
+//      memory.  While the ring is in flight the CTA issues L2 prefetches of its share of the K/V
+//      runs the unit selected at the previous decode step (selections change little from token to
+//      token, so step 3 then mostly reads L2).
+//   2. select (D2; Alg. 1 l.17, readings A13-A15): the budgeted selection is the maximal
+//      prefix of the ranking by key64 = (ordered(score) << 32) | (0xffffffff - s) whose length
+//      fits tau.  Each CTA first cuts its own range down to *local candidates*: a sentence whose
+//      local weight-above (summed lengths of the CTA's sentences ranked above it) exceeds tau can
+//      never be selected, so it keeps every sentence ranked at or above its local crossing point
+//      (one length-weighted 1024-bin histogram over the local key range; the crossing bin is kept
+//      whole, so the list is a superset of local prefix + crossing sentence).  Claim: ranking the
+//      union U of the lists is exact -- for s in U, (weight of U ranked above s) + n_s <= tau iff s
+//      is selected.  (If a sentence t above s is missing from U, the crossing sentence of t's CTA and
+//      everything above it are in U and above s, and they already weigh more than tau.)  After one
+//      cluster barrier every CTA copies the lists (DSMEM) into its own shared memory and ranks U
+//      (typically ~100 candidates per CTA instead of S/kUC sentences) by the same range-refining
+//      histogram as select_kernel -- redundantly in all CTAs, so no second exchange is needed.
+//      Lists are in ascending sentence order, so an ordered block scan yields the ascending ids and
+//      gathered token offsets.  Rank 0 stores the selection (double-buffered SelBufs slot) and does
+//      the deferred Eq. 2 state update (every CTA has read Sq before the barrier).
+//   3. gather + attend (D3 + D4; Alg. 1 l.18-19): CTA r takes its 1/kUC of the 16-token
+//      tiles of the gathered tokens; rows are read straight from the context K/V (one contiguous
+//      run per sentence) into mma.sync fragments (mma_attend.cuh); warps merge through shared
+//      memory, the kUC CTA partials through DSMEM (second cluster barrier).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "device_util.cuh"
+#include "mma_attend.cuh"
+#include "skv_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace skv {
+SKV_TRACE_DEFINE(unit)
+#ifdef SKV_TRACE
+// per CTA (unit * kUC + rank < 1024): SM id + globaltimer (ns) at the phase boundaries
+__device__ unsigned long long g_unit_t[1024][16];
+extern "C" __attribute__((visibility("default"))) int sentencekv_debug_unit(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_unit_t, sizeof(g_unit_t));
+}
+__device__ __forceinline__ void unit_stamp(int cta, int ph) {
+    if (threadIdx.x == 0 && cta < 1024) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_unit_t[cta][ph] = t;
+        if (ph == 0) {
+            unsigned int sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_unit_t[cta][15] = sm;
+        }
+    }
+}
+#define SKV_USTAMP(ph) unit_stamp(unit * kUC + rank, (ph))
+#else
+#define SKV_USTAMP(ph) \
+    do {               \
+    } while (0)
+#endif
+
+namespace {
+
+constexpr int kUT = 256;                 // threads per CTA
+constexpr int kUW = kUT / 32;
+constexpr int kUC = 8;                   // CTAs per cluster (= per unit)
+constexpr int kUTileBytes = 16384;       // E bytes per TMA stage
+constexpr int kUStages = 3;
+constexpr int kULocalCap = 2048;         // sentences per CTA (supported: Smax <= kUC * kULocalCap)
+constexpr int kUOwnCap = 512;            // own candidate list kept in shared memory (else global scratch)
+constexpr int kUBins = 1024;
+constexpr int kUExact = kUT;             // crossing-bin candidates ranked exactly per refinement level
+constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
+constexpr int kUBandCap = 256;           // band-path list entries per CTA
+constexpr int kUBandSel = 256;           // band path: selected sentences ranked by counting (else general path)
+static_assert(kUBandSel + kUC * kUBandCap <= kUGather, "band lists fit the ring");
+using mma::kInvalid;
+using mma::kTile;
+
+template <int D>
+using USmemMerge = mma::MergeSmem<D, kUW>;
+static_assert(sizeof(USmemMerge<128>) <= (size_t)kUStages * kUTileBytes, "merge area aliases the E ring");
+
+// candidate entry: (ordered key, sentence id, first context row, length)
+struct Ctl {
+    int own_count;      // general path: local candidates of this CTA
+    int own_global;     // general path: list stored in global scratch (overflow)
+    int bn;             // band path: entries of this CTA at or above the band's lower edge
+    uint32_t whi, wband;  // band path: weight above the band / inside it (this CTA)
+    int base[kUC + 1];  // exclusive prefix of the cluster's list sizes
+    int ok, nsel, nband, count, ntok, reset, cnt0, kc_set;
+    uint32_t WHI, ks, kc;
+    uint32_t lo, hi, cb, rem, ncand;
+    unsigned long long thr;
+};
+
+__device__ __forceinline__ unsigned long long ukey64(uint32_t k, int s) {
+    return ((unsigned long long)k << 32) | (unsigned long long)(0xffffffffu - (uint32_t)s);
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_hint(const void* p, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+
+// bin(k) = (k - lo) * kUBins / span as a 32.32 fixed-point multiply: monotone in k, < kUBins;
+// spans below kUBins map one key per bin.
+struct Binner {
+    uint32_t lo;
+    unsigned long long mul;
+    __device__ Binner(uint32_t lo_, uint32_t hi_) : lo(lo_) {
+        const unsigned long long span = (unsigned long long)(hi_ - lo_) + 1ull;
+        mul = span >= kUBins ? ((unsigned long long)kUBins << 32) / span : 0ull;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t k) const {
+        return mul ? (uint32_t)(((unsigned long long)(k - lo) * mul) >> 32) : (k - lo);
+    }
+};
+
+// Length-weighted histogram of `hist` (kUBins, zeroed by the caller and complete on entry): the
+// crossing bin, i.e. the bin b with (weight above b) <= rem < (weight above b) + w_b, and the
+// budget left inside it.  Returns false if the total weight fits (no crossing bin).  Block-wide.
+__device__ __forceinline__ bool crossing_bin(const uint32_t* hist, uint32_t rem, uint32_t* ws32, Ctl& ctl,
+                                             uint32_t* cb_out, uint32_t* rem_out) {
+    constexpr int PB = kUBins / kUT;  // bins per thread, thread t owns [PB*t, PB*t+PB)
+    const int tid = threadIdx.x;
+    uint32_t w[PB], sum = 0;
+#pragma unroll
+    for (int i = 0; i < PB; ++i) {
+        w[i] = hist[PB * tid + i];
+        sum += w[i];
+    }
+    uint32_t total;
+    const uint32_t incl = block_incl_sum<uint32_t>(sum, ws32, &total);
+    if (total <= rem) return false;
+    uint32_t above = total - incl;  // weight of the bins above this thread's
+#pragma unroll
+    for (int i = PB - 1; i >= 0; --i) {
+        if (above <= rem && above + w[i] > rem) {
+            ctl.cb = PB * tid + i;
+            ctl.rem = rem - above;
+        }
+        above += w[i];
+    }
+    __syncthreads();
+    *cb_out = ctl.cb;
+    *rem_out = ctl.rem;
+    return true;
+}
+
+}  // namespace
+
+template <int D, int GRP>
+__global__ void __cluster_dims__(kUC, 1, 1) __launch_bounds__(kUT, 2)
+unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
+                 const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq, int32_t* __restrict__ cnt,
+                 const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
+                 int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv,
+                 int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
+                 float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
+                 int32_t* __restrict__ out_tokens, float scale_log2) {
+    constexpr int LPS = D / 8;                  // lanes per sentence (scoring)
+    constexpr int GPW = 32 / LPS;               // sentences per warp step
+    constexpr int TS = kUTileBytes / (D * 2);   // sentences per E tile
+    static_assert(TS % (kUW * GPW) == 0, "tile must split evenly over the warps");
+    static_assert(GRP <= 8, "heads fill the N = 8 side of the MMA");
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // [ring | keys | offs | own list | band list | sel_tok | sel_src | sel_id | rowtab]; the ring is
+    // reused for the gathered lists, then for the warp-merge area
+    __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+    int4* gath = reinterpret_cast<int4*>(smem_raw);
+    USmemMerge<D>& msm = *reinterpret_cast<USmemMerge<D>*>(smem_raw);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw + kUStages * kUTileBytes);
+    int32_t* offs = reinterpret_cast<int32_t*>(keys + kULocalCap);
+    int4* own = reinterpret_cast<int4*>(offs + kULocalCap + 4);
+    int4* blist = own + kUOwnCap;
+    const int tau = sel.tau;
+    int32_t* sel_tok = reinterpret_cast<int32_t*>(blist + kUBandCap);  // [tau + 1]
+    int32_t* sel_src = sel_tok + (tau + 1);                              // [tau]
+    int32_t* sel_id = sel_src + tau;                                     // [tau]
+    int32_t* rowtab = sel_id + tau;                                      // [rows per CTA]
+
+    __shared__ uint64_t bar[kUStages];
+    __shared__ float qt[D];
+    __shared__ float sqsum[GRP * D];  // Sq + q_t of this step (the Eq. 2 state update, stored by rank 0)
+    __shared__ uint32_t hist[kUBins];
+    __shared__ uint32_t ws32[32];
+    __shared__ unsigned long long ws64[32];
+    __shared__ unsigned long long ckey[kUExact];
+    __shared__ uint32_t clen[kUExact];
+    __shared__ Ctl ctl;
+    __shared__ const int4* lists[kUC];
+
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int g = blockIdx.y, b = blockIdx.z;
+    const int unit = b * G + g;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int Hq = G * GRP;
+
+    if (tid == 0) {
+        for (int i = 0; i < kUStages; ++i) mbar_init(&bar[i], 1);
+        ctl.lo = 0xffffffffu;
+        ctl.hi = 0u;
+        ctl.bn = 0;
+        ctl.whi = 0u;
+        ctl.wband = 0u;
+        ctl.ks = 0xffffffffu;
+        ctl.kc_set = 0;
+        ctl.nsel = 0;
+        ctl.nband = 0;
+        ctl.ntok = 0;
+    }
+    pdl_wait();
+    SKV_TRACE_POINT(0);
+    SKV_USTAMP(0);
+    const int Sb = S[b];
+    const int chunk = (Sb + kUC - 1) / kUC;
+    const int s0 = min(Sb, rank * chunk), s1 = min(Sb, s0 + chunk);
+    const int n = s1 - s0;
+    const int ntiles = (n + TS - 1) / TS;
+    const __nv_bfloat16* Eu = E + ((size_t)unit * Smax) * D;
+    const int32_t* o = off + (size_t)b * off_stride;
+    const int prev = sel.parity[unit], cur = prev ^ 1;
+    const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
+    const uint32_t klo = band.x, khi = band.y;
+
+    // ---------------------------------------------------------------- 1. score (D1)
+    if (tid == 0) {
+        const uint64_t pol = policy_evict_first();
+        for (int i = 0; i < kUStages && i < ntiles; ++i) {
+            const int ts = s0 + i * TS, m = min(TS, s1 - ts);
+            mbar_arrive_expect_tx(&bar[i], (uint32_t)(m * D * 2));
+            bulk_g2s_hint(ring + (size_t)i * TS * D, Eu + (size_t)ts * D, (uint32_t)(m * D * 2), &bar[i], pol);
+        }
+    }
+    // previous step's selected runs of this CTA's share (the L2 prefetch is issued after scoring,
+    // when HBM would otherwise idle during the selection)
+    constexpr int kPf = 4;
+    int pf_src[kPf], pf_len[kPf];
+#pragma unroll
+    for (int k = 0; k < kPf; ++k) pf_len[k] = 0;
+    if (prefetch && warp == kUW - 1) {
+        const int pc = *sel.count_of(prev, unit);
+        const int32_t* pt = sel.tok_of(prev, unit);
+        const int32_t* ps = sel.src_of(prev, unit);
+#pragma unroll
+        for (int k = 0; k < kPf; ++k) {
+            const int i = rank + kUC * (lane + 32 * k);
+            if (i < pc) {
+                pf_src[k] = ps[i];
+                pf_len[k] = pt[i + 1] - pt[i];
+            }
+        }
+    }
+    if (warp == kUW - 2) {
+        // does this step's input token end a sentence (Q_s reset after this step, A11)?
+        const int it = input_token[b];
+        const bool hit = (lane < nb && bset[lane] == it) || (lane + 32 < nb && bset[lane + 32] == it);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) ctl.reset = m ? 1 : 0;
+    }
+    // first context row of every local sentence (+ the end of the last)
+    for (int i = tid; i <= n; i += kUT) offs[i] = o[s0 + i];
+    // group query of this step: qbar_h = (Sq_h + q_h) / (cnt + 1) (the appended, not yet stored,
+    // Q_s), qt_g = ascending-h fp32 sum (canonical order, A23)
+    if (tid < D) {
+        const int c0 = cnt[unit];
+        const float c = (float)(c0 + 1);
+        float sv[GRP], qv[GRP];
+#pragma unroll
+        for (int h = 0; h < GRP; ++h) {
+            const size_t idx = ((size_t)b * Hq + g * GRP + h) * D + tid;
+            sv[h] = Sq[idx];
+            qv[h] = __bfloat162float(q[idx]);
+        }
+        float acc = 0.0f;
+#pragma unroll
+        for (int h = 0; h < GRP; ++h) {
+            const float sum = __fadd_rn(sv[h], qv[h]);
+            sqsum[h * D + tid] = sum;
+            const float qb = __fdiv_rn(sum, c);
+            acc = h == 0 ? qb : __fadd_rn(acc, qb);
+        }
+        qt[tid] = acc;
+        if (tid == 0) ctl.cnt0 = c0;
+    }
+    __syncthreads();
+    {
+        const int l = lane % LPS, gw = lane / LPS;
+        float qr[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qr[i] = qt[8 * l + i];
+        float* sc_out = scores + (size_t)unit * Smax;
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        for (int it = 0; it < ntiles; ++it) {
+            const int st = it % kUStages;
+            mbar_wait(&bar[st], (it / kUStages) & 1);
+            const __nv_bfloat16* tile = ring + (size_t)st * TS * D;
+            const int ts = it * TS, m = min(TS, n - ts);  // local index of the tile's first sentence
+#pragma unroll
+            for (int j = 0; j < TS / (kUW * GPW); ++j) {
+                const int r = (j * kUW + warp) * GPW + gw;
+                float f[8];
+                unpack8(*reinterpret_cast<const uint4*>(tile + (size_t)r * D + 8 * l), f);
+                float p = __fmul_rn(qr[0], f[0]);
+#pragma unroll
+                for (int i = 1; i < 8; ++i) p = __fmaf_rn(qr[i], f[i], p);
+#pragma unroll
+                for (int x = LPS / 2; x >= 1; x >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, x));
+                if (l == 0 && r < m) {
+                    const int i = ts + r;
+                    const uint32_t k = ordered_key(p);
+                    keys[i] = k;
+                    sc_out[s0 + i] = p;
+                    mn = min(mn, k);
+                    mx = max(mx, k);
+                    if (k >= klo) {  // band list: everything at or above the band's lower edge
+                        const uint32_t len = (uint32_t)(offs[i + 1] - offs[i]);
+                        const int pos = atomicAdd(&ctl.bn, 1);
+                        if (pos < kUBandCap) blist[pos] = make_int4((int)k, s0 + i, offs[i], (int)len);
+                        atomicAdd(k > khi ? &ctl.whi : &ctl.wband, len);
+                    }
+                }
+            }
+            __syncthreads();  // stage st fully read
+            if (tid == 0 && it + kUStages < ntiles) {
+                const int tn = s0 + (it + kUStages) * TS, nn = min(TS, s1 - tn);
+                mbar_arrive_expect_tx(&bar[st], (uint32_t)(nn * D * 2));
+                bulk_g2s_hint(ring + (size_t)st * TS * D, Eu + (size_t)tn * D, (uint32_t)(nn * D * 2), &bar[st],
+                              policy_evict_first());
+            }
+        }
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0 && n > 0) {
+            atomicMin(&ctl.lo, mn);
+            atomicMax(&ctl.hi, mx);
+        }
+    }
+    if (prefetch && warp == kUW - 1) {
+        // L2 prefetch of the previous step's selection (a hint: the attention reads whatever is
+        // selected now; selections change little from token to token)
+        const uint64_t pol = policy_evict_last();
+        const size_t ub = (size_t)unit * kv.unit_stride;
+#pragma unroll
+        for (int k = 0; k < kPf; ++k) {
+            const int len = pf_len[k], src = pf_src[k];
+            if (len > 0 && src >= 0 && (long long)src + len <= kv.unit_stride) {
+                prefetch_l2_hint(kv.K + (ub + src) * D, (uint32_t)(len * D * 2), pol);
+                prefetch_l2_hint(kv.V + (ub + src) * D, (uint32_t)(len * D * 2), pol);
+            }
+        }
+    }
+    __syncthreads();
+    SKV_USTAMP(1);
+    cluster.sync();  // #A: band lists and counters of every CTA are complete; every CTA has read Sq
+    SKV_USTAMP(2);
+
+    // ---------------------------------------------------------------- 2. select (D2)
+    // Fast path: the crossing point lies in the band [klo, khi] around the previous step's (the
+    // ranking changes little from token to token): everything above khi is selected and only the
+    // band is ranked.  Exact whenever its conditions hold; otherwise the general path below.
+    if (warp == 0) {
+        uint32_t whi = 0, wband = 0;
+        int bn = 0;
+        const int4* lp = nullptr;
+        if (lane < kUC) {
+            Ctl* rc = cluster.map_shared_rank(&ctl, lane);
+            whi = rc->whi;
+            wband = rc->wband;
+            bn = rc->bn;
+            lp = cluster.map_shared_rank(blist, lane);
+        }
+        const bool ovf = __any_sync(0xffffffffu, bn > kUBandCap);
+        const int incl = warp_incl_sum<int>(bn);
+        const uint32_t WHI = __reduce_add_sync(0xffffffffu, whi), WB = __reduce_add_sync(0xffffffffu, wband);
+        if (lane < kUC) {
+            ctl.base[lane + 1] = incl;
+            lists[lane] = lp;
+        }
+        if (lane == 0) {
+            ctl.base[0] = 0;
+            ctl.WHI = WHI;
+            ctl.ok = !ovf && WHI <= (uint32_t)tau && (WHI + WB > (uint32_t)tau || klo == 0u);
+#ifdef SKV_TRACE
+            if (unit * kUC + rank < 1024) {
+                g_unit_t[unit * kUC + rank][10] = (ovf ? 1 : 0) | (WHI > (uint32_t)tau ? 2 : 0) |
+                                                  (WHI + WB <= (uint32_t)tau && klo != 0u ? 4 : 0);
+                g_unit_t[unit * kUC + rank][13] = (unsigned long long)incl;
+            }
+#endif
+        }
+    }
+    __syncthreads();
+    bool ok = ctl.ok != 0;
+    if (ok) {
+        // gather: above-band entries are selected outright (sl), band entries are ranked
+        int4* sl = gath;                    // [kUBandSel] selected (unordered)
+        int4* bd = gath + kUBandSel;        // band entries
+        const int ntot = ctl.base[kUC];
+        for (int i = tid; i < ntot; i += kUT) {
+            int j = 0;
+            while (i >= ctl.base[j + 1]) ++j;
+            const int4 e = lists[j][i - ctl.base[j]];
+            if ((uint32_t)e.x > khi) {
+                const int p = atomicAdd(&ctl.nsel, 1);
+                if (p < kUBandSel) sl[p] = e;
+            } else {
+                bd[atomicAdd(&ctl.nband, 1)] = e;
+            }
+        }
+        __syncthreads();
+        if (ctl.nsel <= kUBandSel) {
+            const int nbd = ctl.nband;
+            const uint32_t WHI = ctl.WHI;
+            for (int i = tid; i < nbd; i += kUT) {
+                const int4 e = bd[i];
+                const unsigned long long ke = ukey64((uint32_t)e.x, e.y);
+                uint32_t w = WHI;
+                for (int c = 0; c < nbd; ++c) {
+                    const int4 f = bd[c];
+                    if (ukey64((uint32_t)f.x, f.y) > ke) w += (uint32_t)f.w;
+                }
+                if (w + (uint32_t)e.w <= (uint32_t)tau) {
+                    const int p = atomicAdd(&ctl.nsel, 1);
+                    if (p < kUBandSel) sl[p] = e;
+                } else if (w <= (uint32_t)tau) {
+                    ctl.kc = (uint32_t)e.x;  // the crossing sentence (unique)
+                    ctl.kc_set = 1;
+                }
+            }
+        }
+        __syncthreads();
+        const int ns = ctl.nsel;
+        ok = ns <= kUBandSel;
+#ifdef SKV_TRACE
+        if (tid == 0 && unit * kUC + rank < 1024) {
+            g_unit_t[unit * kUC + rank][10] |= ok ? 0 : 8;
+            g_unit_t[unit * kUC + rank][11] = ctl.nband;
+            g_unit_t[unit * kUC + rank][12] = ns;
+        }
+#endif
+        if (ok) {
+            // ascending sentence order by counting (ns is small)
+            for (int i = tid; i < ns; i += kUT) {
+                const int4 e = sl[i];
+                int pos = 0, toff = 0;
+                for (int c = 0; c < ns; ++c) {
+                    const int4 f = sl[c];
+                    if (f.y < e.y) {
+                        ++pos;
+                        toff += f.w;
+                    }
+                }
+                sel_tok[pos] = toff;
+                sel_src[pos] = e.z;
+                sel_id[pos] = e.y;
+                atomicAdd(&ctl.ntok, e.w);
+                atomicMin(&ctl.ks, (uint32_t)e.x);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                ctl.count = ns;
+                sel_tok[ns] = ctl.ntok;
+            }
+            __syncthreads();
+        }
+    }
+    SKV_USTAMP(3);
+    if (!ok) {
+        // ------------------------------------------------------------ general path
+        // 2a. local candidates
+        for (int i = tid; i < kUBins; i += kUT) hist[i] = 0u;
+        __syncthreads();
+        const int per_t = (n + kUT - 1) / kUT;
+        const int i0 = min(n, tid * per_t), i1 = min(n, i0 + per_t);
+        {
+            const Binner bin(ctl.lo, ctl.hi);
+            for (int i = i0; i < i1; ++i) atomicAdd(&hist[bin(keys[i])], (uint32_t)(offs[i + 1] - offs[i]));
+            __syncthreads();
+            uint32_t cb = 0, rem_unused;
+            const bool cross = crossing_bin(hist, (uint32_t)tau, ws32, ctl, &cb, &rem_unused);
+            // keep bins >= cb (all sentences if the CTA's total fits), in ascending sentence order
+            uint32_t mine = 0;
+            for (int i = i0; i < i1; ++i) mine += (!cross || bin(keys[i]) >= cb) ? 1u : 0u;
+            uint32_t total;
+            const uint32_t excl = block_incl_sum<uint32_t>(mine, ws32, &total) - mine;
+            const bool to_global = total > (uint32_t)kUOwnCap;
+            int4* dst = to_global ? cand_g + ((size_t)unit * kUC + rank) * kULocalCap : own;
+            uint32_t pos = excl;
+            for (int i = i0; i < i1; ++i) {
+                const uint32_t k = keys[i];
+                if (!cross || bin(k) >= cb) dst[pos++] = make_int4((int)k, s0 + i, offs[i], offs[i + 1] - offs[i]);
+            }
+            if (tid == 0) {
+                ctl.own_count = (int)total;
+                ctl.own_global = to_global ? 1 : 0;
+            }
+        }
+        cluster.sync();  // #1: every CTA's candidate list is complete
+        SKV_USTAMP(4);
+
+        // 2b. gather the lists
+        if (warp == 0) {
+            int c = 0;
+            const int4* lp = nullptr;
+            if (lane < kUC) {
+                Ctl* rc = cluster.map_shared_rank(&ctl, lane);
+                c = rc->own_count;
+                lp = rc->own_global ? cand_g + ((size_t)unit * kUC + lane) * kULocalCap
+                                    : cluster.map_shared_rank(own, lane);
+            }
+            const int incl = warp_incl_sum<int>(c);
+            if (lane < kUC) {
+                ctl.base[lane + 1] = incl;
+                lists[lane] = lp;
+            }
+            if (lane == 0) ctl.base[0] = 0;
+        }
+        __syncthreads();
+        const int ntot = ctl.base[kUC];
+        const bool gathered = ntot <= kUGather;
+        if (gathered) {
+            for (int i = tid; i < ntot; i += kUT) {
+                int j = 0;
+                while (i >= ctl.base[j + 1]) ++j;
+                gath[i] = lists[j][i - ctl.base[j]];
+            }
+        }
+        auto cand = [&](int i) -> int4 {
+            if (gathered) return gath[i];
+            int j = 0;
+            while (i >= ctl.base[j + 1]) ++j;
+            return lists[j][i - ctl.base[j]];
+        };
+        if (tid == 0) {
+            ctl.lo = 0xffffffffu;
+            ctl.hi = 0u;
+        }
+        __syncthreads();
+        const int per_c = (ntot + kUT - 1) / kUT;
+        const int c0 = min(ntot, tid * per_c), c1 = min(ntot, c0 + per_c);
+        {
+            uint32_t mn = 0xffffffffu, mx = 0u;
+            for (int i = c0; i < c1; ++i) {
+                const uint32_t k = (uint32_t)cand(i).x;
+                mn = min(mn, k);
+                mx = max(mx, k);
+            }
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0 && c0 < c1) {
+                atomicMin(&ctl.lo, mn);
+                atomicMax(&ctl.hi, mx);
+            }
+        }
+        __syncthreads();
+
+        // 2c. exact selection over the union of the lists
+        uint32_t lo = ctl.lo, hi = ctl.hi, rem = (uint32_t)tau;
+        bool all_fit = false;
+        unsigned long long thr = 0;  // select key64 > thr
+        for (int level = 0;; ++level) {
+            if (lo == hi) {
+                // the remaining contenders all carry key lo: ascending sentence order decides (A14)
+                uint32_t tw = 0;
+                for (int i = c0; i < c1; ++i) {
+                    const int4 e = cand(i);
+                    if ((uint32_t)e.x == lo) tw += (uint32_t)e.w;
+                }
+                uint32_t ttot;
+                const uint32_t before = block_incl_sum<uint32_t>(tw, ws32, &ttot) - tw;
+                if (level == 0 && ttot <= rem) {
+                    all_fit = true;
+                    break;
+                }
+                if (before <= rem && before + tw > rem) {
+                    uint32_t acc = before;
+                    for (int i = c0; i < c1; ++i) {
+                        const int4 e = cand(i);
+                        if ((uint32_t)e.x != lo) continue;
+                        acc += (uint32_t)e.w;
+                        if (acc > rem) {
+                            ctl.thr = ukey64(lo, e.y);
+                            break;
+                        }
+                    }
+                }
+                __syncthreads();
+                thr = ctl.thr;
+                break;
+            }
+            for (int i = tid; i < kUBins; i += kUT) hist[i] = 0u;
+            __syncthreads();
+            const Binner bin(lo, hi);
+            for (int i = c0; i < c1; ++i) {
+                const int4 e = cand(i);
+                const uint32_t k = (uint32_t)e.x;
+                if (k >= lo && k <= hi) atomicAdd(&hist[bin(k)], (uint32_t)e.w);
+            }
+            __syncthreads();
+            uint32_t cb, rem_in;
+            if (!crossing_bin(hist, rem, ws32, ctl, &cb, &rem_in)) {
+                // only possible at level 0 (the crossing bin of a level above holds more than rem)
+                all_fit = true;
+                break;
+            }
+            rem = rem_in;
+            if (tid == 0) {
+                ctl.lo = 0xffffffffu;
+                ctl.hi = 0u;
+                ctl.ncand = 0u;
+            }
+            __syncthreads();
+            {
+                uint32_t mn = 0xffffffffu, mx = 0u;
+                for (int i = c0; i < c1; ++i) {
+                    const int4 e = cand(i);
+                    const uint32_t k = (uint32_t)e.x;
+                    if (k < lo || k > hi || bin(k) != cb) continue;
+                    mn = min(mn, k);
+                    mx = max(mx, k);
+                    const uint32_t p = atomicAdd(&ctl.ncand, 1u);
+                    if (p < (uint32_t)kUExact) {
+                        ckey[p] = ukey64(k, e.y);
+                        clen[p] = (uint32_t)e.w;
+                    }
+                }
+                mn = __reduce_min_sync(0xffffffffu, mn);
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                if (lane == 0) {
+                    atomicMin(&ctl.lo, mn);
+                    atomicMax(&ctl.hi, mx);
+                }
+            }
+            __syncthreads();
+            if (ctl.ncand <= (uint32_t)kUExact) {
+                const int nc = (int)ctl.ncand;
+                if (tid < nc) {
+                    const unsigned long long mk = ckey[tid];
+                    uint32_t wabove = 0;
+                    for (int c = 0; c < nc; ++c)
+                        if (ckey[c] > mk) wabove += clen[c];
+                    if (wabove <= rem && wabove + clen[tid] > rem) ctl.thr = mk;
+                }
+                __syncthreads();
+                thr = ctl.thr;
+                break;
+            }
+            lo = ctl.lo;
+            hi = ctl.hi;
+            __syncthreads();
+        }
+
+        // 2d. ordered compaction (ascending ids + gathered token offsets)
+        unsigned long long mine = 0;
+        uint32_t kmin = 0xffffffffu;
+        for (int i = c0; i < c1; ++i) {
+            const int4 e = cand(i);
+            if (all_fit || ukey64((uint32_t)e.x, e.y) > thr) {
+                mine += (1ull << 32) | (uint32_t)e.w;
+                kmin = min(kmin, (uint32_t)e.x);
+            }
+        }
+        unsigned long long tot;
+        const unsigned long long excl = block_incl_sum<unsigned long long>(mine, ws64, &tot) - mine;
+        if (mine) {
+            int pos = (int)(excl >> 32);
+            int32_t toff = (int32_t)(excl & 0xffffffffull);
+            for (int i = c0; i < c1; ++i) {
+                const int4 e = cand(i);
+                if (all_fit || ukey64((uint32_t)e.x, e.y) > thr) {
+                    sel_tok[pos] = toff;
+                    sel_src[pos] = e.z;
+                    sel_id[pos] = e.y;
+                    ++pos;
+                    toff += e.w;
+                }
+            }
+            atomicMin(&ctl.ks, kmin);
+        }
+        if (tid == 0) {
+            const int count = (int)(tot >> 32);
+            ctl.count = count;
+            ctl.ntok = (int)(tot & 0xffffffffull);
+            sel_tok[count] = ctl.ntok;
+            ctl.kc = (uint32_t)(thr >> 32);
+            ctl.kc_set = all_fit ? 0 : 1;
+        }
+        __syncthreads();
+    }
+    SKV_USTAMP(5);
+
+    // ---------------------------------------------------------------- 3. gather + attend (D3 + D4)
+    const int count = ctl.count, ntok = ctl.ntok;
+    const int ntl = (ntok + kTile - 1) / kTile;
+    const int per = (ntl + kUC - 1) / kUC;
+    const int tb = min(ntl, rank * per), te = min(ntl, tb + per);
+    const int T0 = tb * kTile, T1 = min(ntok, te * kTile);
+    for (int t = T0 + tid; t < te * kTile; t += kUT) {
+        int r = kInvalid;
+        if (t < T1) {
+            int lo2 = 0, hi2 = count - 1;  // largest i with sel_tok[i] <= t
+            while (lo2 < hi2) {
+                const int mid = (lo2 + hi2 + 1) >> 1;
+                if (sel_tok[mid] <= t) lo2 = mid; else hi2 = mid - 1;
+            }
+            r = sel_src[lo2] + (t - sel_tok[lo2]);
+        }
+        rowtab[t - T0] = r;
+    }
+    __syncthreads();
+    SKV_USTAMP(6);
+    {
+        const int gq = lane >> 2, cq = lane & 3;
+        const __nv_bfloat16* Kd = kv.K + (size_t)unit * kv.unit_stride * D;
+        const __nv_bfloat16* Vd = kv.V + (size_t)unit * kv.unit_stride * D;
+        uint4 qseg[D / 32];
+        mma::load_q<D, GRP>(qseg, q + ((size_t)b * Hq + g * GRP) * D, lane);
+        mma::WarpAcc<D> wacc;
+        wacc.init();
+        for (int tile = tb + warp; tile < te; tile += kUW) {
+            const int t0 = tile * kTile;
+            const int rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+            const __nv_bfloat16* pv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int rv = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+                pv[k] = rv != kInvalid ? Vd + (size_t)rv * D : nullptr;
+            }
+            mma::TileRegs<D> tr;
+            mma::load_tile<D>(tr, rk0 != kInvalid ? Kd + (size_t)rk0 * D : nullptr,
+                              rk1 != kInvalid ? Kd + (size_t)rk1 * D : nullptr, pv, lane);
+            mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
+        }
+        SKV_USTAMP(7);
+        // ---- stores of this step's state, spread over the CTAs (nothing waits on them) ----
+        {
+            const int sh = (count + kUC - 1) / kUC;  // selection entries written by this CTA
+            int32_t* gids = sel.ids_of(cur, unit);
+            int32_t* gtok = sel.tok_of(cur, unit);
+            int32_t* gsrc = sel.src_of(cur, unit);
+            for (int i = rank * sh + tid; i < min(count, (rank + 1) * sh); i += kUT) {
+                gids[i] = sel_id[i];
+                gtok[i] = sel_tok[i];
+                gsrc[i] = sel_src[i];
+                if (out_ids) out_ids[(size_t)unit * tau + i] = sel_id[i];
+            }
+            if (out_ids) {
+                const int pad = (tau - count + kUC - 1) / kUC;
+                for (int i = count + rank * pad + tid; i < min(tau, count + (rank + 1) * pad); i += kUT)
+                    out_ids[(size_t)unit * tau + i] = -1;
+            }
+            if (rank == 0) {
+                // deferred Eq. 2 state update: Sq += q_t, or reset after a boundary input (A11)
+                const bool reset = ctl.reset != 0;
+                for (int i = tid; i < GRP * D; i += kUT)
+                    Sq[((size_t)b * Hq + g * GRP) * D + i] = reset ? 0.0f : sqsum[i];
+                if (tid == 0) {
+                    cnt[unit] = reset ? 0 : ctl.cnt0 + 1;
+                    gtok[count] = ntok;
+                    *sel.count_of(cur, unit) = count;
+                    if (out_count) out_count[unit] = count;
+                    if (out_tokens) out_tokens[unit] = ntok;
+                }
+            }
+            if (rank == kUC - 1 && tid == 0) {
+                // the next step's band: the crossing point and the lowest selected key, widened
+                uint2 h = make_uint2(0u, 0xffffffffu);  // everything fits: the band is everything
+                if (ctl.kc_set) {
+                    const uint32_t kc = ctl.kc, ks = ctl.ks, w = (uint32_t)band_w;
+                    h.x = kc > w ? kc - w : 0u;
+                    h.y = ks < 0xffffffffu - w ? ks + w : 0xffffffffu;
+                }
+                hint[unit] = h;
+            }
+        }
+        mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
+    }
+    pdl_trigger();
+    cluster.sync();  // #2: CTA partials ready
+    SKV_USTAMP(8);
+    mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT);
+    cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
+    if (rank == 0 && tid == 0) sel.parity[unit] = cur;
+    SKV_USTAMP(9);
+}
+
+size_t unit_smem_bytes(int d, int tau) {
+    (void)d;
+    const size_t rows = (((size_t)tau + kTile - 1) / kTile + kUC - 1) / kUC * kTile;
+    return (size_t)kUStages * kUTileBytes + sizeof(uint32_t) * kULocalCap + sizeof(int32_t) * (kULocalCap + 4) +
+           sizeof(int4) * (kUOwnCap + kUBandCap) + sizeof(int32_t) * (3 * (size_t)tau + 1 + rows);
+}
+
+bool unit_supported(int d, int grp, int Smax, int tau) {
+    return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap && unit_smem_bytes(d, tau) <= 200 * 1024;
+}
+
+size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
+
+bool unit_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_UNIT");
+        return !(e && e[0] == '0');  // SKV_UNIT=0 selects the score / select / attend kernels
+    }();
+    return on;
+}
+
+static int band_width() {
+    static const int w = [] {
+        const char* e = getenv("SKV_BAND_LOG2");  // half-width of the band in ordered-key units (2^19 ~ 6%)
+        const int l = e ? atoi(e) : 19;
+        return l <= 0 ? 0 : (1 << std::min(l, 30));
+    }();
+    return w;
+}
+
+static bool prefetch_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_PREFETCH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <int D, int GRP>
+static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
+    const size_t smem = unit_smem_bytes(D, a.sel.tau);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(unit_step_kernel<D, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(unit_step_kernel<D, GRP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
+    return launch_pdl(unit_step_kernel<D, GRP>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st, a.q, a.input_token, a.bset,
+                      a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.cand,
+                      a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.out, a.out_ids, a.out_count, a.out_tokens,
+                      scale_log2);
+}
+
+cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
+#define SKV_UN(DV, GV) return launch_unit_t<DV, GV>(a, st)
+    if (d == 128) {
+        switch (grp) {
+            case 1: SKV_UN(128, 1);
+            case 2: SKV_UN(128, 2);
+            case 4: SKV_UN(128, 4);
+            case 8: SKV_UN(128, 8);
+        }
+    } else {
+        switch (grp) {
+            case 1: SKV_UN(64, 1);
+            case 2: SKV_UN(64, 2);
+            case 4: SKV_UN(64, 4);
+            case 8: SKV_UN(64, 8);
+        }
+    }
+#undef SKV_UN
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace skv

@@ -81,6 +81,7 @@ struct LayerState {
     float* lk_part_o = nullptr;        // [units][n_att][8][d]
     int4* lk_cand = nullptr;           // [units][n_score_max][NL] local selection candidates
     int32_t* lk_cand_count = nullptr;  // [units][n_score_max]
+    uint2* unit_hint = nullptr;        // [units] one-launch step kernel: band of the selection's crossing point
 };
 
 }  // namespace skv
@@ -106,6 +107,7 @@ struct skv_ctx {
     int2* lk_items = nullptr;          // device work queue of the per-layer kernel (per prompt)
     int lk_n_items = 0;
     int lk_n_score_max = 0;            // SCORE items of the longest sequence (per-layer candidate lists)
+    int4* unit_cand = nullptr;         // overflow scratch of the per-unit step kernel's candidate lists
 
     // kernel profiler: (kind, start, stop) event triples awaiting a read
     bool profiling = false;
@@ -235,5 +237,35 @@ cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, 
                                        const int32_t* input_token, const int32_t* bset, int nb, float* Sq,
                                        int32_t* cnt, KvSrc kv, SelBufs sel, int32_t* out_ids, int32_t* out_count,
                                        int32_t* out_tokens, float* out, cudaStream_t st);
+
+// ---- one launch per layer and step (decode_unit.cu): D1-D4 in one cluster per (b, g) unit ----
+struct UnitArgs {
+    const __nv_bfloat16* q;        // [B][Hq][d]
+    const int32_t* input_token;    // [B]
+    const int32_t* bset;
+    int nb;
+    float* Sq;                     // [B][Hq][d]
+    int32_t* cnt;                  // [B][G]
+    const __nv_bfloat16* E;        // [B][G][Smax][d]
+    const int32_t* S;              // [B]
+    const int32_t* off;            // [B][off_stride]
+    int off_stride;
+    int B, G, Smax;
+    float* scores;                 // [B][G][Smax]
+    SelBufs sel;
+    KvSrc kv;                      // device residency: context K/V
+    int4* cand;                    // [unit_cand_entries] overflow scratch of the candidate lists
+    uint2* hint;                   // [units] selection band of the previous step (klo, khi ordered keys)
+    int prefetch;                  // L2 prefetch of the previous step's selection
+    float* out;                    // [B][Hq][d]
+    int32_t* out_ids;              // optional [B][G][tau]
+    int32_t* out_count;            // optional [B][G]
+    int32_t* out_tokens;           // optional [B][G]
+};
+bool unit_enabled();
+bool unit_supported(int d, int grp, int Smax, int tau);
+size_t unit_smem_bytes(int d, int tau);
+size_t unit_cand_entries(int units);
+cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st);
 
 }  // namespace skv

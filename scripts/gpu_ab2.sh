@@ -1,0 +1,23 @@
+#!/bin/bash
+# GPU call: parity tests, then A/B benches of decode_step variants (device residency)
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.txt 2>&1
+tail -3 gpurun_out/pytest_gpu.txt
+run() {  # name, env...
+  local name=$1; shift
+  env "$@" timeout 600 python bench.py --steps 300 --warmup 10 --residency device --no-cpu-baseline --e2e-steps 20 > gpurun_out/bench_$name.txt 2>&1
+  python - "$name" <<'PY'
+import json, sys
+f = f"gpurun_out/bench_{sys.argv[1]}.txt"
+try:
+    d = json.loads(open(f).read().strip().splitlines()[-1])
+    print(sys.argv[1], "ms/step", d["ms_per_step"], {k: (v["avg_us"], v["gbs"]) for k, v in d["kernels"].items()}, "e2e", d["e2e"]["ms_per_step"], "frac", d["roofline"]["frac"])
+except Exception as e:
+    print(f, "ERR", e, open(f).read()[-1500:])
+PY
+}
+run unit
+run unit_nopf SKV_PREFETCH=0
+run unit_pdl SKV_PDL=1
+run split SKV_UNIT=0
+timeout 900 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 20 > gpurun_out/bench_host.txt 2>&1; tail -c 600 gpurun_out/bench_host.txt

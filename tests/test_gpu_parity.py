@@ -150,6 +150,36 @@ def test_many_one_token_sentences(cuda_device):
     _custom_case(cuda_device, toks, K, V, qs, np.full((2, B), 300, np.int32), tau, Hq, G, d)
 
 
+@pytest.mark.parametrize("L", [3000, 12000])
+def test_one_token_sentences_zero_query(cuda_device, L):
+    """q = 0 on one-token sentences: every score ties at +0, so the one-launch step kernel keeps every
+    sentence as a local candidate (L = 12000: lists overflow shared memory into the global scratch
+    and the union is ranked in place); the selection must still be the first tau sentences."""
+    B, Hq, G, d, tau = 1, 8, 2, 64, 100
+    toks = np.full((B, L), synth.BOUNDARY_IDS[2], np.int32)
+    rng = np.random.default_rng(L)
+    K = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    V = synth.f32_to_bf16_bits(rng.standard_normal((B, G, L, d)).astype(np.float32))
+    q0 = np.zeros((B, Hq, d), np.uint16)
+    q1 = synth.f32_to_bf16_bits(rng.standard_normal((B, Hq, d)).astype(np.float32))
+    _custom_case(cuda_device, toks, K, V, [q0, q0, q1], np.array([[300], [13], [300]], np.int32), tau, Hq, G, d)
+
+
+def test_unit_step_kernel_off_parity_subprocess(cuda_device):
+    """decode_step with the one-launch step kernel switched off (SKV_UNIT=0: score, select and attend
+    kernels) must pass the same decode_step parity cases."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_UNIT="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
+                        "-k", "(step or ties or all_equal or tau_cap or one_token) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_deterministic_run_to_run(cuda_device):
     B, M, Hq, G, d, L, tau, steps = 2, 1, 8, 2, 128, 6000, 512, 5
     toks, _, Ks, Vs, qs, script = make_case(8, B, M, Hq, G, d, L, tau, steps, median=25.0)
@@ -180,7 +210,7 @@ def test_fused_select_attend_kernel_parity_subprocess(cuda_device):
     import subprocess
     import sys
 
-    env = dict(os.environ, SKV_FUSED="1", SKV_LAYER="0")
+    env = dict(os.environ, SKV_FUSED="1", SKV_LAYER="0", SKV_UNIT="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
                         "-k", "(step or ties or all_equal or tau_cap or many_one) and not subprocess"],
@@ -264,7 +294,7 @@ def test_persistent_layer_kernel_parity_subprocess(cuda_device):
     import subprocess
     import sys
 
-    env = dict(os.environ, SKV_LAYER="1")
+    env = dict(os.environ, SKV_LAYER="1", SKV_UNIT="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
                         "tests/test_gpu_fullsize.py",
