@@ -90,6 +90,9 @@ void free_layer_prompt(skv::LayerState& ls) {
     dfree(ls.lk_cand);
     dfree(ls.lk_cand_count);
     dfree(ls.unit_hint);
+    dfree(ls.pc_pt);
+    dfree(ls.pc_own);
+    dfree(ls.pc_hand);
 }
 
 void free_host_store(skv::LayerState& ls) {
@@ -279,6 +282,41 @@ SKV_API skv_status sentencekv_sync(skv_ctx* c) {
     return c->sticky;
 }
 
+// Host residency, one-launch kernel: pages of the HBM working set per unit, floor(r * tau) tokens.
+static int cache_slots(const skv_ctx* c) {
+    const long long cap = (long long)std::floor((double)c->cfg.semantic_factor * (double)c->tau);
+    return (int)std::max(1LL, cap / skv::unit_page_tokens());
+}
+
+// Empties the page cache of a layer (every page -> host).
+static skv_status reset_page_cache(skv_ctx* c, skv::LayerState& ls, cudaStream_t st) {
+    const size_t U = (size_t)c->B * c->G;
+    SKV_CUDA(c, cudaMemsetAsync(ls.pc_pt, 0xff, sizeof(int32_t) * U * ls.pc_pages, st));
+    SKV_CUDA(c, cudaMemsetAsync(ls.pc_own, 0xff, sizeof(int32_t) * U * cache_slots(c), st));
+    SKV_CUDA(c, cudaMemsetAsync(ls.pc_hand, 0, sizeof(int32_t) * U, st));
+    ls.last_path = 0;
+    return SKV_OK;
+}
+
+// Host residency keeps a working set per path (split kernels: previous + current selection;
+// one-launch kernel: page cache).  Switching paths on a layer forgets the other path's state:
+// no previous selection (the split path has no hits, the page-cache plan nothing to fill).
+static skv_status switch_host_path(skv_ctx* c, skv::LayerState& ls, int path, cudaStream_t st) {
+    if (c->cfg.residency != SKV_KV_HOST || ls.last_path == path) {
+        ls.last_path = path;
+        return SKV_OK;
+    }
+    if (ls.last_path != 0) {
+        SKV_CUDA(c, cudaMemsetAsync(ls.sel.count, 0, sizeof(int32_t) * 2 * c->B * c->G, st));
+        if (path == 1) {
+            skv_status s = reset_page_cache(c, ls, st);
+            if (s != SKV_OK) return s;
+        }
+    }
+    ls.last_path = path;
+    return SKV_OK;
+}
+
 // (Re)allocates the sentence-dependent buffers of every layer for a prompt with capacity Smax.
 static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
     const size_t B = c->B, G = c->G, d = c->d, tau = c->tau, U = B * G;
@@ -294,8 +332,15 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
         SKV_CUDA(c, dalloc(&sb.count, 2 * U));
         SKV_CUDA(c, dalloc(&sb.parity, U));
         if (c->cfg.residency == SKV_KV_HOST) {
-            SKV_CUDA(c, dalloc(&ls.wsK, U * 2 * tau * d));
-            SKV_CUDA(c, dalloc(&ls.wsV, U * 2 * tau * d));
+            // split kernels: [U][2][tau] gathered rows; one-launch kernel: [U][slots][page] rows
+            const size_t rows = std::max((size_t)2 * tau, (size_t)cache_slots(c) * skv::unit_page_tokens());
+            SKV_CUDA(c, dalloc(&ls.wsK, U * rows * d));
+            SKV_CUDA(c, dalloc(&ls.wsV, U * rows * d));
+            const int P = skv::unit_page_tokens();
+            ls.pc_pages = (c->cfg.max_context + P - 1) / P;
+            SKV_CUDA(c, dalloc(&ls.pc_pt, U * (size_t)ls.pc_pages));
+            SKV_CUDA(c, dalloc(&ls.pc_own, U * (size_t)cache_slots(c)));
+            SKV_CUDA(c, dalloc(&ls.pc_hand, U));
         }
         const size_t n_att = (size_t)skv::layer_attend_items((int)tau);
         SKV_CUDA(c, dalloc(&ls.lk_counters, 3 + 3 * U));
@@ -381,6 +426,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             // no band yet (klo = 0, khi = max: everything is in the band)
             SKV_CUDA(c, cudaMemsetAsync(ls.unit_hint, 0xff, sizeof(uint2) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemset2DAsync(ls.unit_hint, sizeof(uint2), 0, sizeof(uint32_t), (size_t)c->B * c->G, st));
+            if (c->cfg.residency == SKV_KV_HOST) {
+                skv_status rs = reset_page_cache(c, ls, st);
+                if (rs != SKV_OK) return rs;
+            }
         }
     }
 
@@ -439,6 +488,10 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    {
+        skv_status ps = switch_host_path(c, ls, 2, st);
+        if (ps != SKV_OK) return ps;
+    }
     cudaEvent_t pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
     prof_end(c, SKV_K_SCORE, pa, st);
@@ -464,10 +517,20 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
-    if (skv::unit_enabled() && c->cfg.residency == SKV_KV_DEVICE &&
-        skv::unit_supported(c->d, c->grp, c->Smax, c->tau)) {
+    const bool host = c->cfg.residency == SKV_KV_HOST;
+    if (skv::unit_enabled() && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
+        if (host) {
+            if (!ls.host_ready) {  // first decode of the layer after its prefill: the offload must be done
+                SKV_CUDA(c, cudaEventSynchronize(ls.offload_done));
+                ls.host_ready = true;
+            }
+            skv_status ps = switch_host_path(c, ls, 1, st);
+            if (ps != SKV_OK) return ps;
+            a.hc = skv::HostCache{ls.Kh, ls.Vh, ls.wsK, ls.wsV, ls.pc_pt, ls.pc_own, ls.pc_hand, cache_slots(c),
+                                  ls.pc_pages, c->L, ls.ledger};
+        }
         a.q = qb;
         a.input_token = input_token;
         a.bset = c->bset;

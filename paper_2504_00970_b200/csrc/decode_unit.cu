@@ -76,7 +76,11 @@ constexpr int kUC = 8;                   // CTAs per cluster (= per unit)
 constexpr int kUTileBytes = 16384;       // E bytes per TMA stage
 constexpr int kUStages = 3;
 constexpr int kULocalCap = 2048;         // sentences per CTA (supported: Smax <= kUC * kULocalCap)
-constexpr int kUOwnCap = 512;            // own candidate list kept in shared memory (else global scratch)
+constexpr int kUOwnCap = 256;            // own candidate list kept in shared memory (else global scratch)
+constexpr int kPage = 16;                // host residency: tokens per working-set page
+constexpr int kNeedCap = 256;            // host residency: pages of a selection tracked by the cache plan
+constexpr int kMaxSlots = 1024;          // host residency: working-set pages per unit
+constexpr uint32_t kEmpty = 0xffffffffu; // page-table entry of a page that is not resident
 constexpr int kUBins = 1024;
 constexpr int kUExact = kUT;             // crossing-bin candidates ranked exactly per refinement level
 constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
@@ -176,12 +180,12 @@ __device__ __forceinline__ bool crossing_bin(const uint32_t* hist, uint32_t rem,
 
 }  // namespace
 
-template <int D, int GRP>
+template <int D, int GRP, bool HOST>
 __global__ void __cluster_dims__(kUC, 1, 1) __launch_bounds__(kUT, 2)
 unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
                  const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq, int32_t* __restrict__ cnt,
                  const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
-                 int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv,
+                 int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
                  float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, float scale_log2) {
@@ -205,7 +209,17 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int32_t* sel_tok = reinterpret_cast<int32_t*>(blist + kUBandCap);  // [tau + 1]
     int32_t* sel_src = sel_tok + (tau + 1);                              // [tau]
     int32_t* sel_id = sel_src + tau;                                     // [tau]
-    int32_t* rowtab = sel_id + tau;                                      // [rows per CTA]
+    int2* rowtab = reinterpret_cast<int2*>(sel_tok + (3 * tau + 5) / 4 * 4);  // [rows per CTA] (source, write-through row)
+    // host residency: the page-cache plan of this step, in the ring behind the merge area
+    constexpr int kPlanOff = (int)((sizeof(USmemMerge<D>) + 127) / 128 * 128);
+    int* need = reinterpret_cast<int*>(smem_raw + kPlanOff);            // [kNeedCap] pages of the selection
+    uint32_t* pslot = reinterpret_cast<uint32_t*>(need + kNeedCap);     // [kNeedCap] their page-table entries
+    int* slotof = reinterpret_cast<int*>(pslot + kNeedCap);             // [kNeedCap] slot this step (-1 none)
+    int* oldof = slotof + kNeedCap;                                     // [kNeedCap] page evicted for it
+    uint32_t* rowbits = reinterpret_cast<uint32_t*>(oldof + kNeedCap);  // [kNeedCap] selected rows
+    int* newj = reinterpret_cast<int*>(rowbits + kNeedCap);             // [kNeedCap] non-resident pages
+    int* frees = newj + kNeedCap;                                       // [kNeedCap] their slots
+    static_assert(!HOST || kPlanOff + kNeedCap * 28 <= kUStages * kUTileBytes, "plan fits the ring");
 
     __shared__ uint64_t bar[kUStages];
     __shared__ float qt[D];
@@ -217,6 +231,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     __shared__ uint32_t clen[kUExact];
     __shared__ Ctl ctl;
     __shared__ const int4* lists[kUC];
+    __shared__ int n_need_s, last_slot_s;
 
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -267,7 +282,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int pf_src[kPf], pf_len[kPf];
 #pragma unroll
     for (int k = 0; k < kPf; ++k) pf_len[k] = 0;
-    if (prefetch && warp == kUW - 1) {
+    if (!HOST && prefetch && warp == kUW - 1) {
         const int pc = *sel.count_of(prev, unit);
         const int32_t* pt = sel.tok_of(prev, unit);
         const int32_t* ps = sel.src_of(prev, unit);
@@ -365,7 +380,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             atomicMax(&ctl.hi, mx);
         }
     }
-    if (prefetch && warp == kUW - 1) {
+    if (!HOST && prefetch && warp == kUW - 1) {
         // L2 prefetch of the previous step's selection (a hint: the attention reads whatever is
         // selected now; selections change little from token to token)
         const uint64_t pol = policy_evict_last();
@@ -725,15 +740,132 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int per = (ntl + kUC - 1) / kUC;
     const int tb = min(ntl, rank * per), te = min(ntl, tb + per);
     const int T0 = tb * kTile, T1 = min(ntok, te * kTile);
+    if constexpr (HOST) {
+        // Host residency (D3 host): the HBM working set is a page cache (pages of kPage
+        // context rows); a page-table entry holds the page's slot and the mask of its rows already
+        // in HBM.  Plan of this step, identical in every CTA (ascending page / clock order): pages
+        // of the selection that are not resident get a slot whose page the selection does not use
+        // (clock order from the hand); rows read from host are written through to their slot.
+        uint32_t* ownc = hist;  // slot -> page, copied (the histogram is idle now)
+        static_assert(kUBins >= kMaxSlots, "slot table fits the histogram");
+        if (warp == 0) {
+            for (int j = lane; j < kNeedCap; j += 32) rowbits[j] = 0u;
+            __syncwarp();
+            int n_need = 0, carry = -1;  // carry: last page of the previous sentence
+            for (int base = 0; base < count; base += 32) {
+                const int i = base + lane;
+                int p0 = 0, p1 = -1, r0 = 0, r1 = -1;
+                if (i < count) {
+                    r0 = sel_src[i];
+                    r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
+                    p0 = r0 / kPage;
+                    p1 = r1 / kPage;
+                }
+                int pp = __shfl_up_sync(0xffffffffu, p1, 1);
+                if (lane == 0) pp = carry;
+                const bool shared = p1 >= 0 && p0 == pp;  // first page already listed by the previous sentence
+                const int first = shared ? p0 + 1 : p0;
+                const int cntp = p1 >= first ? p1 - first + 1 : 0;
+                const int incl = warp_incl_sum<int>(cntp);
+                const int pos0 = n_need + incl - cntp;
+                for (int p = first, pos = pos0; p <= p1 && pos < kNeedCap; ++p, ++pos) need[pos] = p;
+                __syncwarp();
+                for (int p = p0; p <= p1; ++p) {  // this sentence's rows of page p
+                    const int j = (shared && p == p0) ? pos0 - 1 : pos0 + (p - first);
+                    const int lo = max(r0, p * kPage) - p * kPage, hi = min(r1, p * kPage + kPage - 1) - p * kPage;
+                    if (j >= 0 && j < kNeedCap) atomicOr(&rowbits[j], ((2u << hi) - 1u) & ~((1u << lo) - 1u));
+                }
+                n_need = min(kNeedCap, n_need + __shfl_sync(0xffffffffu, incl, 31));
+                const int last = __shfl_sync(0xffffffffu, p1, min(31, count - 1 - base));
+                carry = last >= 0 ? last : carry;
+            }
+            if (lane == 0) n_need_s = n_need;
+        }
+        __syncthreads();
+        const int n_need = n_need_s;
+        for (int j = tid; j < n_need; j += kUT) pslot[j] = hc.pt[(size_t)unit * hc.pages + need[j]];
+        for (int j = tid; j < hc.slots; j += kUT) ownc[j] = (uint32_t)hc.own[(size_t)unit * hc.slots + j];
+        __syncthreads();
+        if (warp == 0) {
+            // new pages (ascending) -> free slots (clock order from the hand): empty, or holding a page
+            // this selection does not use
+            const unsigned lt = (1u << lane) - 1u;
+            for (int j = lane; j < n_need; j += 32) {
+                const uint32_t e = pslot[j];
+                slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
+                oldof[j] = -1;
+            }
+            int n_new = 0;
+            for (int j0 = 0; j0 < n_need; j0 += 32) {
+                const int j = j0 + lane;
+                const bool nw = j < n_need && pslot[j] == kEmpty;
+                const unsigned m = __ballot_sync(0xffffffffu, nw);
+                if (nw) newj[n_new + __popc(m & lt)] = j;
+                n_new += __popc(m);
+            }
+            int n_free = 0;
+            const int hand = hc.hand[unit];
+            for (int t0 = 0; t0 < hc.slots && n_free < n_new; t0 += 32) {
+                const int t = t0 + lane;
+                bool fr = false;
+                int sl = 0;
+                if (t < hc.slots) {
+                    sl = (hand + t) % hc.slots;
+                    const int o = (int)ownc[sl];
+                    fr = o < 0;
+                    if (!fr) {  // is page o used by this selection? (need is ascending)
+                        int lo = 0, hi = n_need;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (need[mid] < o) lo = mid + 1; else hi = mid;
+                        }
+                        fr = !(lo < n_need && need[lo] == o);
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, fr);
+                if (fr) {
+                    const int k = n_free + __popc(m & lt);
+                    if (k < n_new) frees[k] = sl;
+                }
+                n_free += __popc(m);
+            }
+            const int n_asg = min(n_new, n_free);
+            __syncwarp();
+            for (int k = lane; k < n_asg; k += 32) {
+                const int j = newj[k], sl = frees[k];
+                slotof[j] = sl;
+                oldof[j] = (int)ownc[sl];
+            }
+            if (lane == 0) last_slot_s = n_asg > 0 ? frees[n_asg - 1] : -1;
+        }
+        __syncthreads();
+    }
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
-        int r = kInvalid;
+        int2 r = make_int2(kInvalid, -1);
         if (t < T1) {
             int lo2 = 0, hi2 = count - 1;  // largest i with sel_tok[i] <= t
             while (lo2 < hi2) {
                 const int mid = (lo2 + hi2 + 1) >> 1;
                 if (sel_tok[mid] <= t) lo2 = mid; else hi2 = mid - 1;
             }
-            r = sel_src[lo2] + (t - sel_tok[lo2]);
+            const int row = sel_src[lo2] + (t - sel_tok[lo2]);
+            r.x = row;
+            if constexpr (HOST) {
+                // row held in its slot -> working-set row; else host row -(row+1), written through
+                // to the slot of its page (if it has one this step)
+                const int p = row / kPage, w = row % kPage, n_need = n_need_s;
+                int lo = 0, hi = n_need;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (need[mid] < p) lo = mid + 1; else hi = mid;
+                }
+                r.x = -(row + 1);
+                if (lo < n_need && need[lo] == p) {
+                    const uint32_t e = pslot[lo];
+                    if (e != kEmpty && ((e >> (16 + w)) & 1u)) r.x = (int)(e & 0xffffu) * kPage + w;
+                    else if (slotof[lo] >= 0) r.y = slotof[lo] * kPage + w;
+                }
+            }
         }
         rowtab[t - T0] = r;
     }
@@ -741,27 +873,66 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     SKV_USTAMP(6);
     {
         const int gq = lane >> 2, cq = lane & 3;
-        const __nv_bfloat16* Kd = kv.K + (size_t)unit * kv.unit_stride * D;
-        const __nv_bfloat16* Vd = kv.V + (size_t)unit * kv.unit_stride * D;
+        // device residency: rows of the context K/V; host residency: r >= 0 working-set row, r < 0 host
+        // row -(r+1) of the mapped pinned store
+        const __nv_bfloat16* Kd = HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D;
+        const __nv_bfloat16* Vd = HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D;
+        const __nv_bfloat16* Khu = HOST ? hc.Kh + (size_t)unit * hc.L * D : nullptr;
+        const __nv_bfloat16* Vhu = HOST ? hc.Vh + (size_t)unit * hc.L * D : nullptr;
+        auto rowK = [&](int r) -> const __nv_bfloat16* {
+            return (HOST && r < 0) ? Khu + (size_t)(-(r + 1)) * D : Kd + (size_t)r * D;
+        };
+        auto rowV = [&](int r) -> const __nv_bfloat16* {
+            return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : Vd + (size_t)r * D;
+        };
+        unsigned long long host_bytes = 0;
         uint4 qseg[D / 32];
         mma::load_q<D, GRP>(qseg, q + ((size_t)b * Hq + g * GRP) * D, lane);
         mma::WarpAcc<D> wacc;
         wacc.init();
         for (int tile = tb + warp; tile < te; tile += kUW) {
             const int t0 = tile * kTile;
-            const int rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+            const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+            int2 rv[4];
             const __nv_bfloat16* pv[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const int rv = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
-                pv[k] = rv != kInvalid ? Vd + (size_t)rv * D : nullptr;
+                rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+                pv[k] = rv[k].x != kInvalid ? rowV(rv[k].x) : nullptr;
             }
             mma::TileRegs<D> tr;
-            mma::load_tile<D>(tr, rk0 != kInvalid ? Kd + (size_t)rk0 * D : nullptr,
-                              rk1 != kInvalid ? Kd + (size_t)rk1 * D : nullptr, pv, lane);
+            mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr, rk1.x != kInvalid ? rowK(rk1.x) : nullptr,
+                              pv, lane);
             mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
+            if constexpr (HOST) {
+                // write-through of the rows read from host into their working-set slot
+                constexpr int NU = D / 32, NVP = D / 64;
+                __nv_bfloat16* Kw = hc.wsK + (size_t)unit * hc.slots * kPage * D;
+                __nv_bfloat16* Vw = hc.wsV + (size_t)unit * hc.slots * kPage * D;
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + cq * (D / 4) + 8 * u) = tr.kA[u];
+                    if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + cq * (D / 4) + 8 * u) = tr.kB[u];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int pp = 0; pp < NVP; ++pp)
+                        if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
+                // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
+                if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
+                if (gq == 0)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
+            }
         }
         SKV_USTAMP(7);
+        if constexpr (HOST) {
+            // transfer ledger: host rows read by this CTA
+#pragma unroll
+            for (int o2 = 16; o2 >= 1; o2 >>= 1) host_bytes += __shfl_xor_sync(0xffffffffu, host_bytes, o2);
+            if (lane == 0 && host_bytes) atomicAdd(hc.ledger, host_bytes);
+        }
         // ---- stores of this step's state, spread over the CTAs (nothing waits on them) ----
         {
             const int sh = (count + kUC - 1) / kUC;  // selection entries written by this CTA
@@ -809,6 +980,22 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     cluster.sync();  // #2: CTA partials ready
     SKV_USTAMP(8);
     mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT);
+    if (HOST && rank == 0) {
+        // page-table update of this step's plan (every CTA has done its lookups: after barrier #2);
+        // all selected rows of a page with a slot are in it now
+        const int n_need = n_need_s;
+        int32_t* pt = hc.pt + (size_t)unit * hc.pages;
+        for (int j = tid; j < n_need; j += kUT) {
+            const int sl = slotof[j];
+            if (sl < 0) continue;
+            const uint32_t e = pslot[j];
+            const uint32_t mask = (e == kEmpty ? 0u : (e >> 16)) | rowbits[j];
+            pt[need[j]] = (int32_t)((uint32_t)sl | (mask << 16));
+            hc.own[(size_t)unit * hc.slots + sl] = need[j];
+            if (oldof[j] >= 0) pt[oldof[j]] = (int32_t)kEmpty;
+        }
+        if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
+    }
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
     if (rank == 0 && tid == 0) sel.parity[unit] = cur;
     SKV_USTAMP(9);
@@ -818,11 +1005,14 @@ size_t unit_smem_bytes(int d, int tau) {
     (void)d;
     const size_t rows = (((size_t)tau + kTile - 1) / kTile + kUC - 1) / kUC * kTile;
     return (size_t)kUStages * kUTileBytes + sizeof(uint32_t) * kULocalCap + sizeof(int32_t) * (kULocalCap + 4) +
-           sizeof(int4) * (kUOwnCap + kUBandCap) + sizeof(int32_t) * (3 * (size_t)tau + 1 + rows);
+           sizeof(int4) * (kUOwnCap + kUBandCap) + sizeof(int32_t) * ((3 * (size_t)tau + 5) / 4 * 4) + sizeof(int2) * rows;
 }
 
-bool unit_supported(int d, int grp, int Smax, int tau) {
-    return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap && unit_smem_bytes(d, tau) <= 200 * 1024;
+int unit_page_tokens() { return kPage; }
+
+bool unit_supported(int d, int grp, int Smax, int tau, int slots) {
+    return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap && unit_smem_bytes(d, tau) <= 200 * 1024 &&
+           slots <= kMaxSlots;
 }
 
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
@@ -852,28 +1042,29 @@ static bool prefetch_enabled() {
     return on;
 }
 
-template <int D, int GRP>
+template <int D, int GRP, bool HOST>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     const size_t smem = unit_smem_bytes(D, a.sel.tau);
     static size_t configured = 0;
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(unit_step_kernel<D, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(unit_step_kernel<D, GRP, HOST>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(unit_step_kernel<D, GRP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(unit_step_kernel<D, GRP, HOST>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
-    return launch_pdl(unit_step_kernel<D, GRP>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st, a.q, a.input_token, a.bset,
-                      a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.cand,
-                      a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.out, a.out_ids, a.out_count, a.out_tokens,
-                      scale_log2);
+    return launch_pdl(unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st, a.q, a.input_token,
+                      a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
+                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.out, a.out_ids,
+                      a.out_count, a.out_tokens, scale_log2);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
-#define SKV_UN(DV, GV) return launch_unit_t<DV, GV>(a, st)
+    const bool host = a.hc.Kh != nullptr;
+#define SKV_UN(DV, GV) return host ? launch_unit_t<DV, GV, true>(a, st) : launch_unit_t<DV, GV, false>(a, st)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_UN(128, 1);

@@ -82,6 +82,11 @@ struct LayerState {
     int4* lk_cand = nullptr;           // [units][n_score_max][NL] local selection candidates
     int32_t* lk_cand_count = nullptr;  // [units][n_score_max]
     uint2* unit_hint = nullptr;        // [units] one-launch step kernel: band of the selection's crossing point
+    int32_t* pc_pt = nullptr;          // host residency, one-launch kernel: page table [units][pages]
+    int32_t* pc_own = nullptr;         // [units][slots]
+    int32_t* pc_hand = nullptr;        // [units]
+    int pc_pages = 0;
+    int last_path = 0;                 // host residency: 1 = one-launch kernel (page cache), 2 = split kernels
 };
 
 }  // namespace skv
@@ -239,6 +244,20 @@ cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, 
                                        int32_t* out_tokens, float* out, cudaStream_t st);
 
 // ---- one launch per layer and step (decode_unit.cu): D1-D4 in one cluster per (b, g) unit ----
+// Host residency (P3 + D3): the HBM working set of a unit is a page cache of `slots` pages of
+// unit_page_tokens() context rows; pt maps a context page to its slot (-1 = not resident), own
+// maps a slot to its page (-1 = empty), hand is the clock hand of the slot search.
+struct HostCache {
+    const __nv_bfloat16* Kh;       // mapped pinned host store [B][G][L][d] (nullptr: device residency)
+    const __nv_bfloat16* Vh;
+    __nv_bfloat16* wsK;            // [units][slots][page][d]
+    __nv_bfloat16* wsV;
+    int32_t* pt;                   // [units][pages]
+    int32_t* own;                  // [units][slots]
+    int32_t* hand;                 // [units]
+    int slots, pages, L;
+    unsigned long long* ledger;    // host bytes read (cumulative)
+};
 struct UnitArgs {
     const __nv_bfloat16* q;        // [B][Hq][d]
     const int32_t* input_token;    // [B]
@@ -254,6 +273,7 @@ struct UnitArgs {
     float* scores;                 // [B][G][Smax]
     SelBufs sel;
     KvSrc kv;                      // device residency: context K/V
+    HostCache hc;                  // host residency (hc.Kh == nullptr in device residency)
     int4* cand;                    // [unit_cand_entries] overflow scratch of the candidate lists
     uint2* hint;                   // [units] selection band of the previous step (klo, khi ordered keys)
     int prefetch;                  // L2 prefetch of the previous step's selection
@@ -263,7 +283,8 @@ struct UnitArgs {
     int32_t* out_tokens;           // optional [B][G]
 };
 bool unit_enabled();
-bool unit_supported(int d, int grp, int Smax, int tau);
+bool unit_supported(int d, int grp, int Smax, int tau, int slots);
+int unit_page_tokens();
 size_t unit_smem_bytes(int d, int tau);
 size_t unit_cand_entries(int units);
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st);

@@ -28,3 +28,19 @@ for v in "$@"; do
     split) run split SKV_UNIT=0 ;;
   esac
 done
+for v in "$@"; do
+  case $v in
+    host)
+      timeout 900 python bench.py --steps 300 --warmup 10 --no-cpu-baseline --e2e-steps 20 > gpurun_out/bench_host.txt 2>&1
+      python - <<'PY'
+import json
+f = "gpurun_out/bench_host.txt"
+try:
+    d = json.loads(open(f).read().strip().splitlines()[-1])
+    print("host ms/step", d["ms_per_step"], {k: (v["avg_us"], v["gbs"]) for k, v in d["kernels"].items()}, "e2e", d["e2e"]["ms_per_step"], "frac", d["roofline"]["frac"], d.get("host_residency"))
+except Exception as e:
+    print(f, "ERR", e, open(f).read()[-1500:])
+PY
+      ;;
+  esac
+done
