@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_util.cuh"
 #include "mma_attend.cuh"
@@ -101,7 +102,7 @@ struct Ctl {
     int bn;             // band path: entries of this CTA at or above the band's lower edge
     uint32_t whi, wband;  // band path: weight above the band / inside it (this CTA)
     int base[kUC + 1];  // exclusive prefix of the cluster's list sizes
-    int ok, nsel, nband, count, ntok, reset, cnt0, kc_set;
+    int ok, nsel, nband, count, ntok, reset, cnt0, kc_set, any_miss;
     uint32_t WHI, ks, kc;
     uint32_t lo, hi, cb, rem, ncand;
     unsigned long long thr;
@@ -252,6 +253,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         ctl.nsel = 0;
         ctl.nband = 0;
         ctl.ntok = 0;
+        ctl.any_miss = 0;
     }
     pdl_wait();
     SKV_TRACE_POINT(0);
@@ -740,12 +742,13 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int per = (ntl + kUC - 1) / kUC;
     const int tb = min(ntl, rank * per), te = min(ntl, tb + per);
     const int T0 = tb * kTile, T1 = min(ntok, te * kTile);
-    if constexpr (HOST) {
-        // Host residency (D3 host): the HBM working set is a page cache (pages of kPage
-        // context rows); a page-table entry holds the page's slot and the mask of its rows already
-        // in HBM.  Plan of this step, identical in every CTA (ascending page / clock order): pages
-        // of the selection that are not resident get a slot whose page the selection does not use
-        // (clock order from the hand); rows read from host are written through to their slot.
+    // Host residency (D3 host): the HBM working set is a page cache (pages of kPage context
+    // rows); a page-table entry holds the page's slot and the mask of its rows already in HBM.  A
+    // selected row is read from its slot if the row is there, else from the mapped host store.  When
+    // a CTA meets such a miss it plans the cache for the whole selection (identically in every CTA:
+    // ascending page / clock order): pages that are not resident get a slot whose page this selection
+    // does not use (clock order from the hand), and the rows read from host are written through.
+    auto cache_plan = [&]() {
         uint32_t* ownc = hist;  // slot -> page, copied (the histogram is idle now)
         static_assert(kUBins >= kMaxSlots, "slot table fits the histogram");
         if (warp == 0) {
@@ -839,7 +842,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (lane == 0) last_slot_s = n_asg > 0 ? frees[n_asg - 1] : -1;
         }
         __syncthreads();
-    }
+    };
+    int my_miss = 0;
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
         if (t < T1) {
@@ -851,25 +855,40 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             const int row = sel_src[lo2] + (t - sel_tok[lo2]);
             r.x = row;
             if constexpr (HOST) {
-                // row held in its slot -> working-set row; else host row -(row+1), written through
-                // to the slot of its page (if it has one this step)
-                const int p = row / kPage, w = row % kPage, n_need = n_need_s;
-                int lo = 0, hi = n_need;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (need[mid] < p) lo = mid + 1; else hi = mid;
-                }
-                r.x = -(row + 1);
-                if (lo < n_need && need[lo] == p) {
-                    const uint32_t e = pslot[lo];
-                    if (e != kEmpty && ((e >> (16 + w)) & 1u)) r.x = (int)(e & 0xffffu) * kPage + w;
-                    else if (slotof[lo] >= 0) r.y = slotof[lo] * kPage + w;
+                const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + row / kPage];
+                const int w = row % kPage;
+                if (e != kEmpty && ((e >> (16 + w)) & 1u)) {
+                    r.x = (int)(e & 0xffffu) * kPage + w;
+                } else {
+                    r.x = -(row + 1);
+                    my_miss = 1;
                 }
             }
         }
         rowtab[t - T0] = r;
     }
-    __syncthreads();
+    const bool any_miss = __syncthreads_or(my_miss) != 0;  // (always false in device residency)
+    if (HOST && any_miss) {
+        cache_plan();
+        // write-through targets of the rows read from host
+        const int n_need = n_need_s;
+        for (int t = T0 + tid; t < T1; t += kUT) {
+            int2 r = rowtab[t - T0];
+            if (r.x >= 0) continue;
+            const int row = -(r.x + 1), p = row / kPage;
+            int lo = 0, hi = n_need;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (need[mid] < p) lo = mid + 1; else hi = mid;
+            }
+            if (lo < n_need && need[lo] == p && slotof[lo] >= 0) {
+                r.y = slotof[lo] * kPage + row % kPage;
+                rowtab[t - T0] = r;
+            }
+        }
+        if (tid == 0) atomicOr(cluster.map_shared_rank(&ctl.any_miss, 0), 1);  // rank 0 updates the table
+        __syncthreads();
+    }
     SKV_USTAMP(6);
     {
         const int gq = lane >> 2, cq = lane & 3;
@@ -890,42 +909,51 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         mma::load_q<D, GRP>(qseg, q + ((size_t)b * Hq + g * GRP) * D, lane);
         mma::WarpAcc<D> wacc;
         wacc.init();
+        auto tiles = [&](auto miss_tag) {  // miss_tag: some rows of this CTA come from host
+            constexpr bool MISS = decltype(miss_tag)::value;
         for (int tile = tb + warp; tile < te; tile += kUW) {
-            const int t0 = tile * kTile;
-            const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
-            int2 rv[4];
-            const __nv_bfloat16* pv[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
-                pv[k] = rv[k].x != kInvalid ? rowV(rv[k].x) : nullptr;
-            }
-            mma::TileRegs<D> tr;
-            mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr, rk1.x != kInvalid ? rowK(rk1.x) : nullptr,
-                              pv, lane);
-            mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
-            if constexpr (HOST) {
-                // write-through of the rows read from host into their working-set slot
-                constexpr int NU = D / 32, NVP = D / 64;
-                __nv_bfloat16* Kw = hc.wsK + (size_t)unit * hc.slots * kPage * D;
-                __nv_bfloat16* Vw = hc.wsV + (size_t)unit * hc.slots * kPage * D;
-#pragma unroll
-                for (int u = 0; u < NU; ++u) {
-                    if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + cq * (D / 4) + 8 * u) = tr.kA[u];
-                    if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + cq * (D / 4) + 8 * u) = tr.kB[u];
+                const int t0 = tile * kTile;
+                const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+                int2 rv[4];
+                const __nv_bfloat16* pv[4];
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+                    pv[k] = rv[k].x != kInvalid ? (MISS ? rowV(rv[k].x) : Vd + (size_t)rv[k].x * D) : nullptr;
                 }
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-                    for (int pp = 0; pp < NVP; ++pp)
-                        if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
-                // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
-                if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
-                if (gq == 0)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
+                mma::TileRegs<D> tr;
+                if constexpr (MISS)
+                    mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr,
+                                      rk1.x != kInvalid ? rowK(rk1.x) : nullptr, pv, lane);
+                else
+                    mma::load_tile<D>(tr, rk0.x != kInvalid ? Kd + (size_t)rk0.x * D : nullptr,
+                                      rk1.x != kInvalid ? Kd + (size_t)rk1.x * D : nullptr, pv, lane);
+                mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
+                if constexpr (MISS) {
+                    // write-through of the rows read from host into their working-set slot
+                    constexpr int NU = D / 32, NVP = D / 64;
+                    __nv_bfloat16* Kw = hc.wsK + (size_t)unit * hc.slots * kPage * D;
+                    __nv_bfloat16* Vw = hc.wsV + (size_t)unit * hc.slots * kPage * D;
+    #pragma unroll
+                    for (int u = 0; u < NU; ++u) {
+                        if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + cq * (D / 4) + 8 * u) = tr.kA[u];
+                        if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + cq * (D / 4) + 8 * u) = tr.kB[u];
+                    }
+    #pragma unroll
+                    for (int k = 0; k < 4; ++k)
+    #pragma unroll
+                        for (int pp = 0; pp < NVP; ++pp)
+                            if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
+                    // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
+                    if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
+                    if (gq == 0)
+    #pragma unroll
+                        for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
+                }
             }
-        }
+        };
+        if (HOST && any_miss) tiles(std::true_type{});
+        else tiles(std::false_type{});
         SKV_USTAMP(7);
         if constexpr (HOST) {
             // transfer ledger: host rows read by this CTA
@@ -980,9 +1008,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     cluster.sync();  // #2: CTA partials ready
     SKV_USTAMP(8);
     mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT);
-    if (HOST && rank == 0) {
+    if (HOST && rank == 0 && ctl.any_miss) {
         // page-table update of this step's plan (every CTA has done its lookups: after barrier #2);
         // all selected rows of a page with a slot are in it now
+        if (!any_miss) cache_plan();  // the misses were in other CTAs: same plan, from the same table
         const int n_need = n_need_s;
         int32_t* pt = hc.pt + (size_t)unit * hc.pages;
         for (int j = tid; j < n_need; j += kUT) {
@@ -1035,9 +1064,11 @@ static int band_width() {
 }
 
 static bool prefetch_enabled() {
+    // L2 prefetch of the previous selection: opt-in (SKV_PREFETCH=1).  Measured on B200 (r01): the
+    // attention phase does not get faster and the issuing warp delays the first cluster barrier.
     static const bool on = [] {
         const char* e = getenv("SKV_PREFETCH");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }

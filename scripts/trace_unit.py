@@ -11,7 +11,9 @@ import paper_2504_00970_b200 as skvlib, synth
 B, M, Hq, G, d, L, tau = 4, 2, 32, 8, 128, 131072, 2048
 dev = torch.device("cuda:0")
 toks, topics = synth.prompts(0, B, L, 25.0)
-skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau)
+HOST = len(sys.argv) > 1 and sys.argv[1] == "host"
+skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
+                        residency=skvlib.SKV_KV_HOST if HOST else skvlib.SKV_KV_DEVICE)
 top = torch.from_numpy(topics).to(dev)
 KV = [synth.kv_layer_torch(0, l, top, G, d, device=dev) for l in range(M)]
 for l in range(M):
@@ -24,7 +26,7 @@ it = torch.full((B,), 300, dtype=torch.int32, device=dev)
 n = B * G * 8
 buf = (ctypes.c_ulonglong * (1024 * 16))()
 names = ["start", "scored", "csyncA", "bandpath", "general", "selected", "rowtab", "attended", "csync2", "end"]
-for step in range(6):
+for step in range(10):
     for l in range(M):
         q = synth.queries_torch(gen, KV[l][2], tgt, Hq, G, d).contiguous()
         skv.decode_step(l, q, it, out)
