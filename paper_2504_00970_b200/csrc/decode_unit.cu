@@ -46,7 +46,7 @@ namespace skv {
 SKV_TRACE_DEFINE(unit)
 #ifdef SKV_TRACE
 // per CTA (unit * kUC + rank < 1024): SM id + globaltimer (ns) at the phase boundaries
-__device__ unsigned long long g_unit_t[1024][16];
+__device__ unsigned long long g_unit_t[1024][24];
 extern "C" __attribute__((visibility("default"))) int sentencekv_debug_unit(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_unit_t, sizeof(g_unit_t));
 }
@@ -58,7 +58,7 @@ __device__ __forceinline__ void unit_stamp(int cta, int ph) {
         if (ph == 0) {
             unsigned int sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-            g_unit_t[cta][15] = sm;
+            g_unit_t[cta][23] = sm;
         }
     }
 }
@@ -437,6 +437,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
     }
     __syncthreads();
+    SKV_USTAMP(16);
     bool ok = ctl.ok != 0;
     if (ok) {
         // gather: above-band entries are selected outright (sl), band entries are ranked
@@ -455,6 +456,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
         }
         __syncthreads();
+        SKV_USTAMP(17);
         if (ctl.nsel <= kUBandSel) {
             const int nbd = ctl.nband;
             const uint32_t WHI = ctl.WHI;
@@ -476,6 +478,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
         }
         __syncthreads();
+        SKV_USTAMP(18);
         const int ns = ctl.nsel;
         ok = ns <= kUBandSel;
 #ifdef SKV_TRACE
@@ -1004,7 +1007,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
     }
-    pdl_trigger();
     cluster.sync();  // #2: CTA partials ready
     SKV_USTAMP(8);
     mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT);
@@ -1026,6 +1028,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
     }
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
+    pdl_trigger();
     if (rank == 0 && tid == 0) sel.parity[unit] = cur;
     SKV_USTAMP(9);
 }

@@ -24,7 +24,7 @@ tgt = torch.zeros(B, dtype=torch.int32, device=dev)
 out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
 it = torch.full((B,), 300, dtype=torch.int32, device=dev)
 n = B * G * 8
-buf = (ctypes.c_ulonglong * (1024 * 16))()
+buf = (ctypes.c_ulonglong * (1024 * 24))()
 names = ["start", "scored", "csyncA", "bandpath", "general", "selected", "rowtab", "attended", "csync2", "end"]
 for step in range(10):
     for l in range(M):
@@ -32,8 +32,8 @@ for step in range(10):
         skv.decode_step(l, q, it, out)
     torch.cuda.synchronize()
     skvlib.lib.sentencekv_debug_unit(buf)
-    T = np.array(buf, dtype=np.float64).reshape(1024, 16)[:n]
-    sm = T[:, 15].astype(int)
+    T = np.array(buf, dtype=np.float64).reshape(1024, 24)[:n]
+    sm = T[:, 23].astype(int)
     gen_path = T[:, 4] > T[:, 3]  # the general path stamps phase 4 after the band attempt
     T[~gen_path, 4] = T[~gen_path, 3]
     t = (T[:, :10] - T[:, 0].min()) / 1e3
@@ -44,5 +44,8 @@ for step in range(10):
     reason = T[::8, 10].astype(int)
     print(f"   band path per unit: reasons {np.bincount(reason, minlength=16)[:16].tolist()} (1 ovf, 2 above>tau, 4 below band, 8 nsel>cap); "
           f"band entries median {np.median(T[::8, 11]):.0f} max {T[::8, 11].max():.0f}; selected median {np.median(T[::8, 12]):.0f}; listed median {np.median(T[::8, 13]):.0f} max {T[::8,13].max():.0f}")
+    sub = (T[:, [2, 16, 17, 18, 3]] - T[:, 0].min()) / 1e3
+    ds = np.diff(sub, axis=1)
+    print("   band sub-phases (median/max): " + ", ".join(f"{nm}={np.median(ds[:, i]):.2f}/{ds[:, i].max():.2f}" for i, nm in enumerate(["decide", "gather", "rank", "compact"])))
     d_ = np.diff(t, axis=1)
     print("   durations (median/max): " + ", ".join(f"{names[i+1]}={np.median(d_[:, i]):.2f}/{d_[:, i].max():.2f}" for i in range(9)))
