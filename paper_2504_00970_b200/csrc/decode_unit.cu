@@ -86,8 +86,7 @@ constexpr int kUBins = 1024;
 constexpr int kUExact = kUT;             // crossing-bin candidates ranked exactly per refinement level
 constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
 constexpr int kUBandCap = 256;           // band-path list entries per CTA
-constexpr int kUBandSel = 256;           // band path: selected sentences ranked by counting (else general path)
-static_assert(kUBandSel + kUC * kUBandCap <= kUGather, "band lists fit the ring");
+static_assert(kUC * kUBandCap * (16 + 4 + 4) <= kUStages * kUTileBytes, "band lists fit the ring");
 using mma::kInvalid;
 using mma::kTile;
 
@@ -359,12 +358,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                     sc_out[s0 + i] = p;
                     mn = min(mn, k);
                     mx = max(mx, k);
-                    if (k >= klo) {  // band list: everything at or above the band's lower edge
-                        const uint32_t len = (uint32_t)(offs[i + 1] - offs[i]);
-                        const int pos = atomicAdd(&ctl.bn, 1);
-                        if (pos < kUBandCap) blist[pos] = make_int4((int)k, s0 + i, offs[i], (int)len);
-                        atomicAdd(k > khi ? &ctl.whi : &ctl.wband, len);
-                    }
                 }
             }
             __syncthreads();  // stage st fully read
@@ -395,6 +388,33 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 prefetch_l2_hint(kv.V + (ub + src) * D, (uint32_t)(len * D * 2), pol);
             }
         }
+    }
+    __syncthreads();
+    // band list (ascending sentence order): everything at or above the band's lower edge, with the
+    // weights above the band and inside it
+    const int per_t = (n + kUT - 1) / kUT;
+    const int i0 = min(n, tid * per_t), i1 = min(n, i0 + per_t);
+    {
+        uint32_t mine = 0, whi = 0, wband = 0;
+        for (int i = i0; i < i1; ++i) {
+            const uint32_t k = keys[i];
+            if (k >= klo) {
+                ++mine;
+                const uint32_t len = (uint32_t)(offs[i + 1] - offs[i]);
+                if (k > khi) whi += len; else wband += len;
+            }
+        }
+        uint32_t total;
+        uint32_t pos = block_incl_sum<uint32_t>(mine, ws32, &total) - mine;
+        for (int i = i0; i < i1 && pos < (uint32_t)kUBandCap; ++i)
+            if (keys[i] >= klo) blist[pos++] = make_int4((int)keys[i], s0 + i, offs[i], offs[i + 1] - offs[i]);
+        whi = __reduce_add_sync(0xffffffffu, whi);
+        wband = __reduce_add_sync(0xffffffffu, wband);
+        if (lane == 0) {
+            atomicAdd(&ctl.whi, whi);
+            atomicAdd(&ctl.wband, wband);
+        }
+        if (tid == 0) ctl.bn = (int)total;
     }
     __syncthreads();
     SKV_USTAMP(1);
@@ -440,37 +460,37 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     SKV_USTAMP(16);
     bool ok = ctl.ok != 0;
     if (ok) {
-        // gather: above-band entries are selected outright (sl), band entries are ranked
-        int4* sl = gath;                    // [kUBandSel] selected (unordered)
-        int4* bd = gath + kUBandSel;        // band entries
+        // gather the lists in rank order (so in ascending sentence order); band entries are ranked
         const int ntot = ctl.base[kUC];
+        int* bidx = reinterpret_cast<int*>(gath + kUC * kUBandCap);  // [ntot] indices of band entries
+        int* flag = bidx + kUC * kUBandCap;                          // [ntot] selected
         for (int i = tid; i < ntot; i += kUT) {
             int j = 0;
             while (i >= ctl.base[j + 1]) ++j;
             const int4 e = lists[j][i - ctl.base[j]];
-            if ((uint32_t)e.x > khi) {
-                const int p = atomicAdd(&ctl.nsel, 1);
-                if (p < kUBandSel) sl[p] = e;
-            } else {
-                bd[atomicAdd(&ctl.nband, 1)] = e;
-            }
+            gath[i] = e;
+            const bool above = (uint32_t)e.x > khi;
+            flag[i] = above ? 1 : 0;
+            if (!above) bidx[atomicAdd(&ctl.nband, 1)] = i;
         }
         __syncthreads();
         SKV_USTAMP(17);
-        if (ctl.nsel <= kUBandSel) {
+        {
+            // a band entry is selected iff (weight above the band) + (weight of band entries ranked
+            // above it) + its length fits tau; the one that first does not fit is the crossing point
             const int nbd = ctl.nband;
             const uint32_t WHI = ctl.WHI;
-            for (int i = tid; i < nbd; i += kUT) {
-                const int4 e = bd[i];
+            for (int x = tid; x < nbd; x += kUT) {
+                const int i = bidx[x];
+                const int4 e = gath[i];
                 const unsigned long long ke = ukey64((uint32_t)e.x, e.y);
                 uint32_t w = WHI;
                 for (int c = 0; c < nbd; ++c) {
-                    const int4 f = bd[c];
+                    const int4 f = gath[bidx[c]];
                     if (ukey64((uint32_t)f.x, f.y) > ke) w += (uint32_t)f.w;
                 }
                 if (w + (uint32_t)e.w <= (uint32_t)tau) {
-                    const int p = atomicAdd(&ctl.nsel, 1);
-                    if (p < kUBandSel) sl[p] = e;
+                    flag[i] = 1;
                 } else if (w <= (uint32_t)tau) {
                     ctl.kc = (uint32_t)e.x;  // the crossing sentence (unique)
                     ctl.kc_set = 1;
@@ -479,40 +499,45 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         __syncthreads();
         SKV_USTAMP(18);
-        const int ns = ctl.nsel;
-        ok = ns <= kUBandSel;
-#ifdef SKV_TRACE
-        if (tid == 0 && unit * kUC + rank < 1024) {
-            g_unit_t[unit * kUC + rank][10] |= ok ? 0 : 8;
-            g_unit_t[unit * kUC + rank][11] = ctl.nband;
-            g_unit_t[unit * kUC + rank][12] = ns;
-        }
-#endif
-        if (ok) {
-            // ascending sentence order by counting (ns is small)
-            for (int i = tid; i < ns; i += kUT) {
-                const int4 e = sl[i];
-                int pos = 0, toff = 0;
-                for (int c = 0; c < ns; ++c) {
-                    const int4 f = sl[c];
-                    if (f.y < e.y) {
-                        ++pos;
-                        toff += f.w;
-                    }
-                }
+        // ordered compaction: ascending ids and gathered token offsets
+        const int pc_ = (ntot + kUT - 1) / kUT;
+        const int c0 = min(ntot, tid * pc_), c1 = min(ntot, c0 + pc_);
+        unsigned long long mine = 0;
+        uint32_t kmin = 0xffffffffu;
+        for (int i = c0; i < c1; ++i)
+            if (flag[i]) {
+                const int4 e = gath[i];
+                mine += (1ull << 32) | (uint32_t)e.w;
+                kmin = min(kmin, (uint32_t)e.x);
+            }
+        unsigned long long tot;
+        const unsigned long long excl = block_incl_sum<unsigned long long>(mine, ws64, &tot) - mine;
+        int pos = (int)(excl >> 32);
+        int32_t toff = (int32_t)(excl & 0xffffffffull);
+        for (int i = c0; i < c1; ++i)
+            if (flag[i]) {
+                const int4 e = gath[i];
                 sel_tok[pos] = toff;
                 sel_src[pos] = e.z;
                 sel_id[pos] = e.y;
-                atomicAdd(&ctl.ntok, e.w);
-                atomicMin(&ctl.ks, (uint32_t)e.x);
+                ++pos;
+                toff += e.w;
             }
-            __syncthreads();
-            if (tid == 0) {
-                ctl.count = ns;
-                sel_tok[ns] = ctl.ntok;
-            }
-            __syncthreads();
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        if (lane == 0 && kmin != 0xffffffffu) atomicMin(&ctl.ks, kmin);
+        if (tid == 0) {
+            const int count = (int)(tot >> 32);
+            ctl.count = count;
+            ctl.ntok = (int)(tot & 0xffffffffull);
+            sel_tok[count] = ctl.ntok;
         }
+        __syncthreads();
+#ifdef SKV_TRACE
+        if (tid == 0 && unit * kUC + rank < 1024) {
+            g_unit_t[unit * kUC + rank][11] = ctl.nband;
+            g_unit_t[unit * kUC + rank][12] = ctl.count;
+        }
+#endif
     }
     SKV_USTAMP(3);
     if (!ok) {
@@ -520,8 +545,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         // 2a. local candidates
         for (int i = tid; i < kUBins; i += kUT) hist[i] = 0u;
         __syncthreads();
-        const int per_t = (n + kUT - 1) / kUT;
-        const int i0 = min(n, tid * per_t), i1 = min(n, i0 + per_t);
         {
             const Binner bin(ctl.lo, ctl.hi);
             for (int i = i0; i < i1; ++i) atomicAdd(&hist[bin(keys[i])], (uint32_t)(offs[i + 1] - offs[i]));
