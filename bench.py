@@ -361,8 +361,11 @@ def main():
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
+        # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from one
+        # `ncu --set full` capture of this workload (scripts/gpu_profile.sh), per residency
         with open(tf) as f:
-            traffic = json.load(f).get(dom)
+            tj = json.load(f)
+        traffic = tj.get(f"{dom}_{residency}", tj.get(dom))
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                 "per_unit": "step (one launch per layer): G*S*d*2 B (bf16 E) + sum(ntok)*d*2*2 B (selected K,V rows) "

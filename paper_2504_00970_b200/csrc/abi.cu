@@ -177,6 +177,14 @@ bool skv::pdl_enabled() {
     return on;
 }
 
+bool skv::pdl_step_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SKV_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 SKV_API void sentencekv_config_default(skv_config* cfg) {
     if (!cfg) return;
     std::memset(cfg, 0, sizeof(*cfg));

@@ -1113,7 +1113,8 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
         configured = smem;
     }
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
-    return launch_pdl(unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st, a.q, a.input_token,
+    return launch_pdl_if(pdl_step_enabled(), unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
+                      a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.out, a.out_ids,
                       a.out_count, a.out_tokens, scale_log2);

@@ -125,9 +125,27 @@ struct skv_ctx {
 
 namespace skv {
 
-// Launches `kernel` on `st` with programmatic stream serialization (PDL) when enabled by the
-// environment (opt-in: SKV_PDL=1).  Kernels launched this way call pdl_wait() before reading inputs.
+// Launches `kernel` on `st` with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel of the stream drains; it calls pdl_wait() before reading any input.
+// pdl_enabled(): the score / select / attend kernels (opt-in, SKV_PDL=1); pdl_step_enabled(): the
+// one-launch step kernel (default on, SKV_PDL=0 turns it off).
 bool pdl_enabled();
+bool pdl_step_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
