@@ -254,9 +254,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         ctl.ntok = 0;
         ctl.any_miss = 0;
     }
-    pdl_wait();
-    SKV_TRACE_POINT(0);
-    SKV_USTAMP(0);
+    // The prompt's sentence counts and embeddings are written only by the prefill, never by the
+    // decode kernel this one may overlap (programmatic launch), so the first E tiles are requested
+    // before waiting for it; everything the previous step wrote is read after pdl_wait().
     const int Sb = S[b];
     const int chunk = (Sb + kUC - 1) / kUC;
     const int s0 = min(Sb, rank * chunk), s1 = min(Sb, s0 + chunk);
@@ -264,9 +264,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int ntiles = (n + TS - 1) / TS;
     const __nv_bfloat16* Eu = E + ((size_t)unit * Smax) * D;
     const int32_t* o = off + (size_t)b * off_stride;
-    const int prev = sel.parity[unit], cur = prev ^ 1;
-    const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
-    const uint32_t klo = band.x, khi = band.y;
 
     // ---------------------------------------------------------------- 1. score (D1)
     if (tid == 0) {
@@ -277,6 +274,12 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             bulk_g2s_hint(ring + (size_t)i * TS * D, Eu + (size_t)ts * D, (uint32_t)(m * D * 2), &bar[i], pol);
         }
     }
+    pdl_wait();
+    SKV_TRACE_POINT(0);
+    SKV_USTAMP(0);
+    const int prev = sel.parity[unit], cur = prev ^ 1;
+    const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
+    const uint32_t klo = band.x, khi = band.y;
     // previous step's selected runs of this CTA's share (the L2 prefetch is issued after scoring,
     // when HBM would otherwise idle during the selection)
     constexpr int kPf = 4;
@@ -1028,6 +1031,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 hint[unit] = h;
             }
         }
+        // the next kernel of the stream may start launching (it reads this step's state only after
+        // its pdl_wait, i.e. after this grid has completed)
+        pdl_trigger();
         mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
     }
     cluster.sync();  // #2: CTA partials ready
@@ -1051,7 +1057,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
     }
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
-    pdl_trigger();
     if (rank == 0 && tid == 0) sel.parity[unit] = cur;
     SKV_USTAMP(9);
 }

@@ -22,6 +22,7 @@ for v in "$@"; do
     unit) run unit ;;
     nopf) run unit_nopf SKV_PREFETCH=0 ;;
     pdl) run unit_pdl SKV_PDL=1 ;;
+    nopdl) run unit_nopdl SKV_PDL=0 ;;
     band0) run unit_band0 SKV_BAND_LOG2=0 ;;
     band21) run unit_band21 SKV_BAND_LOG2=21 ;;
     band17) run unit_band17 SKV_BAND_LOG2=17 ;;
