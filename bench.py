@@ -338,13 +338,13 @@ def main():
     skv.set_profiling(False)
     S_tot = sum(S)
     # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md "Measurement"
-    score_bytes = Gl * S_tot * d * 2 + Bl * Hl * d * (2 + 4) + Bl * Gl * S_tot * 4  # E + q,Sq + scores written
+    score_bytes = Gl * S_tot * d * 2 + Bl * Hl * d * (2 + 4) + Gl * S_tot * 4  # E + q,Sq + scores written
     nlaunch = max(1, prof["step"][1] or prof["fused"][1] or prof["attend"][1])
     kv_bytes = ntok_sum * d * 2 * 2 / nlaunch  # selected K and V rows
-    sel_bytes = Bl * Gl * S_tot * (4 + 4) + Bl * Hl * d * (2 + 4 * 2)  # scores + offsets read, q + Sq
+    sel_bytes = Gl * S_tot * (4 + 4) + Bl * Hl * d * (2 + 4 * 2)  # scores + offsets read, q + Sq
     kern = {}
     # one-launch step (decode_unit.cu): E + q/Sq + scores written, offsets read, selected K/V, Sq update, O
-    unit_bytes = score_bytes + Bl * Gl * S_tot * 4 + kv_bytes + Bl * Hl * d * (4 + 4)
+    unit_bytes = score_bytes + Gl * S_tot * 4 + kv_bytes + Bl * Hl * d * (4 + 4)
     for name, nbytes in (("step", unit_bytes), ("score", score_bytes), ("fused", kv_bytes + sel_bytes + Bl * Hl * d * 4),
                          ("select", sel_bytes), ("attend", kv_bytes + Bl * Hl * d * (2 + 4))):
         ms, n = prof[name]

@@ -203,13 +203,15 @@ __device__ __forceinline__ void merge_warps(MergeSmem<D, NW>& sm, const WarpAcc<
         for (int x = 0; x < NW; ++x) M = fmaxf(M, sm.mw[x][h]);
         wsc[e] = (w.m[e] == -INFINITY) ? 0.0f : exp2f(w.m[e] - M);
     }
+    if (2 * cq < GRP) {  // lanes holding real heads only
 #pragma unroll
-    for (int i = 0; i < NKS; ++i) {
+        for (int i = 0; i < NKS; ++i) {
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int dim = (D == 128) ? (half ? 64 + 8 * gq + i : 8 * gq + i) : (8 * gq + 2 * i + half);
-            sm.red[warp][2 * cq][dim] = w.acc[i][2 * half] * wsc[0];
-            sm.red[warp][2 * cq + 1][dim] = w.acc[i][2 * half + 1] * wsc[1];
+            for (int half = 0; half < 2; ++half) {
+                const int dim = (D == 128) ? (half ? 64 + 8 * gq + i : 8 * gq + i) : (8 * gq + 2 * i + half);
+                sm.red[warp][2 * cq][dim] = w.acc[i][2 * half] * wsc[0];
+                if (2 * cq + 1 < GRP) sm.red[warp][2 * cq + 1][dim] = w.acc[i][2 * half + 1] * wsc[1];
+            }
         }
     }
     __syncthreads();
