@@ -189,8 +189,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
                  float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, float scale_log2) {
-    constexpr int LPS = D / 8;                  // lanes per sentence (scoring)
-    constexpr int GPW = 32 / LPS;               // sentences per warp step
+    constexpr int TPS = 4;                      // threads per sentence (scoring)
+    constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
+    constexpr int GPW = 32 / TPS;               // sentences per warp step
     constexpr int TS = kUTileBytes / (D * 2);   // sentences per E tile
     static_assert(TS % (kUW * GPW) == 0, "tile must split evenly over the warps");
     static_assert(GRP <= 8, "heads fill the N = 8 side of the MMA");
@@ -333,10 +334,17 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     }
     __syncthreads();
     {
-        const int l = lane % LPS, gw = lane / LPS;
-        float qr[8];
+        // Canonical dot (A23): d/8 partials p_l = q[8l..8l+7] . e[8l..8l+7] (mul, then 7 fma), then
+        // the tree of the xor butterfly with offsets d/16, ..., 1.  Here a sentence has TPS = 4
+        // threads; thread j holds the partials l = j, j+4, (j+8, j+12): the first tree levels are
+        // local adds in the same pairing, the last two are shuffles (offsets 2 and 1) -- the same
+        // additions in the same order, so the score is bit-identical to the 16-lane form.
+        const int j = lane % TPS, gw = lane / TPS;
+        float qr[NPT][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) qr[i] = qt[8 * l + i];
+        for (int c = 0; c < NPT; ++c)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) qr[c][i] = qt[8 * (j + TPS * c) + i];
         float* sc_out = scores + (size_t)unit * Smax;
         uint32_t mn = 0xffffffffu, mx = 0u;
         for (int it = 0; it < ntiles; ++it) {
@@ -345,16 +353,27 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             const __nv_bfloat16* tile = ring + (size_t)st * TS * D;
             const int ts = it * TS, m = min(TS, n - ts);  // local index of the tile's first sentence
 #pragma unroll
-            for (int j = 0; j < TS / (kUW * GPW); ++j) {
-                const int r = (j * kUW + warp) * GPW + gw;
-                float f[8];
-                unpack8(*reinterpret_cast<const uint4*>(tile + (size_t)r * D + 8 * l), f);
-                float p = __fmul_rn(qr[0], f[0]);
+            for (int jj = 0; jj < TS / (kUW * GPW); ++jj) {
+                const int r = (jj * kUW + warp) * GPW + gw;
+                float pp[NPT];
 #pragma unroll
-                for (int i = 1; i < 8; ++i) p = __fmaf_rn(qr[i], f[i], p);
+                for (int c = 0; c < NPT; ++c) {
+                    float f[8];
+                    unpack8(*reinterpret_cast<const uint4*>(tile + (size_t)r * D + 8 * (j + TPS * c)), f);
+                    float p = __fmul_rn(qr[c][0], f[0]);
 #pragma unroll
-                for (int x = LPS / 2; x >= 1; x >>= 1) p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, x));
-                if (l == 0 && r < m) {
+                    for (int i = 1; i < 8; ++i) p = __fmaf_rn(qr[c][i], f[i], p);
+                    pp[c] = p;
+                }
+                float p;
+                if constexpr (NPT == 4) {  // d = 128: levels 8 and 4 are local
+                    p = __fadd_rn(__fadd_rn(pp[0], pp[2]), __fadd_rn(pp[1], pp[3]));
+                } else {                   // d = 64: level 4 is local
+                    p = __fadd_rn(pp[0], pp[1]);
+                }
+                p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, 2));
+                p = __fadd_rn(p, __shfl_xor_sync(0xffffffffu, p, 1));
+                if (j == 0 && r < m) {
                     const int i = ts + r;
                     const uint32_t k = ordered_key(p);
                     keys[i] = k;
