@@ -180,6 +180,25 @@ def test_unit_step_kernel_off_parity_subprocess(cuda_device):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("band_log2", ["0", "30"])
+def test_step_kernel_selection_paths_subprocess(cuda_device, band_log2):
+    """The one-launch step kernel ranks either the band around the previous crossing point or, when
+    the crossing left the band, the union of the local candidate lists.  A zero-width band
+    (SKV_BAND_LOG2=0) sends most steps down the general path, a very wide one (30) overflows the band
+    lists: both must give the oracle's selections and outputs."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_BAND_LOG2=band_log2)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
+                        "tests/test_gpu_fullsize.py",
+                        "-k", "(step or ties or all_equal or one_token or config2) and not subprocess"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_deterministic_run_to_run(cuda_device):
     B, M, Hq, G, d, L, tau, steps = 2, 1, 8, 2, 128, 6000, 512, 5
     toks, _, Ks, Vs, qs, script = make_case(8, B, M, Hq, G, d, L, tau, steps, median=25.0)
