@@ -23,6 +23,11 @@ for v in "$@"; do
     nopf) run unit_nopf SKV_PREFETCH=0 ;;
     pdl) run unit_pdl SKV_PDL=1 ;;
     nopdl) run unit_nopdl SKV_PDL=0 ;;
+    pull) run unit_pull SKV_PUSH_MERGE=0 ;;
+    unit2) run unit2 ;;
+    pull2) run unit_pull2 SKV_PUSH_MERGE=0 ;;
+    prev) run prev SKV_LIB=paper_2504_00970_b200/libsentencekv_prev.so ;;
+    prev2) run prev2 SKV_LIB=paper_2504_00970_b200/libsentencekv_prev.so ;;
     band0) run unit_band0 SKV_BAND_LOG2=0 ;;
     band21) run unit_band21 SKV_BAND_LOG2=21 ;;
     band17) run unit_band17 SKV_BAND_LOG2=17 ;;

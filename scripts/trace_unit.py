@@ -4,7 +4,7 @@ globaltimer at each phase boundary, for the 8b-128k shapes (device residency), 2
 import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SKV_LIB"] = os.path.join(ROOT, "paper_2504_00970_b200", "libsentencekv_trace.so")
+os.environ["SKV_LIB"] = os.environ.get("SKV_TRACE_LIB") or os.path.join(ROOT, "paper_2504_00970_b200", "libsentencekv_trace.so")
 import numpy as np, torch
 import paper_2504_00970_b200 as skvlib, synth
 
