@@ -444,7 +444,9 @@ def main():
             "step_bytes_per_gpu": int(step_bytes),
             "step_gbs_per_gpu": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
             "e2e": e2e,
-            "gpu_launches": (3 * M if prof["select"][1] else 2 * M) * args.steps,
+            # kernels of this library per timed step: one unit_step_kernel per layer (decode_unit.cu),
+            # else score + select + attend (or score + fused)
+            "gpu_launches": (M if prof["step"][1] else (3 * M if prof["select"][1] else 2 * M)) * args.steps,
             "clocks": clk.summary(),
             "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(Bl * Gl * L * d * 2 * M),
                         "segment_ms": round(prof_prefill["segment"][0], 3),

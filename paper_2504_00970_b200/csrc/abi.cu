@@ -558,6 +558,16 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.cand = c->unit_cand;
         a.hint = ls.unit_hint;
         a.prefetch = 1;
+        {
+            // the next layer's embeddings go to L2 while this layer selects and merges (a hint; a real
+            // decoder calls the layers in order).  SKV_PF_NEXT=0 turns it off.
+            static const bool pf_next = [] {
+                const char* e = getenv("SKV_PF_NEXT");
+                return !(e && e[0] == '0');
+            }();
+            const int nl = layer + 1 < c->cfg.layers ? layer + 1 : 0;
+            a.E_next = (pf_next && nl != layer && c->layer[nl].prefilled) ? c->layer[nl].E : nullptr;
+        }
         a.out = out;
         a.out_ids = sel_ids;
         a.out_count = sel_count;

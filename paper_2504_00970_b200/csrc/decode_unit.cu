@@ -187,7 +187,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
                  int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
-                 float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
+                 const __nv_bfloat16* __restrict__ E_next, float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, float scale_log2) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
@@ -396,6 +396,17 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             atomicMin(&ctl.lo, mn);
             atomicMax(&ctl.hi, mx);
         }
+    }
+    if (E_next != nullptr && warp == 0 && n > 0) {
+        // L2 prefetch of the NEXT layer's embeddings of this CTA's sentence range (prefill data, so
+        // independent of this step): HBM would otherwise idle during the selection and the merge, and
+        // the next layer's scoring then streams E from L2.  16 KB pieces, one per lane.
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(E_next + ((size_t)unit * Smax + s0) * D);
+        const uint32_t bytes = (uint32_t)n * D * 2;
+        for (uint32_t o2 = (uint32_t)lane * kUTileBytes; o2 < bytes; o2 += 32u * kUTileBytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + o2),
+                         "r"(min((uint32_t)kUTileBytes, bytes - o2))
+                         : "memory");
     }
     if (!HOST && prefetch && warp == kUW - 1) {
         // L2 prefetch of the previous step's selection (a hint: the attention reads whatever is
@@ -631,6 +642,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             ctl.hi = 0u;
         }
         __syncthreads();
+        SKV_USTAMP(19);
         const int per_c = (ntot + kUT - 1) / kUT;
         const int c0 = min(ntot, tid * per_c), c1 = min(ntot, c0 + per_c);
         {
@@ -648,6 +660,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
         }
         __syncthreads();
+        SKV_USTAMP(20);
 
         // 2c. exact selection over the union of the lists
         uint32_t lo = ctl.lo, hi = ctl.hi, rem = (uint32_t)tau;
@@ -745,6 +758,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             __syncthreads();
         }
 
+        SKV_USTAMP(21);
         // 2d. ordered compaction (ascending ids + gathered token offsets)
         unsigned long long mine = 0;
         uint32_t kmin = 0xffffffffu;
@@ -1140,7 +1154,7 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     return launch_pdl_if(pdl_step_enabled(), unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
-                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.out, a.out_ids,
+                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.E_next, a.out, a.out_ids,
                       a.out_count, a.out_tokens, scale_log2);
 }
 

@@ -295,6 +295,7 @@ struct UnitArgs {
     int4* cand;                    // [unit_cand_entries] overflow scratch of the candidate lists
     uint2* hint;                   // [units] selection band of the previous step (klo, khi ordered keys)
     int prefetch;                  // L2 prefetch of the previous step's selection
+    const __nv_bfloat16* E_next;   // nullable: the next layer's E, prefetched into L2 while HBM idles
     float* out;                    // [B][Hq][d]
     int32_t* out_ids;              // optional [B][G][tau]
     int32_t* out_count;            // optional [B][G]

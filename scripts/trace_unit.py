@@ -47,5 +47,9 @@ for step in range(10):
     sub = (T[:, [2, 16, 17, 18, 3]] - T[:, 0].min()) / 1e3
     ds = np.diff(sub, axis=1)
     print("   band sub-phases (median/max): " + ", ".join(f"{nm}={np.median(ds[:, i]):.2f}/{ds[:, i].max():.2f}" for i, nm in enumerate(["decide", "gather", "rank", "compact"])))
+    if gen_path.any():
+        gs = (T[gen_path][:, [4, 19, 20, 21, 5]] - T[:, 0].min()) / 1e3
+        dg = np.diff(gs, axis=1)
+        print("   general sub-phases (median/max): " + ", ".join(f"{nm}={np.median(dg[:, i]):.2f}/{dg[:, i].max():.2f}" for i, nm in enumerate(["gather", "minmax", "levels", "compact"])))
     d_ = np.diff(t, axis=1)
     print("   durations (median/max): " + ", ".join(f"{names[i+1]}={np.median(d_[:, i]):.2f}/{d_[:, i].max():.2f}" for i in range(9)))
