@@ -559,11 +559,12 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.hint = ls.unit_hint;
         a.prefetch = 1;
         {
-            // the next layer's embeddings go to L2 while this layer selects and merges (a hint; a real
-            // decoder calls the layers in order).  SKV_PF_NEXT=0 turns it off.
+            // opt-in (SKV_PF_NEXT=1): the next layer's embeddings go to L2 while this layer selects
+            // and merges (a real decoder calls the layers in order).  Measured on B200 (r01): no gain
+            // (0.850 vs 0.854 ms/step) -- the scoring stream does not get faster from L2.
             static const bool pf_next = [] {
                 const char* e = getenv("SKV_PF_NEXT");
-                return !(e && e[0] == '0');
+                return e && e[0] == '1';
             }();
             const int nl = layer + 1 < c->cfg.layers ? layer + 1 : 0;
             a.E_next = (pf_next && nl != layer && c->layer[nl].prefilled) ? c->layer[nl].E : nullptr;

@@ -29,7 +29,10 @@
 //   3. gather + attend (D3 + D4; Alg. 1 l.18-19): CTA r takes its 1/kUC of the 16-token
 //      tiles of the gathered tokens; rows are read straight from the context K/V (one contiguous
 //      run per sentence) into mma.sync fragments (mma_attend.cuh); warps merge through shared
-//      memory, the kUC CTA partials through DSMEM (second cluster barrier).
+//      memory, the kUC CTA partials through DSMEM (second cluster barrier).  (Storing the partials
+//      to global memory for the unit's last CTA to combine, with a split cluster barrier so that
+//      CTAs exit early, was measured slower on B200: with programmatic launch the next layer's
+//      clusters then fill the freed SMs unevenly and part of the grid runs as a second wave.)
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -50,6 +53,26 @@ __device__ unsigned long long g_unit_t[1024][24];
 extern "C" __attribute__((visibility("default"))) int sentencekv_debug_unit(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_unit_t, sizeof(g_unit_t));
 }
+// per launch (ring of 64): [0] first CTA entry, [1] first return from the programmatic-launch wait,
+// [2] last CTA exit (globaltimer ns)
+__device__ unsigned long long g_launch_t[64][4];
+extern "C" __attribute__((visibility("default"))) int sentencekv_debug_launches(unsigned long long* out, int reset) {
+    if (reset) {
+        static unsigned long long init[64][4];
+        for (auto& r : init) r[0] = r[1] = ~0ull, r[2] = r[3] = 0ull;
+        return (int)cudaMemcpyToSymbol(g_launch_t, init, sizeof(init));
+    }
+    return (int)cudaMemcpyFromSymbol(out, g_launch_t, sizeof(g_launch_t));
+}
+__device__ __forceinline__ void launch_stamp(int idx, int which) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (which == 2) atomicMax(&g_launch_t[idx & 63][2], t);
+        else atomicMin(&g_launch_t[idx & 63][which], t);
+    }
+}
+#define SKV_LSTAMP(w) launch_stamp(trace_idx, (w))
 __device__ __forceinline__ void unit_stamp(int cta, int ph) {
     if (threadIdx.x == 0 && cta < 1024) {
         unsigned long long t;
@@ -66,6 +89,9 @@ __device__ __forceinline__ void unit_stamp(int cta, int ph) {
 #else
 #define SKV_USTAMP(ph) \
     do {               \
+    } while (0)
+#define SKV_LSTAMP(w) \
+    do {              \
     } while (0)
 #endif
 
@@ -102,7 +128,8 @@ struct Ctl {
     uint32_t whi, wband;  // band path: weight above the band / inside it (this CTA)
     int base[kUC + 1];  // exclusive prefix of the cluster's list sizes
     int ok, nsel, nband, count, ntok, reset, cnt0, kc_set, any_miss;
-    uint32_t WHI, ks, kc;
+    int mode;           // band-list ranking mode (see step 2), -1 = general path
+    uint32_t WHI, WB, ks, kc;
     uint32_t lo, hi, cb, rem, ncand;
     unsigned long long thr;
 };
@@ -187,8 +214,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
                  int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
-                 const __nv_bfloat16* __restrict__ E_next, float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
-                 int32_t* __restrict__ out_tokens, float scale_log2) {
+                 const __nv_bfloat16* __restrict__ E_next, int attend_pf, float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
+                 int32_t* __restrict__ out_tokens, float scale_log2, int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
     constexpr int GPW = 32 / TPS;               // sentences per warp step
@@ -196,6 +223,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     static_assert(TS % (kUW * GPW) == 0, "tile must split evenly over the warps");
     static_assert(GRP <= 8, "heads fill the N = 8 side of the MMA");
 
+    SKV_LSTAMP(0);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // [ring | keys | offs | own list | band list | sel_tok | sel_src | sel_id | rowtab]; the ring is
     // reused for the gathered lists, then for the warp-merge area
@@ -278,6 +306,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     pdl_wait();
     SKV_TRACE_POINT(0);
     SKV_USTAMP(0);
+    SKV_LSTAMP(1);
     const int prev = sel.parity[unit], cur = prev ^ 1;
     const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
     const uint32_t klo = band.x, khi = band.y;
@@ -479,11 +508,23 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         if (lane == 0) {
             ctl.base[0] = 0;
             ctl.WHI = WHI;
-            ctl.ok = !ovf && WHI <= (uint32_t)tau && (WHI + WB > (uint32_t)tau || klo == 0u);
+            ctl.WB = WB;
+            // 0: the crossing point is in the band; 2: above it (only entries above khi can be
+            // selected, and all of them are listed); -1: a list overflowed, or the crossing point is
+            // below the band -> general path.  (Rebuilding the lists below the band instead was
+            // measured slower than the general path: its candidate set is as large and the band
+            // ranking is quadratic in it.)
+            int mode = -1;
+            if (!ovf) {
+                if (WHI <= (uint32_t)tau && (WHI + WB > (uint32_t)tau || klo == 0u)) mode = 0;
+                else if (WHI > (uint32_t)tau) mode = 2;
+            }
+            ctl.mode = mode;
+            ctl.ok = mode >= 0;
 #ifdef SKV_TRACE
             if (unit * kUC + rank < 1024) {
                 g_unit_t[unit * kUC + rank][10] = (ovf ? 1 : 0) | (WHI > (uint32_t)tau ? 2 : 0) |
-                                                  (WHI + WB <= (uint32_t)tau && klo != 0u ? 4 : 0);
+                                                  (WHI + WB <= (uint32_t)tau && klo != 0u ? 4 : 0) | ((mode + 1) << 4);
                 g_unit_t[unit * kUC + rank][13] = (unsigned long long)incl;
             }
 #endif
@@ -491,20 +532,43 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     }
     __syncthreads();
     SKV_USTAMP(16);
-    bool ok = ctl.ok != 0;
+    int mode = ctl.mode;
+    // ranking of the gathered lists: entries with key > auto_gt are selected, entries with key in
+    // [rank_ge, auto_gt] are ranked on top of the weight W0 of everything above them, the rest is
+    // not selected
+    uint32_t auto_gt = khi, rank_ge = klo, W0 = ctl.WHI;
+    if (mode == 2) {  // WHI > tau: the crossing point is above the band, among the listed entries > khi
+        auto_gt = 0xffffffffu;
+        rank_ge = khi + 1u;  // khi < 0xffffffff here (else WHI = 0)
+        W0 = 0u;
+    }
+    bool ok = mode >= 0;
     if (ok) {
         // gather the lists in rank order (so in ascending sentence order); band entries are ranked
         const int ntot = ctl.base[kUC];
         int* bidx = reinterpret_cast<int*>(gath + kUC * kUBandCap);  // [ntot] indices of band entries
         int* flag = bidx + kUC * kUBandCap;                          // [ntot] selected
-        for (int i = tid; i < ntot; i += kUT) {
-            int j = 0;
-            while (i >= ctl.base[j + 1]) ++j;
-            const int4 e = lists[j][i - ctl.base[j]];
-            gath[i] = e;
-            const bool above = (uint32_t)e.x > khi;
-            flag[i] = above ? 1 : 0;
-            if (!above) bidx[atomicAdd(&ctl.nband, 1)] = i;
+        for (int i0 = tid; i0 < ntot; i0 += 4 * kUT) {
+            int4 e[4];  // remote (DSMEM) loads issued together, then stored
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * kUT;
+                if (i < ntot) {
+                    int j = 0;
+                    while (i >= ctl.base[j + 1]) ++j;
+                    e[k] = lists[j][i - ctl.base[j]];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k * kUT;
+                if (i < ntot) {
+                    gath[i] = e[k];
+                    const bool above = (uint32_t)e[k].x > auto_gt;
+                    flag[i] = above ? 1 : 0;
+                    if (!above && (uint32_t)e[k].x >= rank_ge) bidx[atomicAdd(&ctl.nband, 1)] = i;
+                }
+            }
         }
         __syncthreads();
         SKV_USTAMP(17);
@@ -512,7 +576,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             // a band entry is selected iff (weight above the band) + (weight of band entries ranked
             // above it) + its length fits tau; the one that first does not fit is the crossing point
             const int nbd = ctl.nband;
-            const uint32_t WHI = ctl.WHI;
+            const uint32_t WHI = W0;
             for (int x = tid; x < nbd; x += kUT) {
                 const int i = bidx[x];
                 const int4 e = gath[i];
@@ -599,6 +663,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (tid == 0) {
                 ctl.own_count = (int)total;
                 ctl.own_global = to_global ? 1 : 0;
+#ifdef SKV_TRACE
+                if (unit * kUC + rank < 1024) g_unit_t[unit * kUC + rank][14] = total | (to_global ? (1ull << 32) : 0ull);
+#endif
             }
         }
         cluster.sync();  // #1: every CTA's candidate list is complete
@@ -624,11 +691,24 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         __syncthreads();
         const int ntot = ctl.base[kUC];
         const bool gathered = ntot <= kUGather;
+#ifdef SKV_TRACE
+        if (tid == 0 && unit * kUC + rank < 1024) g_unit_t[unit * kUC + rank][15] = (unsigned long long)ntot;
+#endif
         if (gathered) {
-            for (int i = tid; i < ntot; i += kUT) {
-                int j = 0;
-                while (i >= ctl.base[j + 1]) ++j;
-                gath[i] = lists[j][i - ctl.base[j]];
+            for (int i0 = tid; i0 < ntot; i0 += 4 * kUT) {
+                int4 e[4];  // remote (DSMEM / global) loads issued together, then stored
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = i0 + k * kUT;
+                    if (i < ntot) {
+                        int j = 0;
+                        while (i >= ctl.base[j + 1]) ++j;
+                        e[k] = lists[j][i - ctl.base[j]];
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (i0 + k * kUT < ntot) gath[i0 + k * kUT] = e[k];
             }
         }
         auto cand = [&](int i) -> int4 {
@@ -905,6 +985,21 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         __syncthreads();
     };
+    if (!HOST && attend_pf) {
+        // L2 prefetch of this CTA's gathered rows (one bulk prefetch per sentence run and K / V),
+        // issued before the row table so that the whole share is requested from HBM at once; the
+        // warps' register loads below then mostly hit L2 (a warp holds one tile in registers).
+        const size_t ub = (size_t)unit * kv.unit_stride;
+        for (int i = tid; i < count; i += kUT) {
+            const int a0 = max(sel_tok[i], T0), a1 = min(sel_tok[i + 1], T1);
+            if (a0 < a1) {
+                const size_t row = ub + sel_src[i] + (a0 - sel_tok[i]);
+                const uint32_t bytes = (uint32_t)((a1 - a0) * D * 2);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.K + row * D), "r"(bytes) : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.V + row * D), "r"(bytes) : "memory");
+            }
+        }
+    }
     int my_miss = 0;
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
@@ -1092,6 +1187,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
     if (rank == 0 && tid == 0) sel.parity[unit] = cur;
     SKV_USTAMP(9);
+    SKV_LSTAMP(2);
 }
 
 size_t unit_smem_bytes(int d, int tau) {
@@ -1109,6 +1205,7 @@ bool unit_supported(int d, int grp, int Smax, int tau, int slots) {
 }
 
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
+
 
 bool unit_enabled() {
     static const bool on = [] {
@@ -1137,6 +1234,18 @@ static bool prefetch_enabled() {
     return on;
 }
 
+static bool attend_prefetch() {
+    // L2 prefetch of the current selection's rows before the attention: opt-in (SKV_ATTEND_PF=1).
+    // Measured on B200 (r01): the attention phase got slower (7.7 vs 6.4 us per CTA, trace).
+    static const bool on = [] {
+        const char* e = getenv("SKV_ATTEND_PF");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
+
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     const size_t smem = unit_smem_bytes(D, a.sel.tau);
@@ -1154,8 +1263,9 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     return launch_pdl_if(pdl_step_enabled(), unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
-                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.E_next, a.out, a.out_ids,
-                      a.out_count, a.out_tokens, scale_log2);
+                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.E_next, attend_prefetch() ? 1 : 0,
+                      a.out, a.out_ids,
+                      a.out_count, a.out_tokens, scale_log2, trace_counter++);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {

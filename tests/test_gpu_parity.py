@@ -180,12 +180,13 @@ def test_unit_step_kernel_off_parity_subprocess(cuda_device):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("band_log2", ["0", "30"])
+@pytest.mark.parametrize("band_log2", ["0", "12", "30"])
 def test_step_kernel_selection_paths_subprocess(cuda_device, band_log2):
     """The one-launch step kernel ranks either the band around the previous crossing point or, when
-    the crossing left the band, the union of the local candidate lists.  A zero-width band
-    (SKV_BAND_LOG2=0) sends most steps down the general path, a very wide one (30) overflows the band
-    lists: both must give the oracle's selections and outputs."""
+    the crossing left the band, the entries above it (mode 2) or the union of the local candidate
+    lists (general path).  A zero-width or narrow band (SKV_BAND_LOG2=0, 12) sends most steps through
+    mode 2 and the general path, a very wide one (30) overflows the
+    band lists: all must give the oracle's selections and outputs."""
     import os
     import subprocess
     import sys
