@@ -268,6 +268,24 @@ def main():
             if world > 1:  # the one exchange: all-gather of the per-head outputs of the layer
                 parallel.all_gather_outputs(outs[l], plan, gathered=gath[l])
 
+    # cold step (host residency): the first decode step after the prefill finds the HBM page cache
+    # empty, so every selected row of every layer crosses the host link (D3 host) -- its
+    # device time and ledger bytes give the offload fetch's host-link GB/s
+    cold = None
+    if host:
+        led0 = sum(skv.host_fetch_bytes(l) for l in range(M))
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        c0.record()
+        step(0)
+        c1.record()
+        torch.cuda.synchronize()
+        cold_ms = c0.elapsed_time(c1)
+        cold_bytes = sum(skv.host_fetch_bytes(l) for l in range(M)) - led0
+        cold = {"ms": round(cold_ms, 3), "host_bytes": int(cold_bytes),
+                "host_link_gbs": round(cold_bytes / (cold_ms / 1e3) / 1e9, 2)}
+
     # eager warm-up, then one CUDA graph per pool step (eager fallback if capture fails)
     for p in range(POOL):
         step(p)
@@ -466,7 +484,7 @@ def main():
             "host_residency": {"host_bytes_per_step": int(host_step_bytes),
                                "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
                                "offload_gbs_p3": round(kv_bytes_total / offload_s / 1e9, 2) if offload_s else None,
-                               "working_set_tokens_per_unit": 2 * tau} if host else None,
+                               "working_set_tokens_per_unit": 2 * tau, "cold_first_step": cold} if host else None,
             "cpu_baseline": cpu,
             "kv_gen_s": round(t_gen, 2),
         }

@@ -577,14 +577,33 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             // above it) + its length fits tau; the one that first does not fit is the crossing point
             const int nbd = ctl.nband;
             const uint32_t WHI = W0;
+            // band entries packed as (key, ~id, length) in the idle keys/offsets area, so the
+            // quadratic rank loop reads one broadcast 16-byte word per entry, no indirection
+            uint4* bent = reinterpret_cast<uint4*>(keys);
+            const bool packed = nbd <= (int)(2 * sizeof(uint32_t) * kULocalCap / sizeof(uint4));
+            if (packed) {
+                for (int x = tid; x < nbd; x += kUT) {
+                    const int4 e = gath[bidx[x]];
+                    bent[x] = make_uint4((uint32_t)e.x, 0xffffffffu - (uint32_t)e.y, (uint32_t)e.w, 0u);
+                }
+                __syncthreads();
+            }
             for (int x = tid; x < nbd; x += kUT) {
                 const int i = bidx[x];
                 const int4 e = gath[i];
                 const unsigned long long ke = ukey64((uint32_t)e.x, e.y);
                 uint32_t w = WHI;
-                for (int c = 0; c < nbd; ++c) {
-                    const int4 f = gath[bidx[c]];
-                    if (ukey64((uint32_t)f.x, f.y) > ke) w += (uint32_t)f.w;
+                if (packed) {
+#pragma unroll 4
+                    for (int c = 0; c < nbd; ++c) {
+                        const uint4 f = bent[c];
+                        if ((((unsigned long long)f.x << 32) | f.y) > ke) w += f.z;
+                    }
+                } else {
+                    for (int c = 0; c < nbd; ++c) {
+                        const int4 f = gath[bidx[c]];
+                        if (ukey64((uint32_t)f.x, f.y) > ke) w += (uint32_t)f.w;
+                    }
                 }
                 if (w + (uint32_t)e.w <= (uint32_t)tau) {
                     flag[i] = 1;
