@@ -209,8 +209,9 @@ typedef enum {
     SKV_K_SELECT = 3,  /* D2 */
     SKV_K_ATTEND = 4,  /* D3 + D4 */
     SKV_K_FUSED = 5,   /* D2 + D3 + D4 fused (decode_step, opt-in kernels) */
-    SKV_K_STEP = 6,    /* D1 + D2 + D3 + D4 in one launch (decode_step, default, device residency) */
-    SKV_K_COUNT = 7
+    SKV_K_STEP = 6,    /* D1 + D2 + D3 + D4 in one launch (decode_step, default) */
+    SKV_K_OFFLOAD = 7, /* P3: the D2H copies of a layer's K and V on the ctx's copy stream (host residency) */
+    SKV_K_COUNT = 8
 } skv_kernel_kind;
 
 skv_status sentencekv_set_profiling(skv_ctx* ctx, int32_t on);

@@ -252,7 +252,7 @@ class SentenceKV:
     def launch_count(self) -> int:
         return int(lib.sentencekv_launch_count(self.ctx))
 
-    KERNELS = ("segment", "compress", "score", "select", "attend", "fused", "step")
+    KERNELS = ("segment", "compress", "score", "select", "attend", "fused", "step", "offload")
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))

@@ -468,8 +468,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         if (!c->copy_event) SKV_CUDA(c, cudaEventCreateWithFlags(&c->copy_event, cudaEventDisableTiming));
         SKV_CUDA(c, cudaEventRecord(c->copy_event, st));
         SKV_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_event, 0));
+        cudaEvent_t po = prof_begin(c, c->copy_stream);
         SKV_CUDA(c, cudaMemcpyAsync(ls.Kh, Kb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
         SKV_CUDA(c, cudaMemcpyAsync(ls.Vh, Vb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        prof_end(c, SKV_K_OFFLOAD, po, c->copy_stream);
         SKV_CUDA(c, cudaEventRecord(ls.offload_done, c->copy_stream));
         ls.host_ready = false;
         ls.K = ls.V = nullptr;  // the caller may free its K/V after sentencekv_sync
