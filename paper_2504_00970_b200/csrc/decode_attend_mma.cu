@@ -159,8 +159,8 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
             // write the tile's rows through to the current working-set slot (gathered order)
 #pragma unroll
             for (int u = 0; u < NU; ++u) {
-                if (rk0 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq) * D + cq * (D / 4) + 8 * u) = tr.kA[u];
-                if (rk1 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq + 8) * D + cq * (D / 4) + 8 * u) = tr.kB[u];
+                if (rk0 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq) * D + mma::kseg(cq, u)) = tr.kA[u];
+                if (rk1 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq + 8) * D + mma::kseg(cq, u)) = tr.kB[u];
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)

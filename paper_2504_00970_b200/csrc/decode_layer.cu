@@ -593,7 +593,7 @@ __device__ void attend_item(const LayerArgs& a, LayerSmem<D>& sm, int u, int c) 
     uint4 qseg[NU];
 #pragma unroll
     for (int uu = 0; uu < NU; ++uu)
-        qseg[uu] = gq < GRP ? ldg16(a.q + ((size_t)b * Hq + g * GRP + gq) * D + cq * (D / 4) + 8 * uu)
+        qseg[uu] = gq < GRP ? ldg16(a.q + ((size_t)b * Hq + g * GRP + gq) * D + (4 * uu + cq) * 8)
                             : make_uint4(0, 0, 0, 0);
     float m2[2] = {-INFINITY, -INFINITY}, l2[2] = {0.0f, 0.0f};
     float acc[NKS][4];
@@ -606,8 +606,8 @@ __device__ void attend_item(const LayerArgs& a, LayerSmem<D>& sm, int u, int c) 
         uint4 kA[NU], kB[NU];
 #pragma unroll
         for (int uu = 0; uu < NU; ++uu) {
-            kA[uu] = rk0 != kInvalidRow ? ldg16(Kd + (size_t)rk0 * D + cq * (D / 4) + 8 * uu) : make_uint4(0, 0, 0, 0);
-            kB[uu] = rk1 != kInvalidRow ? ldg16(Kd + (size_t)rk1 * D + cq * (D / 4) + 8 * uu) : make_uint4(0, 0, 0, 0);
+            kA[uu] = rk0 != kInvalidRow ? ldg16(Kd + (size_t)rk0 * D + (4 * uu + cq) * 8) : make_uint4(0, 0, 0, 0);
+            kB[uu] = rk1 != kInvalidRow ? ldg16(Kd + (size_t)rk1 * D + (4 * uu + cq) * 8) : make_uint4(0, 0, 0, 0);
         }
         uint4 vv[4][NVP];
 #pragma unroll

@@ -1112,8 +1112,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                     __nv_bfloat16* Vw = hc.wsV + (size_t)unit * hc.slots * kPage * D;
     #pragma unroll
                     for (int u = 0; u < NU; ++u) {
-                        if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + cq * (D / 4) + 8 * u) = tr.kA[u];
-                        if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + cq * (D / 4) + 8 * u) = tr.kB[u];
+                        if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + mma::kseg(cq, u)) = tr.kA[u];
+                        if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + mma::kseg(cq, u)) = tr.kB[u];
                     }
     #pragma unroll
                     for (int k = 0; k < 4; ++k)

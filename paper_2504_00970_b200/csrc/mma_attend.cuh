@@ -62,13 +62,19 @@ struct WarpAcc {
     }
 };
 
-// q as the B operand of QK: lane (gq, cq) holds head gq, d-range [cq*D/4, (cq+1)*D/4)
+// Reduction-index permutation of QK (the same for K and q): piece u (8 consecutive d) of lane
+// (gq, cq) starts at d = (4u + cq) * 8, so one load instruction of the 4 lanes of a row reads 64
+// contiguous bytes (whole 32-byte sectors -- over PCIe, rows read from mapped host memory, each
+// sector crosses the link once).
+__device__ __forceinline__ constexpr int kseg(int cq, int u) { return (4 * u + cq) * 8; }
+
+// q as the B operand of QK: lane (gq, cq) holds head gq, pieces kseg(cq, u)
 template <int D, int GRP>
 __device__ __forceinline__ void load_q(uint4 (&qseg)[D / 32], const __nv_bfloat16* qh0, int lane) {
     const int gq = lane >> 2, cq = lane & 3;
 #pragma unroll
     for (int u = 0; u < D / 32; ++u)
-        qseg[u] = gq < GRP ? ldg16(qh0 + (size_t)gq * D + cq * (D / 4) + 8 * u) : make_uint4(0, 0, 0, 0);
+        qseg[u] = gq < GRP ? ldg16(qh0 + (size_t)gq * D + kseg(cq, u)) : make_uint4(0, 0, 0, 0);
 }
 
 // Registers of one tile: K rows of tokens gq, gq+8 and V rows of tokens 2cq, 2cq+1, 2cq+8, 2cq+9.
@@ -86,8 +92,8 @@ __device__ __forceinline__ void load_tile(TileRegs<D>& t, const __nv_bfloat16* r
     const int gq = lane >> 2, cq = lane & 3;
 #pragma unroll
     for (int u = 0; u < TileRegs<D>::NU; ++u) {
-        t.kA[u] = rk0 ? ldg16(rk0 + cq * (D / 4) + 8 * u) : make_uint4(0, 0, 0, 0);
-        t.kB[u] = rk1 ? ldg16(rk1 + cq * (D / 4) + 8 * u) : make_uint4(0, 0, 0, 0);
+        t.kA[u] = rk0 ? ldg16(rk0 + kseg(cq, u)) : make_uint4(0, 0, 0, 0);
+        t.kB[u] = rk1 ? ldg16(rk1 + kseg(cq, u)) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
