@@ -409,15 +409,25 @@ def main():
     tdev = torch.empty((Bl,), dtype=torch.int32, device=dev)
     odev = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
 
+    # each layer's output is read back on a copy stream as soon as its kernel is done, so the
+    # device->host read of the step's result overlaps the later layers
+    cstream = torch.cuda.Stream(device=dev)
+    ev_o = [torch.cuda.Event() for _ in range(M)]
+
     def e2e_step(p):
+        cur = torch.cuda.current_stream()
         qdev.copy_(qhost[p], non_blocking=True)
         tdev.copy_(thost[p], non_blocking=True)
         for l in range(M):
             skvlib.sentencekv_decode_step(skv.ctx, l, qdev[l], tdev, odev[l])
             if world > 1:
                 parallel.all_gather_outputs(odev[l], plan, gathered=gath[l])
-        ohost.copy_(odev, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+            ev_o[l].record(cur)
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(ev_o[l])
+                ohost[l].copy_(odev[l], non_blocking=True)
+        cur.synchronize()
+        cstream.synchronize()
 
     for p in range(3):
         e2e_step(p)
