@@ -7,12 +7,15 @@
 //   1. score (D1; Eq. 2, S = qbar^T kbar P:440-442, Alg. 1 l.14-16): CTA r streams the
 //      embeddings of its contiguous sentence range [r*chunk, (r+1)*chunk) through a TMA bulk-copy
 //      ring (cp.async.bulk + mbarrier, L2 evict-first) and keeps the ordered 32-bit keys in shared
-//      memory.  While the ring is in flight the CTA issues L2 prefetches of its share of the K/V
-//      runs the unit selected at the previous decode step (selections change little from token to
-//      token, so step 3 then mostly reads L2).
+//      memory.  (Opt-in L2 prefetches -- of the K/V runs selected at the previous step, of the next
+//      layer's E, of this step's selection -- were measured on B200 and did not pay.)
 //   2. select (D2; Alg. 1 l.17, readings A13-A15): the budgeted selection is the maximal
 //      prefix of the ranking by key64 = (ordered(score) << 32) | (0xffffffff - s) whose length
-//      fits tau.  Each CTA first cuts its own range down to *local candidates*: a sentence whose
+//      fits tau.  Fast path: each CTA lists its sentences at or above a band around the previous
+//      step's crossing point; after one cluster barrier every CTA ranks the listed band entries
+//      (mode 0) or, if the weight above the band already exceeds tau, the listed entries above it
+//      (mode 2).  General path (a list overflowed, or the crossing point fell below the band): each
+//      CTA first cuts its own range down to *local candidates*: a sentence whose
 //      local weight-above (summed lengths of the CTA's sentences ranked above it) exceeds tau can
 //      never be selected, so it keeps every sentence ranked at or above its local crossing point
 //      (one length-weighted 1024-bin histogram over the local key range; the crossing bin is kept
