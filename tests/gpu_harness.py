@@ -26,7 +26,9 @@ def run_parity(skv, orc: oracle.Oracle, toks, Ks, Vs, qs, script_tok, bset, devi
     Ks/Vs: per layer bf16 bits [B][G][L][d]; qs[step][layer]: bf16 bits [B][Hq][d].
     units: optional list of (b, g) to compare (default: all).
     mode: "split" = sentencekv_decode_select + sentencekv_decode_attend; "step" =
-    sentencekv_decode_step (fused select + attend).
+    sentencekv_decode_step (fused select + attend); "graph" = as bench.py times it: step 0 eager,
+    then ONE CUDA graph of sentencekv_decode_step over all layers, captured once over static input
+    buffers and replayed for every later step with that step's inputs copied in.
     Returns a dict of statistics."""
     B, G, tau = skv.B, skv.G, skv.tau
     M = len(Ks)
@@ -57,22 +59,48 @@ def run_parity(skv, orc: oracle.Oracle, toks, Ks, Vs, qs, script_tok, bset, devi
     sel_cnt = torch.empty((B, G), dtype=torch.int32, device=device)
     sel_tok = torch.empty((B, G), dtype=torch.int32, device=device)
     out = torch.empty((B, skv.Hq, skv.d), dtype=torch.float32, device=device)
+    graph = None
+    if mode == "graph":  # static buffers of the captured step, one set of outputs per layer
+        gq = [torch.empty((B, skv.Hq, skv.d), dtype=torch.bfloat16, device=device) for _ in range(M)]
+        git = torch.empty((B,), dtype=torch.int32, device=device)
+        gids = [torch.empty_like(sel_ids) for _ in range(M)]
+        gcnt = [torch.empty_like(sel_cnt) for _ in range(M)]
+        gtok = [torch.empty_like(sel_tok) for _ in range(M)]
+        gout = [torch.empty_like(out) for _ in range(M)]
     for step, qstep in enumerate(qs):
         it = torch.from_numpy(np.ascontiguousarray(script_tok[step])).to(device)
+        if mode == "graph" and step > 0:
+            for l in range(M):
+                gq[l].copy_(from_bits(qstep[l], device))
+            git.copy_(it)
+            if graph is None:
+                torch.cuda.synchronize()
+                cs = torch.cuda.Stream(device=device)
+                with torch.cuda.stream(cs):
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph, stream=cs):
+                        for l in range(M):
+                            skv.decode_step(l, gq[l], git, gout[l], gids[l], gcnt[l], gtok[l])
+                torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
         for l in range(M):
             q_bits = qstep[l]
             qd = from_bits(q_bits, device)
-            if mode == "step":
+            if mode == "graph" and step > 0:
+                pass  # this step already ran (graph replay)
+            elif mode in ("step", "graph"):
                 skv.decode_step(l, qd, it, out, sel_ids, sel_cnt, sel_tok)
             else:
                 skv.decode_select(l, qd, it, sel_ids, sel_cnt, sel_tok)
                 skv.decode_attend(l, qd, out)
             sc_o, ids_o, ntok_o = orc.decode_select(l, q_bits, script_tok[step])
             O_o = orc.decode_attend(l, q_bits, ids_o)
-            ids_g = sel_ids.cpu().numpy()
-            cnt_g = sel_cnt.cpu().numpy()
-            tok_g = sel_tok.cpu().numpy()
-            O_g = out.cpu().numpy()
+            replayed = mode == "graph" and step > 0
+            ids_g = (gids[l] if replayed else sel_ids).cpu().numpy()
+            cnt_g = (gcnt[l] if replayed else sel_cnt).cpu().numpy()
+            tok_g = (gtok[l] if replayed else sel_tok).cpu().numpy()
+            O_g = (gout[l] if replayed else out).cpu().numpy()
             sc_g = skv.scores(l).cpu().numpy() if check_scores else None
             for b, g in units:
                 if check_scores:

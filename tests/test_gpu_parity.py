@@ -200,6 +200,23 @@ def test_step_kernel_selection_paths_subprocess(cuda_device, band_log2):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("residency", ["device", "host"])
+def test_graph_replay_parity(cuda_device, residency):
+    """bench.py's launch configuration: the decode step of all layers captured once into a CUDA graph
+    (programmatic launch between the layers' kernels) and replayed for every step with new inputs;
+    the device-side state (selection slot parity, band hints, Q_s sums, page cache) must evolve as
+    in the oracle, step after step."""
+    import paper_2504_00970_b200 as skvlib
+
+    B, M, Hq, G, d, L, tau, steps = 2, 3, 16, 4, 128, 8192, 512, 6
+    toks, topics, Ks, Vs, qs, script = make_case(3, B, M, Hq, G, d, L, tau, steps, 25.0)
+    skv = _skv(B, M, Hq, G, d, L, tau,
+               residency=skvlib.SKV_KV_HOST if residency == "host" else skvlib.SKV_KV_DEVICE)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode="graph")
+    assert st["steps"] == steps
+
+
 def test_deterministic_run_to_run(cuda_device):
     B, M, Hq, G, d, L, tau, steps = 2, 1, 8, 2, 128, 6000, 512, 5
     toks, _, Ks, Vs, qs, script = make_case(8, B, M, Hq, G, d, L, tau, steps, median=25.0)
