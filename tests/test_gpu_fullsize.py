@@ -16,9 +16,10 @@ from tests.gpu_harness import ATOL, to_bits
 pytestmark = pytest.mark.gpu
 
 
-def _fullsize(dev, residency, B, Hq, G, d, L, tau, units, steps=3, layer=1, b0=0, g0=0, Gl=None):
+def _fullsize(dev, residency, B, Hq, G, d, L, tau, units, steps=3, layer=1, b0=0, g0=0, Gl=None, graph=False):
     """One rank's shard: global sequences b0 .. b0+B-1, KV heads g0 .. g0+Gl-1 of G (query heads
-    grp*g0 .. grp*(g0+Gl)-1).  units are shard-local (b, g)."""
+    grp*g0 .. grp*(g0+Gl)-1).  units are shard-local (b, g).  graph: steps after the first run as
+    bench.py runs them, one captured CUDA graph of both layers replayed with each step's inputs."""
     import paper_2504_00970_b200 as skvlib
 
     Gl = Gl or G - g0
@@ -60,13 +61,32 @@ def _fullsize(dev, residency, B, Hq, G, d, L, tau, units, steps=3, layer=1, b0=0
     ids = torch.empty((B, Gl, tau), dtype=torch.int32, device=dev)
     out = torch.empty((B, Hl, d), dtype=torch.float32, device=dev)
     bset = set(synth.BOUNDARY_IDS.tolist())
+    g_q0, g_q, g_it, g_o0 = (torch.empty_like(out, dtype=torch.bfloat16), torch.empty_like(out, dtype=torch.bfloat16),
+                             torch.empty((B,), dtype=torch.int32, device=dev), torch.empty_like(out))
+    cg = None
     for s in range(steps):
         tg = torch.from_numpy(target[s]).to(dev)
         q0 = synth.queries_torch(gen, KV[0][2], tg, Hq, G, d)[:, h0:h0 + Hl].contiguous()
         q = synth.queries_torch(gen, KV[layer][2], tg, Hq, G, d)[:, h0:h0 + Hl].contiguous()
         it = torch.from_numpy(script[s]).to(dev)
-        skv.decode_step(0, q0, it, torch.empty_like(out))  # layer 0 runs too, as in a real step
-        skv.decode_step(layer, q, it, out, sel_ids=ids)
+        if graph and s > 0:
+            g_q0.copy_(q0)
+            g_q.copy_(q)
+            g_it.copy_(it)
+            if cg is None:
+                torch.cuda.synchronize()
+                cs = torch.cuda.Stream(device=dev)
+                with torch.cuda.stream(cs):
+                    cg = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(cg, stream=cs):
+                        skv.decode_step(0, g_q0, g_it, g_o0)
+                        skv.decode_step(layer, g_q, g_it, out, sel_ids=ids)
+                torch.cuda.synchronize()
+            cg.replay()
+            torch.cuda.synchronize()
+        else:
+            skv.decode_step(0, q0, it, torch.empty_like(out))  # layer 0 runs too, as in a real step
+            skv.decode_step(layer, q, it, out, sel_ids=ids)
         qb = to_bits(q)
         sc = skv.scores(layer).cpu().numpy()
         got_ids = ids.cpu().numpy()
@@ -87,9 +107,10 @@ def _fullsize(dev, residency, B, Hq, G, d, L, tau, units, steps=3, layer=1, b0=0
 
 @pytest.mark.parametrize("residency", ["host", "device"])
 def test_config2_sampled_units(cuda_device, residency):
-    """configs[2]: 8B shapes, 128K, tau 2048, batch 4, all heads (the bench's N=1 workload)."""
+    """configs[2]: 8B shapes, 128K, tau 2048, batch 4, all heads (the bench's N=1 workload), in the
+    bench's launch configuration (CUDA-graph replay after the first step)."""
     _fullsize(cuda_device, residency, B=4, Hq=32, G=8, d=128, L=131072, tau=2048,
-              units=[(0, 0), (1, 3), (2, 5), (3, 7)])
+              units=[(0, 0), (1, 3), (2, 5), (3, 7)], steps=4, graph=True)
 
 
 def test_config3_head_shard_sampled_units(cuda_device):
