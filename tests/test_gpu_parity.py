@@ -217,7 +217,10 @@ def test_graph_replay_parity(cuda_device, residency):
     assert st["steps"] == steps
 
 
-def test_deterministic_run_to_run(cuda_device):
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_deterministic_run_to_run(cuda_device, mode):
+    """Two runs of the same inputs give bit-identical selections and outputs (static work split,
+    fixed merge order; no atomics decide an fp32 summation order)."""
     B, M, Hq, G, d, L, tau, steps = 2, 1, 8, 2, 128, 6000, 512, 5
     toks, _, Ks, Vs, qs, script = make_case(8, B, M, Hq, G, d, L, tau, steps, median=25.0)
     outs = []
@@ -231,8 +234,12 @@ def test_deterministic_run_to_run(cuda_device):
         res = []
         for s in range(steps):
             qd = from_bits(qs[s][0], cuda_device)
-            skv.decode_select(0, qd, torch.from_numpy(script[s]).to(cuda_device), ids)
-            skv.decode_attend(0, qd, out)
+            it = torch.from_numpy(script[s]).to(cuda_device)
+            if mode == "step":
+                skv.decode_step(0, qd, it, out, ids)
+            else:
+                skv.decode_select(0, qd, it, ids)
+                skv.decode_attend(0, qd, out)
             res.append((ids.cpu().numpy().copy(), out.cpu().numpy().copy()))
         outs.append(res)
     for (i1, o1), (i2, o2) in zip(*outs):
