@@ -115,6 +115,7 @@ constexpr int kUBins = 1024;
 constexpr int kUExact = kUT;             // crossing-bin candidates ranked exactly per refinement level
 constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
 constexpr int kUBandCap = 256;           // band-path list entries per CTA
+constexpr int kBentCap = 2 * 4 * kULocalCap / 16;  // packed band entries in the (idle) keys + offsets area
 static_assert(kUC * kUBandCap * (16 + 4 + 4) <= kUStages * kUTileBytes, "band lists fit the ring");
 using mma::kInvalid;
 using mma::kTile;
@@ -569,7 +570,14 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                     gath[i] = e[k];
                     const bool above = (uint32_t)e[k].x > auto_gt;
                     flag[i] = above ? 1 : 0;
-                    if (!above && (uint32_t)e[k].x >= rank_ge) bidx[atomicAdd(&ctl.nband, 1)] = i;
+                    if (!above && (uint32_t)e[k].x >= rank_ge) {
+                        // band entry: its index, and (key, ~id, length) packed for the rank loop
+                        const int x = atomicAdd(&ctl.nband, 1);
+                        bidx[x] = i;
+                        if (x < kBentCap)
+                            reinterpret_cast<uint4*>(keys)[x] =
+                                make_uint4((uint32_t)e[k].x, 0xffffffffu - (uint32_t)e[k].y, (uint32_t)e[k].w, 0u);
+                    }
                 }
             }
         }
@@ -582,15 +590,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             const uint32_t WHI = W0;
             // band entries packed as (key, ~id, length) in the idle keys/offsets area, so the
             // quadratic rank loop reads one broadcast 16-byte word per entry, no indirection
-            uint4* bent = reinterpret_cast<uint4*>(keys);
-            const bool packed = nbd <= (int)(2 * sizeof(uint32_t) * kULocalCap / sizeof(uint4));
-            if (packed) {
-                for (int x = tid; x < nbd; x += kUT) {
-                    const int4 e = gath[bidx[x]];
-                    bent[x] = make_uint4((uint32_t)e.x, 0xffffffffu - (uint32_t)e.y, (uint32_t)e.w, 0u);
-                }
-                __syncthreads();
-            }
+            const uint4* bent = reinterpret_cast<const uint4*>(keys);  // packed by the gather above
+            const bool packed = nbd <= kBentCap;
             for (int x = tid; x < nbd; x += kUT) {
                 const int i = bidx[x];
                 const int4 e = gath[i];
