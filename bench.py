@@ -178,6 +178,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: SKV_BENCH_SAME_GPU=1 puts every rank on cuda:0 with the gloo backend, so the N > 1
+    # code path (shards, per-layer all-gather, barriers, max over ranks) can be exercised on one GPU;
+    # never used for a reported number
+    same_gpu = os.environ.get("SKV_BENCH_SAME_GPU", "") == "1"
+    if same_gpu:
+        local = 0
     cfg = dict(CONFIGS[args.config])
     B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
     hbm_peak, peak_kind = peaks()
@@ -193,7 +199,10 @@ def main():
         raise SystemExit("--shard batch with host residency would pin world x the host store; use --shard heads")
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import paper_2504_00970_b200 as skvlib

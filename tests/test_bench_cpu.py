@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -38,3 +40,20 @@ def test_reference_arm_torchrun_rank0_only():
     assert r.returncode == 0, r.stderr[-2000:]
     (line,) = _lines(r.stdout)
     assert line["impl"] == "reference" and line["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_same_gpu():
+    """The N > 1 path of bench.py (per-rank head shards, per-layer all-gather of the outputs,
+    barriers, max over ranks, one line from rank 0) on ONE GPU: both ranks on cuda:0 with the gloo
+    backend (SKV_BENCH_SAME_GPU=1; a test hook, not a measurement)."""
+    env = dict(os.environ, SKV_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29537", "bench.py", "--gpus", "2",
+                        "--config", "8b-32k", "--residency", "device", "--steps", "4", "--warmup", "3",
+                        "--e2e-steps", "2", "--no-cpu-baseline"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    (line,) = _lines(r.stdout)
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "1 batch x 2 KV-head shards"
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] == 32 * 4
