@@ -1,15 +1,22 @@
 #!/usr/bin/env python
 """bench.py -- SentenceKV decode-step benchmark on B200 (driver contract: one JSON line on rank 0).
 
-A "step" is one pass of the whole hot path for one decode token: for every layer,
-D1+D2 (sentencekv_decode_select: Eq. 2 query cache, scores over all sentence embeddings,
-budgeted whole-sentence selection) and D3+D4 (sentencekv_decode_attend: gather + Eq. 3
-attention over the selected tokens), for all sequences of the batch.  Prefill (P1 segmentation,
-P2 embeddings) runs once before the timed region.
+A "step" is one pass of the whole hot path for one decode token of every sequence: for every layer
+one sentencekv_decode_step (D1 Eq. 2 query cache + scores over all sentence embeddings, D2 budgeted
+whole-sentence selection, D3 gather, D4 Eq. 3 attention), captured once into a CUDA graph.  Prefill
+(P1 segmentation, P2 embeddings, P3 offload in host residency) runs once before the timed region.
+
+Every timed step gets FRESH inputs: the queries and input tokens of step k of a seeded decode
+script (a boundary input about every 25 steps per sequence, after which the query topic changes,
+synth.decode_script) are copied into the graph's static input buffers before its replay (the 1 MB
+device-to-device copy is inside the timed region).  In host residency the topic switches make the
+selection move, so the per-step host-link traffic of D3 is the real one ("onload
+1024 tokens 0.0038 s" is the paper's cost of that transfer on H100 + PCIe).
 
 Default workload (BASELINE.json metric "decode-step latency (ms) & tokens/s at 128K ctx"):
 configs[2] = Llama-3.1-8B shapes (32 layers, 32 Q / 8 KV heads, d=128), 128K context, tau=2048,
-batch 4.  value = tokens/s = sequences decoded per second (B per step) over all ranks.
+batch 4, full K/V offloaded to pinned host.  value = tokens/s = sequences decoded per second (B per
+step) over all ranks.  --config 8b-32k / 8b-256k give the configs[1] / configs[3] lines.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 8b-128k] [--impl ours|reference]
 
@@ -43,17 +50,19 @@ CONFIGS = {
 }
 METRIC = "decode-step latency (ms) & tokens/s at 128K ctx; achieved HBM GB/s vs B200 peak"
 SEED = 0
-POOL = 8  # distinct decode steps cycled through (CUDA graph per step)
+CHECK_UNITS = 4  # (layer, b, g) units checked against the oracle at the end of the timed run
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="8b-128k", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-split", action="store_true", help="skip the decode_select + decode_attend line")
+    ap.add_argument("--no-check", action="store_true", help="skip the end-of-run oracle check")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--shard", choices=["heads", "batch"], default="heads")
     ap.add_argument("--residency", choices=["device", "host"], default=None,
@@ -68,6 +77,14 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def config_dict(args, cfg, GB, extra=None):
+    d = {"workload": args.config, "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
+         "kv_heads": cfg["G"], "head_dim": cfg["d"], "context": cfg["L"], "token_budget": cfg["tau"],
+         "median_sentence_tokens": cfg["median"]}
+    d.update(extra or {})
+    return d
 
 
 class ClockSampler:
@@ -95,18 +112,15 @@ class ClockSampler:
 
     def _run(self):
         nv = self.nv
-        names = {
-            nv.nvmlClocksEventReasonGpuIdle if hasattr(nv, "nvmlClocksEventReasonGpuIdle") else 0x1: "gpu_idle",
-            0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
-        }
+        names = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+                 0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
         while not self._stop.is_set():
             try:
                 self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in names.items():
-                    if r & bit and name != "gpu_idle":
+                    if r & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
@@ -122,51 +136,77 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
+def pct(xs, p):
+    return float(np.percentile(np.asarray(xs), p)) if len(xs) else None
+
+
 # --------------------------------------------------------------------------- oracle timing
 
 
-def oracle_sample(cfg, toks, Kh, Vh, qs, script, units, layers_sample, n_steps):
-    """Times the CPU oracle (select + attend per unit) on host copies of the same inputs.
-    Kh/Vh: {layer: uint16 [B][G][L][d]}; qs[step][layer]: uint16 [B][Hq][d].
-    Returns (seconds per (unit, layer, step), threads used)."""
-    import concurrent.futures as cf
+class OracleStep:
+    """The CPU oracle (tests' checker, oracle/) driven over full decode steps of a workload: every
+    layer, every (b, g) unit, select (Eq. 2 + scores + budgeted selection) + attend (Eq. 3), units
+    in parallel on all host threads (the C functions release the GIL).  K/V host copies exist for
+    `kv_layers` layers; layer l of a step uses the bytes of layer l % len(kv_layers) (same shapes,
+    same work), its own queries."""
 
-    import oracle
+    def __init__(self, cfg, toks, Kh, Vh):
+        import oracle
+        import synth
 
-    G, Hq, d, tau = cfg["G"], cfg["Hq"], cfg["d"], cfg["tau"]
-    grp = Hq // G
-    B = toks.shape[0]
-    offs = {b: oracle.segment(toks[b], __import__("synth").BOUNDARY_IDS, tau) for b in set(u[0] for u in units)}
-    threads = len(os.sched_getaffinity(0))
-    E = {}
-    with cf.ThreadPoolExecutor(threads) as ex:
-        futs = {(l, b, g): ex.submit(oracle.embed, Kh[l][b, g], offs[b]) for l in layers_sample for b, g in units}
-        for k, f in futs.items():
-            E[k] = f.result()
-    Sq = {(l, b): np.zeros((Hq, d), np.float32) for l in layers_sample for b in range(B)}
-    cnt = {(l, b): np.zeros(1, np.int32) for l in layers_sample for b in range(B)}
+        self.oracle, self.synth = oracle, synth
+        self.cfg = cfg
+        self.G, self.Hq, self.d, self.tau, self.M = cfg["G"], cfg["Hq"], cfg["d"], cfg["tau"], cfg["M"]
+        self.grp = self.Hq // self.G
+        self.B = toks.shape[0]
+        self.Kh, self.Vh = Kh, Vh  # lists of uint16 [B][G][L][d]
+        self.threads = len(os.sched_getaffinity(0))
+        import concurrent.futures as cf
 
-    def unit_step(l, b, g, q_bits, qbar):
-        qt = oracle.group_query(qbar, grp, g)
-        sc = oracle.score(qt, E[(l, b, g)])
-        ids, _ = oracle.select(sc, offs[b], tau)
-        oracle.attend(q_bits[b, g * grp:(g + 1) * grp], Kh[l][b, g], Vh[l][b, g], offs[b], ids)
+        self.ex = cf.ThreadPoolExecutor(self.threads)
+        self.off = [oracle.segment(toks[b], synth.BOUNDARY_IDS, self.tau) for b in range(self.B)]
+        futs = {(i, b, g): self.ex.submit(oracle.embed, Kh[i][b, g], self.off[b])
+                for i in range(len(Kh)) for b in range(self.B) for g in range(self.G)}
+        self.E = {k: f.result() for k, f in futs.items()}
+        self.Sq = np.zeros((self.M, self.B, self.Hq, self.d), np.float32)
+        self.cnt = np.zeros((self.M, self.B), np.int32)
+        self.bset = set(synth.BOUNDARY_IDS.tolist())
 
-    bset = set(__import__("synth").BOUNDARY_IDS.tolist())
-    t0 = time.perf_counter()
-    work = 0
-    with cf.ThreadPoolExecutor(threads) as ex:
-        for s in range(n_steps):
-            for l in layers_sample:
-                q_bits = qs[s % len(qs)][l]
-                qbars = {b: oracle.qs_append_mean(Sq[(l, b)], cnt[(l, b)], q_bits[b]) for b in set(u[0] for u in units)}
-                list(ex.map(lambda u: unit_step(l, u[0], u[1], q_bits, qbars[u[0]]), units))
-                work += len(units)
-                for b in set(u[0] for u in units):
-                    if int(script[s % len(script)][b]) in bset:
-                        oracle.qs_reset(Sq[(l, b)], cnt[(l, b)])
-    dt = time.perf_counter() - t0
-    return dt / work, threads
+    def step(self, q_layers, itok):
+        """One full decode step.  q_layers[l]: uint16 [B][Hq][d]; itok int32 [B]."""
+        o = self.oracle
+        nkv = len(self.Kh)
+
+        def unit(l, b, g, qbar):
+            i = l % nkv
+            qt = o.group_query(qbar, self.grp, g)
+            sc = o.score(qt, self.E[(i, b, g)])
+            ids, _ = o.select(sc, self.off[b], self.tau)
+            return o.attend(q_layers[l][b, g * self.grp:(g + 1) * self.grp], self.Kh[i][b, g], self.Vh[i][b, g],
+                            self.off[b], ids)
+
+        futs = []
+        for l in range(self.M):
+            for b in range(self.B):
+                qbar = o.qs_append_mean(self.Sq[l, b], self.cnt[l, b:b + 1], q_layers[l][b])
+                futs += [self.ex.submit(unit, l, b, g, qbar) for g in range(self.G)]
+                if int(itok[b]) in self.bset:
+                    o.qs_reset(self.Sq[l, b], self.cnt[l, b:b + 1])
+        for f in futs:
+            f.result()
+
+
+def time_oracle(ost, qsteps, itoks, n_steps, budget_s=None):
+    """Times n_steps full oracle steps (or as many as fit budget_s after the first).  Returns
+    (seconds per step list)."""
+    times = []
+    for k in range(n_steps):
+        t0 = time.perf_counter()
+        ost.step(qsteps[k % len(qsteps)], itoks[k % len(itoks)])
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and sum(times) >= budget_s:
+            break
+    return times
 
 
 # --------------------------------------------------------------------------- main
@@ -188,7 +228,7 @@ def main():
     B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
     hbm_peak, peak_kind = peaks()
     if args.impl == "reference":
-        return reference_arm(args, cfg, rank, world)
+        return reference_arm(args, cfg, rank, world, residency)
 
     import torch
     import torch.distributed as dist
@@ -212,6 +252,9 @@ def main():
     plan = parallel.plan(GB, G, Hq, world, rank, "batch" if args.shard == "batch" else "heads")
     Bl, Gl, Hl = plan.batch_count, plan.kv_head_count, plan.q_head_count
     b0, g0, h0 = plan.batch_begin, plan.kv_head_begin, plan.q_head_begin
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline
+    check = rank == 0 and world == 1 and not args.no_check
+    keep_layers = [0, 1][:M] if (cpu_leg or check) else []
 
     # ---------------- inputs (seeded, synthetic; this rank's shard of sequences and heads)
     toks, topics = zip(*(synth.token_stream(SEED, b0 + b, L, cfg["median"]) for b in range(Bl)))
@@ -223,8 +266,8 @@ def main():
                             residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE, **plan.ctx_kwargs())
     # ---------------- K/V generation + prefill (P1 segmentation, P2 embeddings, P3 offload in host
     # residency), per layer; in host residency the device K/V of a layer is freed once offloaded
-    # (layers 0, 1 are kept for the CPU-oracle baseline).
-    Ks, Vs, Cs = [], [], []
+    # (layers 0, 1 are copied to the host for the CPU oracle's baseline and end-of-run check).
+    Ks, Vs, Cs, Kh, Vh = [], [], [], [], []
     t_gen = prefill_ms = offload_s = 0.0
     skv.set_profiling(True)
     for l in range(M):
@@ -244,9 +287,11 @@ def main():
             offload_s += time.perf_counter() - t0
         torch.cuda.synchronize()
         prefill_ms += pf0.elapsed_time(pf1)
-        keep = (not host) or (l < 2 and world == 1)
-        Ks.append(K if keep else None)
-        Vs.append(V if keep else None)
+        if l in keep_layers:
+            Kh.append(K.view(torch.int16).cpu().numpy().view(np.uint16))
+            Vh.append(V.view(torch.int16).cpu().numpy().view(np.uint16))
+        Ks.append(None if host else K)
+        Vs.append(None if host else V)
         Cs.append(c)
         del K, V
     prof_prefill = skv.profile_read()
@@ -254,26 +299,47 @@ def main():
     S = skv.sentence_counts()
     kv_bytes_total = 2 * Bl * Gl * L * d * 2 * M
 
-    # ---------------- decode inputs: POOL distinct steps (queries of the full head set, sliced)
-    script, target = synth.decode_script(SEED, GB, POOL)
+    # ---------------- decode script: one fresh step of queries + input tokens per executed step
+    n_cold, n_eager = (1 if host else 0), 2
+    n_split = 0 if args.no_split else max(3, args.warmup) + min(args.steps, 100)
+    n_prof = 4
+    NQ = n_cold + n_eager + max(1, args.warmup) + args.steps + 1 + n_prof + n_split
+    script, target = synth.decode_script(SEED, GB, NQ)
     script, target = script[:, b0:b0 + Bl].copy(), target[:, b0:b0 + Bl].copy()
-    gen = torch.Generator(device=dev)
     tgt = torch.from_numpy(target).to(dev)
-    qpool = []
-    for p in range(POOL):
-        row = []
-        for l in range(M):
-            gen.manual_seed(1234 + 7919 * p + 104729 * l)
-            row.append(synth.queries_torch(gen, Cs[l], tgt[p], Hq, G, d)[:, h0:h0 + Hl].contiguous())
-        qpool.append(row)
-    itok = [torch.from_numpy(script[p]).to(dev) for p in range(POOL)]
-    outs = [torch.empty((Bl, Hl, d), dtype=torch.float32, device=dev) for _ in range(M)]
+    gen = torch.Generator(device=dev)
+    qall = torch.empty((NQ, M, Bl, Hl, d), dtype=torch.bfloat16, device=dev)
+    for l in range(M):
+        cl = Cs[l][:, tgt.long(), :]                            # [G][NQ][Bl][d]
+        cl = cl.permute(1, 2, 0, 3).repeat_interleave(Hq // G, dim=2)[:, :, h0:h0 + Hl]  # [NQ][Bl][Hl][d]
+        gen.manual_seed(1234 + 104729 * l + 7919 * rank)
+        qall[:, l] = (cl + torch.randn(cl.shape, generator=gen, device=dev)).to(torch.bfloat16)
+    tall = torch.from_numpy(script).to(dev)                     # [NQ][Bl]
+    qbuf = torch.empty((M, Bl, Hl, d), dtype=torch.bfloat16, device=dev)  # static inputs of the graph
+    tbuf = torch.empty((Bl,), dtype=torch.int32, device=dev)
+    outs = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
     gath = [torch.empty((world, Bl, Hl, d), dtype=torch.float32, device=dev) for _ in range(M)] if world > 1 else None
-    sel_tok = [torch.zeros((Bl, Gl), dtype=torch.int32, device=dev) for _ in range(M)]
+    sel_tok = torch.zeros((M, Bl, Gl), dtype=torch.int32, device=dev)
+    history = []  # script index of every decode step executed on the context, in order
+    nxt = [0]
 
-    def step(p, with_tokens=False):
+    def take():
+        k = nxt[0]
+        nxt[0] += 1
+        history.append(k)
+        return k
+
+    def load(k):
+        qbuf.copy_(qall[k], non_blocking=True)
+        tbuf.copy_(tall[k], non_blocking=True)
+
+    def body(with_tokens=False, split=False):
         for l in range(M):
-            skv.decode_step(l, qpool[p][l], itok[p], outs[l], sel_tokens=sel_tok[l] if with_tokens else None)
+            if split:
+                skv.decode_select(l, qbuf[l], tbuf, sel_tokens=sel_tok[l] if with_tokens else None)
+                skv.decode_attend(l, qbuf[l], outs[l])
+            else:
+                skv.decode_step(l, qbuf[l], tbuf, outs[l], sel_tokens=sel_tok[l] if with_tokens else None)
             if world > 1:  # the one exchange: all-gather of the per-head outputs of the layer
                 parallel.all_gather_outputs(outs[l], plan, gathered=gath[l])
 
@@ -283,11 +349,12 @@ def main():
     cold = None
     if host:
         led0 = sum(skv.host_fetch_bytes(l) for l in range(M))
+        load(take())
+        torch.cuda.synchronize()
         c0 = torch.cuda.Event(enable_timing=True)
         c1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
         c0.record()
-        step(0)
+        body()
         c1.record()
         torch.cuda.synchronize()
         cold_ms = c0.elapsed_time(c1)
@@ -295,59 +362,82 @@ def main():
         cold = {"ms": round(cold_ms, 3), "host_bytes": int(cold_bytes),
                 "host_link_gbs": round(cold_bytes / (cold_ms / 1e3) / 1e9, 2)}
 
-    # eager warm-up, then one CUDA graph per pool step (eager fallback if capture fails)
-    for p in range(POOL):
-        step(p)
+    # eager steps, then ONE CUDA graph of the step over the static input buffers
+    for _ in range(n_eager):
+        load(take())
+        body()
     torch.cuda.synchronize()
-    graphs = []
+    stream = torch.cuda.Stream(device=dev)
+    graph = None
     try:
-        stream = torch.cuda.Stream(device=dev)
         with torch.cuda.stream(stream):
-            for p in range(POOL):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    step(p)
-                graphs.append(g)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                body()
         torch.cuda.synchronize()
     except Exception as e:  # noqa: BLE001 -- report and time the eager step instead
         print(f"[bench] CUDA graph capture failed ({type(e).__name__}: {e}); timing eager steps", file=sys.stderr)
-        graphs = []
+        graph = None
         torch.cuda.synchronize()
 
-    def run(k):
-        if graphs:
-            graphs[k % POOL].replay()
+    def run_step():
+        load(take())
+        if graph is not None:
+            graph.replay()
         else:
-            step(k % POOL)
+            body()
 
-    for w in range(args.warmup):
-        run(w)
+    # warm-up: at least one replay (the graph's upload) before the timed region, whatever --warmup is
+    for _ in range(max(1, args.warmup)):
+        run_step()
     torch.cuda.synchronize()
 
     # ---------------- timed region: K steps (device time, CUDA events, max over ranks)
     ledger0 = sum(skv.host_fetch_bytes(l) for l in range(M)) if host else 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    cur = torch.cuda.current_stream()
     with ClockSampler(local) as clk:
-        cur = torch.cuda.current_stream()
         e0.record(cur)
         for k in range(args.steps):
-            run(k)
+            load(take())
+            ev[k][0].record(cur)
+            if graph is not None:
+                graph.replay()
+            else:
+                body()
+            ev[k][1].record(cur)
         e1.record(cur)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms_total = e0.elapsed_time(e1)
+    step_ms = [a.elapsed_time(b) for a, b in ev]  # the replays alone (without the input copies)
+    kern_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([ms_total], device=dev)
+        t = torch.tensor([ms_total, kern_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total, kern_ms = float(t[0].item()), float(t[1].item())
     ms_step = ms_total / args.steps
     value = GB / (ms_step / 1e3)
     host_step_bytes = (sum(skv.host_fetch_bytes(l) for l in range(M)) - ledger0) / args.steps if host else 0
+
+    # ---------------- end-of-run check: one more step, eager, with its selections; sampled units
+    # against the CPU oracle replaying this context's whole decode history (Eq. 2 state included)
+    chk = None
+    if check:
+        ids_all = torch.empty((len(keep_layers), Bl, Gl, tau), dtype=torch.int32, device=dev)
+        k_last = take()
+        load(k_last)
+        for l in range(M):
+            skv.decode_step(l, qbuf[l], tbuf, outs[l], sel_ids=ids_all[l] if l < len(keep_layers) else None)
+        torch.cuda.synchronize()
+        chk = end_check(cfg, toks, Kh, Vh, keep_layers, history, qall, script, ids_all.cpu().numpy(),
+                        outs.cpu().numpy(), Bl, Gl, Hl)
 
     # ---------------- per-kernel durations (profiled eager pass, events on the launching stream)
     # A spin kernel queued first lets the host enqueue the whole profiled pass ahead of the GPU,
@@ -356,158 +446,183 @@ def main():
     tok_hist = []
     torch.cuda.synchronize()
     torch.cuda._sleep(int(2e9 * 0.05))  # ~50 ms head start
-    for p in range(POOL):
-        step(p, with_tokens=True)
-        tok_hist.append(torch.stack(sel_tok).sum())
+    for _ in range(n_prof):
+        load(take())
+        body(with_tokens=True)
+        tok_hist.append(sel_tok.sum())
     torch.cuda.synchronize()
     ntok_sum = int(torch.stack(tok_hist).sum())
     prof = skv.profile_read()
     skv.set_profiling(False)
     S_tot = sum(S)
-    # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md "Measurement"
-    score_bytes = Gl * S_tot * d * 2 + Bl * Hl * d * (2 + 4) + Gl * S_tot * 4  # E + q,Sq + scores written
-    nlaunch = max(1, prof["step"][1] or prof["fused"][1] or prof["attend"][1])
-    kv_bytes = ntok_sum * d * 2 * 2 / nlaunch  # selected K and V rows
-    sel_bytes = Gl * S_tot * (4 + 4) + Bl * Hl * d * (2 + 4 * 2)  # scores + offsets read, q + Sq
+    # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md section 9
+    kv_bytes = ntok_sum * d * 2 * 2 / max(1, prof["step"][1])  # selected K and V rows per launch
+    e_bytes = Gl * S_tot * d * 2                                 # bf16 sentence embeddings
+    qo_bytes = Bl * Hl * d * (2 + 4 + 4 + 4)                     # q, Sq read + write, O
+    unit_bytes = e_bytes + kv_bytes + Gl * S_tot * 4 * 2 + qo_bytes  # + scores written, offsets read
     kern = {}
-    # one-launch step (decode_unit.cu): E + q/Sq + scores written, offsets read, selected K/V, Sq update, O
-    unit_bytes = score_bytes + Gl * S_tot * 4 + kv_bytes + Bl * Hl * d * (4 + 4)
-    for name, nbytes in (("step", unit_bytes), ("score", score_bytes), ("fused", kv_bytes + sel_bytes + Bl * Hl * d * 4),
-                         ("select", sel_bytes), ("attend", kv_bytes + Bl * Hl * d * (2 + 4))):
-        ms, n = prof[name]
-        if not n:
-            continue
-        avg = ms / n
-        kern[name] = {"avg_us": round(avg * 1e3, 3), "bytes_per_launch": int(nbytes),
-                      "gbs": round(nbytes / (avg / 1e3) / 1e9, 1)}
-    tot_prof = sum(prof[k][0] for k in kern)
-    for name in kern:
-        kern[name]["share"] = round(prof[name][0] / tot_prof, 3)
-    dom = max(kern, key=lambda k: prof[k][0])
-    step_bytes = (score_bytes + sel_bytes + kv_bytes + Bl * Hl * d * 4) * M
+    ms_p, n_p = prof["step"]
+    kern["step"] = {"avg_us_isolated": round(ms_p / max(1, n_p) * 1e3, 3), "bytes_per_launch": int(unit_bytes)}
+    # achieved: algorithmic bytes per launch / average launch duration in the timed region = the
+    # graph replays' device time (CUDA events on the replay stream, input copies excluded) / launches
+    launches_timed = M * args.steps
+    avg_us = kern_ms * 1e3 / launches_timed
+    kern["step"]["avg_us"] = round(avg_us, 3)
+    kern["step"]["gbs"] = round(unit_bytes / (avg_us / 1e6) / 1e9, 1)
+    kern["step"]["share"] = round(kern_ms / ms_total, 4)
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tf):
-        # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from one
-        # `ncu --set full` capture of this workload (scripts/gpu_profile.sh), per residency
+        # dram__bytes_read.sum + dram__bytes_write.sum per launch of the step kernel, from one
+        # `ncu --set full` capture of this workload and residency (scripts/gpu_profile.sh)
         with open(tf) as f:
-            tj = json.load(f)
-        traffic = tj.get(f"{dom}_{residency}", tj.get(dom))
-    # achieved: algorithmic bytes per launch / average launch duration.  When every kernel of the
-    # timed region is the one-launch step kernel (M launches per step, nothing else on the stream),
-    # its average duration in the timed region is ms_step / M (CUDA events on the replay stream);
-    # the isolated per-launch time of the profiled eager pass (no PDL overlap) is kept beside it.
-    in_step = dom == "step" and kern[dom]["share"] == 1.0
-    if in_step:
-        kern[dom]["avg_us_isolated"] = kern[dom]["avg_us"]
-        kern[dom]["gbs_isolated"] = kern[dom]["gbs"]
-        kern[dom]["avg_us"] = round(ms_step * 1e3 / M, 3)
-        kern[dom]["gbs"] = round(kern[dom]["bytes_per_launch"] / (ms_step / M / 1e3) / 1e9, 1)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(kern[dom]["gbs"] / hbm_peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "duration": "timed region / (steps x layers)" if in_step else "profiled eager pass (CUDA events)",
-                "per_unit": "step (one launch per layer): G*S*d*2 B (bf16 E) + sum(ntok)*d*2*2 B (selected K,V rows) "
-                            "+ scores/offsets/q/Sq/O; score: E + q/Sq + scores; attend: selected K,V + q + O; "
-                            "select: scores + offsets + q/Sq"}
+            traffic = json.load(f).get(f"step_{residency}")
+    roofline = {"bound": "hbm", "kernel": "unit_step_kernel (decode_unit.cu)", "achieved": kern["step"]["gbs"],
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(kern["step"]["gbs"] / hbm_peak, 4),
+                "traffic": traffic, "peak_kind": peak_kind,
+                "duration": "graph replays' device time in the timed region / (steps x layers)",
+                "per_unit": "per launch (one layer, all units): G*S*d*2 B (bf16 E) + sum(ntok)*d*2*2 B (selected "
+                            "K,V rows) + G*S*4*2 (scores written, offsets read) + B*Hq*d*14 (q, Sq r/w, O)"}
+
+    # ---------------- the split call pair of SURVEY 8(b): decode_select + decode_attend per layer
+    split = None
+    if not args.no_split:
+        torch.cuda.synchronize()
+        sgraph = None
+        try:
+            load(take())
+            body(split=True)  # eager (first split step: working-set path switch in host residency)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                sgraph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(sgraph, stream=stream):
+                    body(split=True)
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] split-call graph capture failed ({e})", file=sys.stderr)
+            sgraph = None
+        n_sw = max(2, args.warmup)
+        n_st = min(args.steps, 100)
+        for _ in range(n_sw):
+            load(take())
+            sgraph.replay() if sgraph is not None else body(split=True)
+        torch.cuda.synchronize()
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_st)]
+        for k in range(n_st):
+            load(take())
+            sev[k][0].record(cur)
+            sgraph.replay() if sgraph is not None else body(split=True)
+            sev[k][1].record(cur)
+        torch.cuda.synchronize()
+        sms = [a.elapsed_time(b) for a, b in sev]
+        sm = sum(sms) / n_st
+        split = {"calls": "sentencekv_decode_select + sentencekv_decode_attend per layer (score, select, attend "
+                          "kernels)", "steps": n_st, "ms_per_step": round(sm, 5), "value": round(GB / (sm / 1e3), 2),
+                 "unit": "tokens/s", "p50_ms": round(pct(sms, 50), 5), "gpu_launches_per_step": 3 * M,
+                 "cuda_graph": sgraph is not None}
 
     # ---------------- end to end through the public API with host buffers
-    qhost = [torch.stack(qpool[p]).cpu().pin_memory() for p in range(POOL)]  # [M][Bl][Hl][d]
-    thost = [t.cpu().pin_memory() for t in itok]
+    ne = args.e2e_steps
+    k0 = nxt[0] % max(1, NQ - ne)
+    qhost = qall[k0:k0 + ne].cpu().pin_memory()  # fresh queries per step, pinned host memory
+    thost = tall[k0:k0 + ne].cpu().pin_memory()
     ohost = torch.empty((M, Bl, Hl, d), dtype=torch.float32).pin_memory()
     qdev = torch.empty((M, Bl, Hl, d), dtype=torch.bfloat16, device=dev)
     tdev = torch.empty((Bl,), dtype=torch.int32, device=dev)
     odev = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
-
     # each layer's output is read back on a copy stream as soon as its kernel is done, so the
     # device->host read of the step's result overlaps the later layers
     cstream = torch.cuda.Stream(device=dev)
     ev_o = [torch.cuda.Event() for _ in range(M)]
 
-    def e2e_step(p):
-        cur = torch.cuda.current_stream()
-        qdev.copy_(qhost[p], non_blocking=True)
-        tdev.copy_(thost[p], non_blocking=True)
+    def e2e_step(j):
+        c = torch.cuda.current_stream()
+        qdev.copy_(qhost[j], non_blocking=True)
+        tdev.copy_(thost[j], non_blocking=True)
         for l in range(M):
             skvlib.sentencekv_decode_step(skv.ctx, l, qdev[l], tdev, odev[l])
             if world > 1:
                 parallel.all_gather_outputs(odev[l], plan, gathered=gath[l])
-            ev_o[l].record(cur)
+            ev_o[l].record(c)
             with torch.cuda.stream(cstream):
                 cstream.wait_event(ev_o[l])
                 ohost[l].copy_(odev[l], non_blocking=True)
-        cur.synchronize()
+        c.synchronize()
         cstream.synchronize()
 
-    for p in range(3):
-        e2e_step(p)
+    for j in range(min(3, ne)):
+        e2e_step(j)
     if world > 1:
         dist.barrier()
     x0 = torch.cuda.Event(enable_timing=True)
     x1 = torch.cuda.Event(enable_timing=True)
     x0.record()
-    for k in range(args.e2e_steps):
-        e2e_step(k % POOL)
+    for j in range(ne):
+        e2e_step(j)
     x1.record()
     torch.cuda.synchronize()
-    e2e_ms = x0.elapsed_time(x1) / args.e2e_steps
+    e2e_ms = x0.elapsed_time(x1) / ne
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": round(GB / (e2e_ms / 1e3), 2), "unit": "tokens/s", "ms_per_step": round(e2e_ms, 4),
-           "h2d_bytes_per_step": int(qhost[0].numel() * 2 + Bl * 4), "d2h_bytes_per_step": int(ohost.numel() * 4)}
+           "h2d_bytes_per_step": int(qhost[0].numel() * 2 + Bl * 4), "d2h_bytes_per_step": int(ohost.numel() * 4),
+           "call": "sentencekv_decode_step per layer, eager from Python, fresh pinned-host queries each step"}
 
-    # ---------------- CPU oracle baseline (rank 0, N=1 only; bounded sample)
+    # ---------------- CPU oracle baseline (rank 0, N=1 only; bounded sample of full steps)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        layers_sample = [0, 1] if M > 1 else [0]
-        units = [(b, g) for b in range(Bl) for g in range(Gl)]
-        Kh = {l: Ks[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
-        Vh = {l: Vs[l].view(torch.int16).cpu().numpy().view(np.uint16) for l in layers_sample}
-        qs_h = [[qpool[p][l].view(torch.int16).cpu().numpy().view(np.uint16) if l in layers_sample else None
-                 for l in range(M)] for p in range(POOL)]
-        n_steps = 2
-        per_unit, threads = oracle_sample(cfg, toks, Kh, Vh, qs_h, script, units, layers_sample, n_steps)
-        step_s = per_unit * Bl * Gl * M
-        cpu = {"value": round(Bl / step_s, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
+    if cpu_leg:
+        ost = OracleStep(cfg | {"B": Bl}, toks, Kh, Vh)
+        q_np = [qall[k].view(torch.int16).cpu().numpy().view(np.uint16) for k in range(4)]
+        times = time_oracle(ost, q_np, script[:4], 30, budget_s=15.0)
+        step_s = sum(times) / len(times)
+        cpu = {"value": round(Bl / step_s, 4), "unit": "tokens/s", "cores": ost.threads, "kind": "oracle",
                "ms_per_step": round(step_s * 1e3, 1),
-               "sample": f"{n_steps} steps x {len(layers_sample)} of {M} layers x all {Bl * Gl} (b,g) units, "
-                         f"select+attend per unit timed, extrapolated to {M} layers"}
+               "sample": f"{len(times)} full decode steps (all {M} layers x all {Bl * Gl} (b,g) units, select + "
+                         f"attend, units in parallel on {ost.threads} threads); K/V bytes of layers "
+                         f"{keep_layers} reused for the other layers (same shapes, same work)"}
 
     if rank == 0:
+        clocks = clk.summary()
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
             "scaling": "weak" if args.shard == "batch" else "strong", "vs_baseline": None,
             "dtype": "bf16 in / fp32 acc (selection canonical fp32)",
-            "data": "synthetic (seeded token streams with punctuation boundaries, topic-structured K/V/q)",
-            "config": {"workload": args.config, "global_batch": GB, "layers": M, "q_heads": Hq, "kv_heads": G,
-                       "head_dim": d, "context": L, "token_budget": tau, "sentences_rank0": S,
-                       "residency": "pinned host K/V + HBM working set" if host else "device (HBM)",
-                       "parallelism": f"{plan.batch_shards} batch x {plan.head_shards} KV-head shards",
-                       "l2": f"inputs > L2: {step_bytes / 1e9:.2f} GB read per step per GPU (L2 126 MB)",
-                       "cuda_graph": bool(graphs)},
+            "data": "synthetic (seeded token streams with punctuation boundaries, topic-structured K/V/q; fresh "
+                    "queries every step, topic switch after each boundary input)",
+            "config": config_dict(args, cfg, GB),
+            "run": {"sentences_rank0": S, "residency": "pinned host K/V + HBM working set" if host else "device (HBM)",
+                    "parallelism": f"{plan.batch_shards} batch x {plan.head_shards} KV-head shards",
+                    "l2": f"inputs > L2: {(e_bytes + kv_bytes) * M / 1e9:.2f} GB read per step per GPU (L2 126 MB), "
+                          "no flush needed",
+                    "cuda_graph": graph is not None},
+            "step_ms": {"p10": round(pct(step_ms, 10), 5), "p50": round(pct(step_ms, 50), 5),
+                        "p90": round(pct(step_ms, 90), 5), "max": round(max(step_ms), 5),
+                        "note": "per-step graph replay device time (input copy excluded)"},
             "roofline": roofline,
             "kernels": kern,
-            "step_bytes_per_gpu": int(step_bytes),
-            "step_gbs_per_gpu": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
             "e2e": e2e,
-            # kernels of this library per timed step: one unit_step_kernel per layer (decode_unit.cu),
-            # else score + select + attend (or score + fused)
-            "gpu_launches": (M if prof["step"][1] else (3 * M if prof["select"][1] else 2 * M)) * args.steps,
-            "clocks": clk.summary(),
+            "split_calls": split,
+            # kernels of this library per timed step: one unit_step_kernel per layer (decode_unit.cu)
+            "gpu_launches": M * args.steps,
+            "clocks": clocks,
             "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(Bl * Gl * L * d * 2 * M),
                         "segment_ms": round(prof_prefill["segment"][0], 3),
                         "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4),
                         "compress_gbs": round(Bl * Gl * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
             "host_residency": {"host_bytes_per_step": int(host_step_bytes),
-                               "host_link_gbs": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
-                               # P3: D2H copy time on the copy stream (CUDA events); the wall time of the
-                               # prefill loop also holds the one-time pinning of the 64 GiB host store
+                               "host_rows_per_step": round(host_step_bytes / (d * 2 * 2), 1),
+                               "host_link_gbs_in_step": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
+                               # P3: D2H copy time on the copy stream (CUDA events)
                                "offload_gbs_p3": round(kv_bytes_total / (prof_prefill["offload"][0] / 1e3) / 1e9, 2)
                                if prof_prefill["offload"][1] else None,
                                "offload_wall_s_incl_pinning": round(offload_s, 2) if offload_s else None,
-                               "working_set_tokens_per_unit": 2 * tau, "cold_first_step": cold} if host else None,
+                               "page_cache_tokens_per_unit": int(2.0 * tau), "cold_first_step": cold,
+                               "paper_onload": "PAPER.md P:740: onload 1024 tokens 0.0038 s (H100 NVL, per step)"}
+            if host else None,
+            "end_check": chk,
             "cpu_baseline": cpu,
             "kv_gen_s": round(t_gen, 2),
         }
@@ -516,33 +631,71 @@ def main():
         dist.destroy_process_group()
 
 
-def reference_arm(args, cfg, rank, world):
-    """--impl reference: the CPU oracle as it stands, on this arm's config, metric and unit.
-    Each step = a bounded sample (4 (b,g) units of one layer, select + attend), extrapolated to
-    the full step (all units, all layers).  Rank 0 only; other ranks exit without work."""
+def end_check(cfg, toks, Kh, Vh, layers, history, qall, script, ids_g, O_g, Bl, Gl, Hl):
+    """CHECK_UNITS sampled (layer, b, g) units of the last executed step against the CPU oracle: the
+    oracle replays the Eq. 2 query cache of the unit's (layer, b) over the whole decode history of
+    the context, then scores, selects and attends at the last step.  ids bit-exact, O <= 2e-3."""
+    import oracle
+    import synth
+
+    tau, grp, d = cfg["tau"], cfg["Hq"] // cfg["G"], cfg["d"]
+    rng = np.random.default_rng(17)
+    units = sorted({(int(rng.integers(len(layers))), int(rng.integers(Bl)), int(rng.integers(Gl)))
+                    for _ in range(CHECK_UNITS)})
+    bset = set(synth.BOUNDARY_IDS.tolist())
+    worst, ok = 0.0, True
+    for li, b, g in units:
+        l = layers[li]
+        off = oracle.segment(toks[b], synth.BOUNDARY_IDS, tau)
+        E = oracle.embed(Kh[li][b, g], off)
+        Sq = np.zeros((Hl, d), np.float32)
+        cnt = np.zeros(1, np.int32)
+        qs = qall[history, l, b].view(__import__("torch").int16).cpu().numpy().view(np.uint16)  # [steps][Hl][d]
+        for j, k in enumerate(history):
+            qbar = oracle.qs_append_mean(Sq, cnt, qs[j])
+            if j + 1 < len(history) and int(script[k][b]) in bset:
+                oracle.qs_reset(Sq, cnt)
+        sc = oracle.score(oracle.group_query(qbar, grp, g), E)
+        ids, _ = oracle.select(sc, off, tau)
+        n = len(ids)
+        same = bool(np.array_equal(ids_g[li, b, g, :n], ids) and np.all(ids_g[li, b, g, n:] == -1))
+        O = oracle.attend(qs[-1][g * grp:(g + 1) * grp], Kh[li][b, g], Vh[li][b, g], off, ids)
+        err = float(np.max(np.abs(O_g[l, b, g * grp:(g + 1) * grp] - O)))
+        worst = max(worst, err)
+        ok = ok and same and err <= 2e-3
+    return {"units": [list(u) for u in units], "steps_replayed": len(history), "ids_bit_exact_and_O_2e-3": ok,
+            "max_abs_O": worst}
+
+
+def reference_arm(args, cfg, rank, world, residency):
+    """--impl reference: the CPU oracle as it stands (oracle/), on this arm's config, metric and unit.
+    Each step is one FULL decode step (all layers x all (b, g) units, select + attend, units in
+    parallel on every host thread).  Host RAM holds one layer of K/V, so every layer reuses its
+    bytes (same shapes, same work).  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
     import synth
 
     B, M, Hq, G, d, L, tau = (cfg[k] for k in ("B", "M", "Hq", "G", "d", "L", "tau"))
-    toks, topics = synth.prompts(SEED, 1, L, cfg["median"])
-    K, V = synth.kv_layer(SEED, 0, topics, G, d)  # host K/V of one sequence, one layer
-    script, target = synth.decode_script(SEED, 1, 8)
-    units = [(0, g) for g in range(min(4, G))]
-    qs = [[synth.queries(SEED, 0, s, target[s], Hq, G, d)] for s in range(8)]
-    oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], max(1, args.warmup))  # warm-up
-    per_unit, threads = oracle_sample(cfg, toks, {0: K}, {0: V}, qs, script, units, [0], args.steps)
     GB = B * world if args.shard == "batch" else B
-    step_s = per_unit * GB * G * M
+    toks, topics = synth.prompts(SEED, GB, L, cfg["median"])
+    K, V = synth.kv_layer(SEED, 0, topics, G, d)
+    ost = OracleStep(cfg | {"B": GB}, toks, [K], [V])
+    script, target = synth.decode_script(SEED, GB, 8)
+    qsteps = [[synth.queries(SEED, l, s, target[s], Hq, G, d) for l in range(M)] for s in range(8)]
+    time_oracle(ost, qsteps, script, max(1, args.warmup))
+    times = time_oracle(ost, qsteps, script, args.steps)
+    step_s = sum(times) / len(times)
     value = GB / step_s
-    cpu = {"value": round(value, 4), "unit": "tokens/s", "cores": threads, "kind": "oracle",
-           "sample": f"each step: {len(units)} (b,g) units of 1 layer (select+attend), extrapolated to "
-                     f"{GB * G} units x {M} layers"}
+    cpu = {"value": round(value, 4), "unit": "tokens/s", "cores": ost.threads, "kind": "oracle",
+           "sample": f"{len(times)} full decode steps (all {M} layers x all {GB * G} (b,g) units, select + attend); "
+                     f"one layer's K/V bytes reused by every layer (host RAM)"}
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
             "higher_is_better": True, "scaling": "weak" if args.shard == "batch" else "strong",
-            "vs_baseline": None, "dtype": "fp32 canonical / fp64", "data": "synthetic",
-            "config": {"workload": args.config, "global_batch": GB, "context": L, "token_budget": tau},
+            "vs_baseline": None, "dtype": "fp32 canonical selection / fp64 attention", "data": "synthetic",
+            "config": config_dict(args, cfg, GB),
+            "run": {"residency": "host RAM (oracle)", "parallelism": f"{ost.threads} CPU threads"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -15,8 +15,10 @@
  *     _UNSUPPORTED) and leave the context unchanged.  CUDA launch or asynchronous errors are
  *     sticky: returned as SKV_ERR_CUDA by the call that sees them or by sentencekv_sync(), with
  *     text from sentencekv_last_error().
- *   - Decode entry points do no host synchronisation and no allocation, so a whole decode step
- *     (all layers) can be captured into a CUDA graph.
+ *   - Decode entry points do no allocation, so a whole decode step (all layers) can be captured
+ *     into a CUDA graph.  The only host synchronisation on the decode path: in SKV_KV_HOST, the
+ *     FIRST decode call of a layer after its prefill waits (cudaEventSynchronize) for that layer's
+ *     P3 offload copy; run one eager decode step before capturing.
  *   - One context per host thread (single writer).  Contexts are independent.
  *   - Tensor layouts are row-major, innermost dimension last; bf16 = IEEE bfloat16 bits.
  *   - Multi-GPU: each rank creates one context over its shard (kv_head_begin/count,
@@ -50,10 +52,13 @@ typedef enum {
 
 typedef enum {
     SKV_KV_DEVICE = 0, /* K/V stay in HBM, borrowed from the caller (kept until next prefill/destroy) */
-    SKV_KV_HOST = 1    /* P3: full K/V offloaded to ctx-owned pinned, mapped host memory; each
-                          decode step re-reads sentences selected at the previous step from an HBM working
-                          set (2*tau tokens per (sequence, layer, KV head), needs r >= 2) and fetches the
-                          others from host memory over PCIe (D3) */
+    SKV_KV_HOST = 1    /* P3: full K/V offloaded to ctx-owned pinned, mapped host memory.  D3
+                          (P:448): the HBM working set of each (sequence, layer, KV head) holds
+                          floor(r*tau) tokens (needs r >= 2).  sentencekv_decode_step: a page cache of
+                          16-token pages (rows resident in HBM are read there, the others from host
+                          memory over PCIe and written through).  decode_select + decode_attend: the
+                          previous and the current selection (2*tau rows); sentences selected again are
+                          re-read from HBM, the others fetched from host memory. */
 } skv_residency;
 
 typedef struct {
@@ -67,7 +72,8 @@ typedef struct {
     float semantic_factor;   /* r >= 1; host residency needs r >= 2: its HBM working set holds
                                 the previous and the current selection, 2*tau <= floor(r*tau) tokens per
                                 (sequence, layer, KV head) (A19, A20) */
-    int32_t obs_window;      /* N; must be 0 -- observation-window retention is NEXT-1 */
+    int32_t obs_window;      /* N: observation-window size of the importance retention (SURVEY 8(f)
+                                NEXT-1); 0 = no retention (every token of a sentence is kept, reading A6) */
     int32_t residency;       /* skv_residency */
     int32_t device;          /* CUDA device ordinal */
     int32_t kv_head_begin;   /* this rank's KV-head shard [begin, begin+count); 0, G = all */
@@ -112,12 +118,18 @@ skv_status sentencekv_sync(skv_ctx* ctx);
  * boundary_ids  host int32 [n_boundary], 1 <= n_boundary <= 64: the punctuation token-id set
  *               (layer 0 only; ignored for layer > 0)
  * K, V          device bf16 [batch_count][kv_head_count][L][d], contiguous, 16-byte aligned
- * semantic_factor, token_budget  must equal cfg values (checked; the paper's REQUIRE line)
+ * semantic_factor, token_budget  must equal cfg values (checked; the paper's REQUIRE line, Alg. 1
+ *               "Prompt tokens, token budget tau, semantic keeping factor r, observation window
+ *               size N")
+ * q_window      device bf16 [batch_count][N][kv_head_count*grp][d] or NULL: queries of the last
+ *               N = cfg.obs_window prompt tokens (the observation window, Sec. 4.1).  NULL: no
+ *               importance retention (reading A6).  Non-NULL with cfg.obs_window == 0:
+ *               INVALID_ARGUMENT.
  */
 skv_status sentencekv_prefill_compress(skv_ctx* ctx, int32_t layer, const int32_t* token_ids, int32_t L,
                                        const int32_t* boundary_ids, int32_t n_boundary, const void* K,
                                        const void* V, float semantic_factor, int32_t token_budget,
-                                       skv_stream_t stream);
+                                       const void* q_window, skv_stream_t stream);
 
 /*
  * Decode, per layer per step: D1 + D2 (Alg. 1 lines 14-17).
@@ -159,12 +171,12 @@ skv_status sentencekv_decode_attend(skv_ctx* ctx, int32_t layer, const void* q, 
 
 /*
  * Decode, per layer per step: D1 + D2 + D3 + D4 in one call (Alg. 1 lines 14-19).
- * Same results as sentencekv_decode_select followed by sentencekv_decode_attend (same arithmetic,
- * bit-identical selection).  Default: the score, select and attend kernels back to back.  With
- * SKV_FUSED=1 in the environment the selection and the attention run fused in one thread-block
- * cluster per (sequence, KV head), with the K/V runs selected at the previous step prefetched into
- * L2 while the selection is computed (falls back to the unfused kernels when S > 32768 or
- * tau > 8192).
+ * Same selection as sentencekv_decode_select followed by sentencekv_decode_attend (same arithmetic,
+ * bit-identical ids; O within the same tolerance).  Runs as ONE kernel launch per call: a
+ * thread-block cluster of 8 CTAs per (sequence, KV head) scores its sentences, selects, gathers
+ * and attends (decode_unit.cu).  When the prompt exceeds that kernel's capacity (more than 16384
+ * sentences per sequence, or a budget whose selection tables do not fit its shared memory) the
+ * call runs the score, select and attend kernels of the two split calls instead (same results).
  *
  * q, input_token  as in sentencekv_decode_select
  * out             device fp32 [batch_count][kv_head_count*grp][d]
@@ -208,7 +220,7 @@ typedef enum {
     SKV_K_SCORE = 2,   /* D1 */
     SKV_K_SELECT = 3,  /* D2 */
     SKV_K_ATTEND = 4,  /* D3 + D4 */
-    SKV_K_FUSED = 5,   /* D2 + D3 + D4 fused (decode_step, opt-in kernels) */
+    SKV_K_FUSED = 5,   /* reserved (r01 opt-in fused kernels, removed) */
     SKV_K_STEP = 6,    /* D1 + D2 + D3 + D4 in one launch (decode_step, default) */
     SKV_K_OFFLOAD = 7, /* P3: the D2H copies of a layer's K and V on the ctx's copy stream (host residency) */
     SKV_K_COUNT = 8

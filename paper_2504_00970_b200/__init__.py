@@ -62,7 +62,7 @@ def _load():
         "sentencekv_destroy": (i32, [P]),
         "sentencekv_last_error": (ctypes.c_char_p, [P]),
         "sentencekv_sync": (i32, [P]),
-        "sentencekv_prefill_compress": (i32, [P, i32, P, i32, P, i32, P, P, f32, i32, P]),
+        "sentencekv_prefill_compress": (i32, [P, i32, P, i32, P, i32, P, P, f32, i32, P, P]),
         "sentencekv_decode_select": (i32, [P, i32, P, P, P, P, P, P]),
         "sentencekv_decode_attend": (i32, [P, i32, P, P, P]),
         "sentencekv_decode_step": (i32, [P, i32, P, P, P, P, P, P, P]),
@@ -135,7 +135,7 @@ def sentencekv_sync(ctx) -> None:
 
 
 def sentencekv_prefill_compress(ctx, layer, token_ids, L, boundary_ids, K, V, semantic_factor, token_budget,
-                                stream=None) -> None:
+                                q_window=None, stream=None) -> None:
     """P1 (layer 0) + P2 (+ P3 in host residency); see include/sentencekv.h."""
     if boundary_ids is not None:
         ids = (ctypes.c_int32 * len(boundary_ids))(*[int(x) for x in boundary_ids])
@@ -143,7 +143,8 @@ def sentencekv_prefill_compress(ctx, layer, token_ids, L, boundary_ids, K, V, se
     else:
         ids, nb = None, 0
     _check(ctx, lib.sentencekv_prefill_compress(ctx, int(layer), _ptr(token_ids), int(L), ids, nb, _ptr(K), _ptr(V),
-                                                float(semantic_factor), int(token_budget), _stream(stream)))
+                                                float(semantic_factor), int(token_budget), _ptr(q_window),
+                                                _stream(stream)))
 
 
 def sentencekv_decode_select(ctx, layer, q, input_token, sel_ids=None, sel_count=None, sel_tokens=None,
@@ -200,9 +201,10 @@ class SentenceKV:
         except Exception:
             pass
 
-    def prefill_compress(self, layer, K, V, token_ids=None, boundary_ids=None, stream=None):
+    def prefill_compress(self, layer, K, V, token_ids=None, boundary_ids=None, q_window=None, stream=None):
         L = K.shape[2]
-        sentencekv_prefill_compress(self.ctx, layer, token_ids, L, boundary_ids, K, V, self.r, self.tau, stream)
+        sentencekv_prefill_compress(self.ctx, layer, token_ids, L, boundary_ids, K, V, self.r, self.tau, q_window,
+                                    stream)
 
     def decode_select(self, layer, q, input_token, sel_ids=None, sel_count=None, sel_tokens=None, stream=None):
         sentencekv_decode_select(self.ctx, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream)

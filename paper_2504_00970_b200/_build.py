@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build_trace" if os.environ.get("SKV_TRACE", "") == "1" else "build")
 TRACE = os.environ.get("SKV_TRACE", "") == "1"  # phase-timestamp build for kernel studies
 LIB = os.path.join(HERE, "libsentencekv_trace.so" if TRACE else "libsentencekv.so")
-SOURCES = ["prefill.cu", "decode_select.cu", "decode_attend.cu", "decode_attend_mma.cu", "decode_fused.cu", "decode_layer.cu", "decode_unit.cu", "abi.cu"]
+SOURCES = ["prefill.cu", "decode_select.cu", "decode_attend_mma.cu", "decode_unit.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v"] + (

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 
 #include "skv_internal.cuh"
@@ -84,11 +86,6 @@ void free_layer_prompt(skv::LayerState& ls) {
     free_sel(ls.sel);
     dfree(ls.wsK);
     dfree(ls.wsV);
-    dfree(ls.lk_counters);
-    dfree(ls.lk_part_ml);
-    dfree(ls.lk_part_o);
-    dfree(ls.lk_cand);
-    dfree(ls.lk_cand_count);
     dfree(ls.unit_hint);
     dfree(ls.pc_pt);
     dfree(ls.pc_own);
@@ -145,44 +142,21 @@ void prof_end(skv_ctx* c, int kind, cudaEvent_t a, cudaStream_t st) {
 
 }  // namespace
 
-bool skv::layer_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_LAYER");  // opt-in: slower than the three kernels on B200
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-static int layer_group() {
-    static const int gsz = [] {
-        const char* e = getenv("SKV_LAYER_GROUP");
-        return e ? std::max(1, atoi(e)) : 8;
-    }();
-    return gsz;
-}
-
-bool skv::fused_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_FUSED");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-bool skv::pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_PDL");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-bool skv::pdl_step_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
+cudaError_t skv::ensure_smem(const void* func, size_t smem) {
+    // cudaFuncSetAttribute is per device context: remember (device, function) -> bytes set
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{dev, func}];
+    if (smem <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) have = smem;
+    return e;
 }
 
 SKV_API void sentencekv_config_default(skv_config* cfg) {
@@ -265,7 +239,6 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     }
     dfree(c->S_dev);
     dfree(c->bset);
-    dfree(c->lk_items);
     dfree(c->unit_cand);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
@@ -350,14 +323,6 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
             SKV_CUDA(c, dalloc(&ls.pc_own, U * (size_t)cache_slots(c)));
             SKV_CUDA(c, dalloc(&ls.pc_hand, U));
         }
-        const size_t n_att = (size_t)skv::layer_attend_items((int)tau);
-        SKV_CUDA(c, dalloc(&ls.lk_counters, 3 + 3 * U));
-        SKV_CUDA(c, cudaMemset(ls.lk_counters, 0, sizeof(uint32_t) * (3 + 3 * U)));
-        SKV_CUDA(c, dalloc(&ls.lk_part_ml, U * n_att * 16));
-        SKV_CUDA(c, dalloc(&ls.lk_part_o, U * n_att * 8 * d));
-        const size_t nsm = (size_t)c->lk_n_score_max;
-        SKV_CUDA(c, dalloc(&ls.lk_cand, U * nsm * (size_t)skv::layer_item_sentences((int)d)));
-        SKV_CUDA(c, dalloc(&ls.lk_cand_count, U * nsm));
         SKV_CUDA(c, dalloc(&ls.unit_hint, U));
     }
     dfree(c->unit_cand);
@@ -369,7 +334,7 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
 SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const int32_t* token_ids, int32_t L,
                                                const int32_t* boundary_ids, int32_t n_boundary, const void* K,
                                                const void* V, float semantic_factor, int32_t token_budget,
-                                               skv_stream_t stream_) {
+                                               const void* q_window, skv_stream_t stream_) {
     if (!c) return SKV_ERR_INVALID_ARGUMENT;
     if (c->sticky != SKV_OK) return c->sticky;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
@@ -379,6 +344,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "K/V must be non-NULL and 16-byte aligned");
     if (semantic_factor != c->cfg.semantic_factor || token_budget != c->tau)
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "semantic_factor/token_budget differ from the context config");
+    if (q_window != nullptr && c->cfg.obs_window < 1)
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "q_window given but cfg.obs_window (N) is 0");
+    if (q_window != nullptr)
+        return fail(c, SKV_ERR_UNSUPPORTED, "importance retention (q_window, SURVEY 8(f) NEXT-1) is not built yet");
     if (layer == 0) {
         if (!token_ids) return fail(c, SKV_ERR_INVALID_ARGUMENT, "token_ids is NULL");
         if (!boundary_ids || n_boundary < 1 || n_boundary > skv::kMaxBoundary)
@@ -407,26 +376,16 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         SKV_CUDA(c, cudaStreamSynchronize(st));
         int Smax = 1;
         for (int b = 0; b < c->B; ++b) Smax = c->S_host[b] > Smax ? c->S_host[b] : Smax;
-        const int nsm = skv::layer_score_items(c->d, Smax);
-        const bool grow = nsm > c->lk_n_score_max;
-        c->lk_n_score_max = std::max(nsm, c->lk_n_score_max);
-        if (Smax > c->Smax || !c->layer[0].E || grow) {
+        if (Smax > c->Smax || !c->layer[0].E) {
             for (auto& ls : c->layer) free_layer_prompt(ls);
             skv_status s = alloc_prompt_buffers(c, Smax);
             if (s != SKV_OK) return s;
-        }
-        {  // work queue of the per-layer kernel for this prompt's sentence counts
-            const std::vector<int2> items = skv::layer_schedule(c->S_host, c->G, c->d, c->tau, layer_group());
-            dfree(c->lk_items);
-            SKV_CUDA(c, dalloc(&c->lk_items, items.size()));
-            SKV_CUDA(c, cudaMemcpy(c->lk_items, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice));
-            c->lk_n_items = (int)items.size();
         }
         for (auto& ls : c->layer) {
             ls.prefilled = false;
             ls.selected = false;
             // no previous selection (empty slot 0, parity 0): the host gather misses everything at the
-            // first step and the fused kernel's L2 prefetch is empty
+            // first step
             SKV_CUDA(c, cudaMemsetAsync(ls.sel.count, 0, sizeof(int32_t) * 2 * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.sel.parity, 0, sizeof(int32_t) * c->B * c->G, st));
             SKV_CUDA(c, cudaMemsetAsync(ls.Sq, 0, sizeof(float) * c->B * c->Hq * c->d, st));
@@ -483,6 +442,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
     }
     ls.prefilled = true;
     ls.selected = false;
+    c->after_prefill = true;
     return SKV_OK;
 }
 
@@ -528,7 +488,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
     const bool host = c->cfg.residency == SKV_KV_HOST;
-    if (skv::unit_enabled() && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
+    if (skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
         if (host) {
@@ -559,18 +519,10 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.kv = skv::KvSrc{ls.K, ls.V, c->L, 0};
         a.cand = c->unit_cand;
         a.hint = ls.unit_hint;
-        a.prefetch = 1;
-        {
-            // opt-in (SKV_PF_NEXT=1): the next layer's embeddings go to L2 while this layer selects
-            // and merges (a real decoder calls the layers in order).  Measured on B200 (r01): no gain
-            // (0.850 vs 0.854 ms/step) -- the scoring stream does not get faster from L2.
-            static const bool pf_next = [] {
-                const char* e = getenv("SKV_PF_NEXT");
-                return e && e[0] == '1';
-            }();
-            const int nl = layer + 1 < c->cfg.layers ? layer + 1 : 0;
-            a.E_next = (pf_next && nl != layer && c->layer[nl].prefilled) ? c->layer[nl].E : nullptr;
-        }
+        // the step kernel reads prefill outputs (S, offsets, E) before its programmatic-launch wait:
+        // never overlap it with a prefill kernel
+        a.pdl = !c->after_prefill;
+        c->after_prefill = false;
         a.out = out;
         a.out_ids = sel_ids;
         a.out_count = sel_count;
@@ -583,71 +535,11 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         ls.input_token = input_token;
         return SKV_OK;
     }
-    if (skv::layer_enabled() && c->cfg.residency == SKV_KV_DEVICE &&
-        skv::layer_smem_bytes(c->d, c->Smax, c->tau) <= 200 * 1024) {
-        // persistent per-layer kernel: D1-D4 of every unit in one launch
-        skv::LayerArgs a{};
-        a.q = qb;
-        a.input_token = input_token;
-        a.bset = c->bset;
-        a.nb = c->n_bset;
-        a.Sq = ls.Sq;
-        a.cnt = ls.cnt;
-        a.E = ls.E;
-        a.S = c->S_dev;
-        a.off = c->off;
-        a.off_stride = c->off_stride;
-        a.scores = ls.scores;
-        a.sel = ls.sel;
-        a.kv = skv::KvSrc{ls.K, ls.V, c->L, 0};
-        a.out = out;
-        a.out_ids = sel_ids;
-        a.out_count = sel_count;
-        a.out_tokens = sel_tokens;
-        a.items = c->lk_items;
-        a.n_items = c->lk_n_items;
-        a.B = c->B;
-        a.G = c->G;
-        a.Smax = c->Smax;
-        a.tau = c->tau;
-        a.scale_log2 = (float)(1.0 / std::sqrt((double)c->d) * 1.4426950408889634);
-        const int U = c->B * c->G;
-        a.ticket = ls.lk_counters;
-        a.exit_count = ls.lk_counters + 1;
-        a.score_done = ls.lk_counters + 3;
-        a.select_done = ls.lk_counters + 3 + U;
-        a.attend_done = ls.lk_counters + 3 + 2 * U;
-        a.part_ml = ls.lk_part_ml;
-        a.part_o = ls.lk_part_o;
-        a.n_att = skv::layer_attend_items(c->tau);
-        a.cand = ls.lk_cand;
-        a.cand_count = ls.lk_cand_count;
-        a.n_score_max = c->lk_n_score_max;
-        cudaEvent_t pa = prof_begin(c, st);
-        SKV_CUDA(c, skv::launch_layer(a, c->grp, c->d, st));
-        prof_end(c, SKV_K_FUSED, pa, st);
-        c->launches += 1;
-        ls.selected = true;
-        return SKV_OK;
-    }
-    if (!skv::fused_enabled() || c->cfg.residency != SKV_KV_DEVICE ||
-        !skv::fused_supported(c->d, c->grp, c->Smax, c->tau)) {
-        skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
-        if (s != SKV_OK) return s;
-        return sentencekv_decode_attend(c, layer, q, out, stream_);
-    }
-    cudaEvent_t pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
-    prof_end(c, SKV_K_SCORE, pa, st);
-    pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_fused_select_attend(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->grp, c->d,
-                                                c->Smax, c->tau, qb, input_token, c->bset, c->n_bset, ls.Sq, ls.cnt,
-                                                skv::KvSrc{ls.K, ls.V, c->L, 0}, ls.sel, sel_ids, sel_count,
-                                                sel_tokens, out, st));
-    prof_end(c, SKV_K_FUSED, pa, st);
-    c->launches += 2;
-    ls.selected = true;
-    return SKV_OK;
+    // capacity fallback (Smax > 16384 sentences or a selection too large for the step kernel's
+    // shared memory): the score, select and attend kernels of the split calls
+    skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
+    if (s != SKV_OK) return s;
+    return sentencekv_decode_attend(c, layer, q, out, stream_);
 }
 
 SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const void* q, float* out,
@@ -670,20 +562,13 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
             ls.host_ready = true;
         }
         pa = prof_begin(c, st);
-        if (skv::mma_enabled())
-            SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
-                                               true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, st));
-        else
-            SKV_CUDA(c, skv::launch_attend_host(qb, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV, c->B, c->G, c->grp, c->d,
-                                                ls.sel, ls.ledger, qs, out, st));
+        SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
+                                           true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, st));
     } else {
         pa = prof_begin(c, st);
         const skv::KvSrc kv{ls.K, ls.V, c->L, 0};
-        if (skv::mma_enabled())
-            SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, c->L, nullptr, nullptr, false, c->B, c->G,
-                                               c->grp, c->d, ls.sel, nullptr, qs, out, st));
-        else
-            SKV_CUDA(c, skv::launch_attend(qb, kv, c->B, c->G, c->grp, c->d, ls.sel, qs, out, st));
+        SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, c->L, nullptr, nullptr, false, c->B, c->G,
+                                           c->grp, c->d, ls.sel, nullptr, qs, out, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;

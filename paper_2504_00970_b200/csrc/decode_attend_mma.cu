@@ -207,26 +207,10 @@ static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16*
     const size_t rows = ((tiles + kMCL - 1) / kMCL) * kTile;
     const size_t meta = (size_t)(2 * sel.tau + 1) + (HOST ? (size_t)(2 * sel.tau + 1) : 0) + rows;
     const size_t smem = sizeof(MmaSmem<D>) + sizeof(int32_t) * meta;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(attend_mma_kernel<D, GRP, HOST>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(attend_mma_kernel<D, GRP, HOST>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
-    return launch_pdl(attend_mma_kernel<D, GRP, HOST>, grid, dim3(kMT), smem, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel,
+    cudaError_t e = ensure_smem((const void*)attend_mma_kernel<D, GRP, HOST>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl_if(false, attend_mma_kernel<D, GRP, HOST>, grid, dim3(kMT), smem, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel,
                       ledger, qs, out, scale_log2);
-}
-
-bool mma_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_ATTEND");
-        return !(e && e[0] == 'f');  // SKV_ATTEND=fma selects the fp32-FMA attend kernels
-    }();
-    return on;
 }
 
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,

@@ -124,16 +124,9 @@ static cudaError_t launch_score_t(dim3 grid, int chunk, cudaStream_t st, const _
                                   const int32_t* cnt, const __nv_bfloat16* E, const int32_t* S, int G, int Smax,
                                   float* scores) {
     const size_t smem = (size_t)kScStages * kScTileBytes;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(score_kernel<D, GRP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(score_kernel<D, GRP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    return launch_pdl(score_kernel<D, GRP>, grid, dim3(kScThreads), smem, st, q, Sq, cnt, E, S, G, Smax, chunk,
+    cudaError_t e = ensure_smem((const void*)score_kernel<D, GRP>, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl_if(false, score_kernel<D, GRP>, grid, dim3(kScThreads), smem, st, q, Sq, cnt, E, S, G, Smax, chunk,
                       scores);
 }
 
@@ -436,17 +429,12 @@ cudaError_t launch_select(const float* scores, const int32_t* off, int off_strid
     dim3 grid(G, B);
     if (Smax <= kSelSmemCap && tau <= 65535) {
         const size_t smem = (size_t)Smax * 10 + 16;
-        static bool configured = false;
-        if (!configured) {
-            cudaError_t e = cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(kSelSmemCap * 10 + 16));
-            if (e != cudaSuccess) return e;
-            configured = true;
-        }
-        return launch_pdl(select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, Smax,
+        cudaError_t e = ensure_smem((const void*)select_kernel<true>, (size_t)(kSelSmemCap * 10 + 16));
+        if (e != cudaSuccess) return e;
+        return launch_pdl_if(false, select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, Smax,
                           tau, sel, src_gathered, out_ids, out_count, out_tokens);
     }
-    return launch_pdl(select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, Smax, tau,
+    return launch_pdl_if(false, select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, Smax, tau,
                       sel, src_gathered, out_ids, out_count, out_tokens);
 }
 

@@ -7,8 +7,8 @@
 //   1. score (D1; Eq. 2, S = qbar^T kbar P:440-442, Alg. 1 l.14-16): CTA r streams the
 //      embeddings of its contiguous sentence range [r*chunk, (r+1)*chunk) through a TMA bulk-copy
 //      ring (cp.async.bulk + mbarrier, L2 evict-first) and keeps the ordered 32-bit keys in shared
-//      memory.  (Opt-in L2 prefetches -- of the K/V runs selected at the previous step, of the next
-//      layer's E, of this step's selection -- were measured on B200 and did not pay.)
+//      memory.  (L2 prefetches -- of the K/V runs selected at the previous step, of the next layer's
+//      E, of this step's selection -- were measured on B200 in r01 and did not pay.)
 //   2. select (D2; Alg. 1 l.17, readings A13-A15): the budgeted selection is the maximal
 //      prefix of the ranking by key64 = (ordered(score) << 32) | (0xffffffff - s) whose length
 //      fits tau.  Fast path: each CTA lists its sentences at or above a band around the previous
@@ -159,10 +159,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void prefetch_l2_hint(const void* p, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
-                 : "memory");
-}
 
 // bin(k) = (k - lo) * kUBins / span as a 32.32 fixed-point multiply: monotone in k, < kUBins;
 // spans below kUBins map one key per bin.
@@ -217,8 +213,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq, int32_t* __restrict__ cnt,
                  const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
                  int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
-                 int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, int prefetch,
-                 const __nv_bfloat16* __restrict__ E_next, int attend_pf, float* __restrict__ out, int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
+                 int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, float* __restrict__ out,
+                 int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, float scale_log2, int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
@@ -265,6 +261,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     __shared__ Ctl ctl;
     __shared__ const int4* lists[kUC];
     __shared__ int n_need_s, last_slot_s;
+    __shared__ uint32_t inuse[HOST ? kMaxSlots / 32 : 1];  // host residency: slots read by this step
 
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -314,25 +311,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int prev = sel.parity[unit], cur = prev ^ 1;
     const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
     const uint32_t klo = band.x, khi = band.y;
-    // previous step's selected runs of this CTA's share (the L2 prefetch is issued after scoring,
-    // when HBM would otherwise idle during the selection)
-    constexpr int kPf = 4;
-    int pf_src[kPf], pf_len[kPf];
-#pragma unroll
-    for (int k = 0; k < kPf; ++k) pf_len[k] = 0;
-    if (!HOST && prefetch && warp == kUW - 1) {
-        const int pc = *sel.count_of(prev, unit);
-        const int32_t* pt = sel.tok_of(prev, unit);
-        const int32_t* ps = sel.src_of(prev, unit);
-#pragma unroll
-        for (int k = 0; k < kPf; ++k) {
-            const int i = rank + kUC * (lane + 32 * k);
-            if (i < pc) {
-                pf_src[k] = ps[i];
-                pf_len[k] = pt[i + 1] - pt[i];
-            }
-        }
-    }
     if (warp == kUW - 2) {
         // does this step's input token end a sentence (Q_s reset after this step, A11)?
         const int it = input_token[b];
@@ -428,31 +406,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         if (lane == 0 && n > 0) {
             atomicMin(&ctl.lo, mn);
             atomicMax(&ctl.hi, mx);
-        }
-    }
-    if (E_next != nullptr && warp == 0 && n > 0) {
-        // L2 prefetch of the NEXT layer's embeddings of this CTA's sentence range (prefill data, so
-        // independent of this step): HBM would otherwise idle during the selection and the merge, and
-        // the next layer's scoring then streams E from L2.  16 KB pieces, one per lane.
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(E_next + ((size_t)unit * Smax + s0) * D);
-        const uint32_t bytes = (uint32_t)n * D * 2;
-        for (uint32_t o2 = (uint32_t)lane * kUTileBytes; o2 < bytes; o2 += 32u * kUTileBytes)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + o2),
-                         "r"(min((uint32_t)kUTileBytes, bytes - o2))
-                         : "memory");
-    }
-    if (!HOST && prefetch && warp == kUW - 1) {
-        // L2 prefetch of the previous step's selection (a hint: the attention reads whatever is
-        // selected now; selections change little from token to token)
-        const uint64_t pol = policy_evict_last();
-        const size_t ub = (size_t)unit * kv.unit_stride;
-#pragma unroll
-        for (int k = 0; k < kPf; ++k) {
-            const int len = pf_len[k], src = pf_src[k];
-            if (len > 0 && src >= 0 && (long long)src + len <= kv.unit_stride) {
-                prefetch_l2_hint(kv.K + (ub + src) * D, (uint32_t)(len * D * 2), pol);
-                prefetch_l2_hint(kv.V + (ub + src) * D, (uint32_t)(len * D * 2), pol);
-            }
         }
     }
     __syncthreads();
@@ -949,10 +902,20 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
             if (lane == 0) n_need_s = n_need;
         }
+        for (int j = tid; j < kMaxSlots / 32; j += kUT) inuse[j] = 0u;
         __syncthreads();
         const int n_need = n_need_s;
         for (int j = tid; j < n_need; j += kUT) pslot[j] = hc.pt[(size_t)unit * hc.pages + need[j]];
         for (int j = tid; j < hc.slots; j += kUT) ownc[j] = (uint32_t)hc.own[(size_t)unit * hc.slots + j];
+        // slots holding a page of this selection -- ALL its pages, also those past the kNeedCap
+        // pages the plan tracks: such a slot is read by this step and must not be given away
+        for (int i = tid; i < count; i += kUT) {
+            const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
+            for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
+                const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + p];
+                if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
+            }
+        }
         __syncthreads();
         if (warp == 0) {
             // new pages (ascending) -> free slots (clock order from the hand): empty, or holding a page
@@ -979,16 +942,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 int sl = 0;
                 if (t < hc.slots) {
                     sl = (hand + t) % hc.slots;
-                    const int o = (int)ownc[sl];
-                    fr = o < 0;
-                    if (!fr) {  // is page o used by this selection? (need is ascending)
-                        int lo = 0, hi = n_need;
-                        while (lo < hi) {
-                            const int mid = (lo + hi) >> 1;
-                            if (need[mid] < o) lo = mid + 1; else hi = mid;
-                        }
-                        fr = !(lo < n_need && need[lo] == o);
-                    }
+                    fr = (int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, fr);
                 if (fr) {
@@ -1008,21 +962,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         __syncthreads();
     };
-    if (!HOST && attend_pf) {
-        // L2 prefetch of this CTA's gathered rows (one bulk prefetch per sentence run and K / V),
-        // issued before the row table so that the whole share is requested from HBM at once; the
-        // warps' register loads below then mostly hit L2 (a warp holds one tile in registers).
-        const size_t ub = (size_t)unit * kv.unit_stride;
-        for (int i = tid; i < count; i += kUT) {
-            const int a0 = max(sel_tok[i], T0), a1 = min(sel_tok[i + 1], T1);
-            if (a0 < a1) {
-                const size_t row = ub + sel_src[i] + (a0 - sel_tok[i]);
-                const uint32_t bytes = (uint32_t)((a1 - a0) * D * 2);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.K + row * D), "r"(bytes) : "memory");
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.V + row * D), "r"(bytes) : "memory");
-            }
-        }
-    }
     int my_miss = 0;
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
@@ -1230,14 +1169,6 @@ bool unit_supported(int d, int grp, int Smax, int tau, int slots) {
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
 
 
-bool unit_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SKV_UNIT");
-        return !(e && e[0] == '0');  // SKV_UNIT=0 selects the score / select / attend kernels
-    }();
-    return on;
-}
-
 static int band_width() {
     static const int w = [] {
         const char* e = getenv("SKV_BAND_LOG2");  // half-width of the band in ordered-key units (2^19 ~ 6%)
@@ -1247,47 +1178,18 @@ static int band_width() {
     return w;
 }
 
-static bool prefetch_enabled() {
-    // L2 prefetch of the previous selection: opt-in (SKV_PREFETCH=1).  Measured on B200 (r01): the
-    // attention phase does not get faster and the issuing warp delays the first cluster barrier.
-    static const bool on = [] {
-        const char* e = getenv("SKV_PREFETCH");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-static bool attend_prefetch() {
-    // L2 prefetch of the current selection's rows before the attention: opt-in (SKV_ATTEND_PF=1).
-    // Measured on B200 (r01): the attention phase got slower (7.7 vs 6.4 us per CTA, trace).
-    static const bool on = [] {
-        const char* e = getenv("SKV_ATTEND_PF");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
 
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     const size_t smem = unit_smem_bytes(D, a.sel.tau);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(unit_step_kernel<D, GRP, HOST>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(unit_step_kernel<D, GRP, HOST>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST>, smem);
+    if (e != cudaSuccess) return e;
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
-    return launch_pdl_if(pdl_step_enabled(), unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
+    return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
-                      a.cand, a.hint, band_width(), (a.prefetch && prefetch_enabled()) ? 1 : 0, a.E_next, attend_prefetch() ? 1 : 0,
-                      a.out, a.out_ids,
+                      a.cand, a.hint, band_width(), a.out, a.out_ids,
                       a.out_count, a.out_tokens, scale_log2, trace_counter++);
 }
 

@@ -75,12 +75,6 @@ struct LayerState {
     unsigned long long* ledger = nullptr;  // device: host->HBM bytes fetched by the gathers (cumulative)
     cudaEvent_t offload_done = nullptr;    // D2H copies of this layer completed
     bool host_ready = false;
-    // persistent per-layer kernel: work queue + dependency counters + merge workspace
-    uint32_t* lk_counters = nullptr;   // [3 + 3 * units]: ticket, exit_count, pad, score/select/attend done
-    float* lk_part_ml = nullptr;       // [units][n_att][8][2]
-    float* lk_part_o = nullptr;        // [units][n_att][8][d]
-    int4* lk_cand = nullptr;           // [units][n_score_max][NL] local selection candidates
-    int32_t* lk_cand_count = nullptr;  // [units][n_score_max]
     uint2* unit_hint = nullptr;        // [units] one-launch step kernel: band of the selection's crossing point
     int32_t* pc_pt = nullptr;          // host residency, one-launch kernel: page table [units][pages]
     int32_t* pc_own = nullptr;         // [units][slots]
@@ -109,9 +103,6 @@ struct skv_ctx {
     int n_bset = 0;
 
     std::vector<skv::LayerState> layer;
-    int2* lk_items = nullptr;          // device work queue of the per-layer kernel (per prompt)
-    int lk_n_items = 0;
-    int lk_n_score_max = 0;            // SCORE items of the longest sequence (per-layer candidate lists)
     int4* unit_cand = nullptr;         // overflow scratch of the per-unit step kernel's candidate lists
 
     // kernel profiler: (kind, start, stop) event triples awaiting a read
@@ -121,16 +112,15 @@ struct skv_ctx {
     std::vector<cudaEvent_t> ev_pool;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_event = nullptr;
+    bool after_prefill = false;        // a prefill kernel was the last launch of this context
 };
 
 namespace skv {
 
 // Launches `kernel` on `st` with programmatic stream serialization (PDL): the kernel may start
 // while the previous kernel of the stream drains; it calls pdl_wait() before reading any input.
-// pdl_enabled(): the score / select / attend kernels (opt-in, SKV_PDL=1); pdl_step_enabled(): the
-// one-launch step kernel (default on, SKV_PDL=0 turns it off).
-bool pdl_enabled();
-bool pdl_step_enabled();
+// launch_pdl_if(false, ...) launches without the attribute (e.g. right after a prefill kernel
+// whose writes the kernel reads before its pdl_wait()).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                           Args&&... args) {
@@ -146,22 +136,6 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 bl
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
-}
-
 // ---- kernel launchers (each returns the cudaError_t of the launch) ----
 
 // P1: sentence offsets for B prompts.  tokens [B][L]; off [B][Smax_cap+1]; S [B].
@@ -182,84 +156,17 @@ cudaError_t launch_select(const float* scores, const int32_t* off, int off_strid
                           int G, int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids,
                           int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
 
-// D3 + D4 with host residency: selected sentences also selected at the previous step are re-read
-// from the previous HBM working-set slot, the others from the mapped pinned host store (PCIe); the
-// staged rows are written through to the current slot; host bytes are added to *ledger.
-cudaError_t launch_attend_host(const __nv_bfloat16* q, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L,
-                               __nv_bfloat16* wsK, __nv_bfloat16* wsV, int B, int G, int grp, int d, SelBufs sel,
-                               unsigned long long* ledger, QsState qs, float* out, cudaStream_t st);
-
-// D3 + D4: split-K attention over the selected sentences' tokens (device residency).
-cudaError_t launch_attend(const __nv_bfloat16* q, KvSrc kv, int B, int G, int grp, int d, SelBufs sel, QsState qs,
-                          float* out, cudaStream_t st);
-
-int attend_chunk_tokens(int d);
-
-// ---- persistent per-layer kernel (decode_layer.cu): D1-D4 for every unit in one launch ----
-struct LayerArgs {  // kernel parameter of layer_kernel
-    // inputs / state (device residency)
-    const __nv_bfloat16* q;        // [B][Hq][d]
-    const int32_t* input_token;    // [B]
-    const int32_t* bset;
-    int nb;
-    float* Sq;                     // [B][Hq][d]
-    int32_t* cnt;                  // [B][G]
-    const __nv_bfloat16* E;        // [B][G][Smax][d]
-    const int32_t* S;              // [B]
-    const int32_t* off;            // [B][off_stride]
-    int off_stride;
-    float* scores;                 // [B][G][Smax]
-    SelBufs sel;
-    KvSrc kv;
-    float* out;                    // [B][Hq][d]
-    int32_t* out_ids;              // optional [B][G][tau]
-    int32_t* out_count;            // optional [B][G]
-    int32_t* out_tokens;           // optional [B][G]
-    // schedule
-    const int2* items;             // (kind, unit | index << 16)
-    int n_items;
-    int B, G, Smax, tau;
-    float scale_log2;
-    // scratch (zeroed once; every launch returns it to zero)
-    uint32_t* ticket;
-    uint32_t* exit_count;
-    uint32_t* score_done;          // [units]
-    uint32_t* select_done;         // [units]
-    uint32_t* attend_done;         // [units]
-    float* part_ml;                // [units][n_att][8][2]
-    float* part_o;                 // [units][n_att][8][D]
-    int n_att;                     // ATTEND items per unit
-    int4* cand;                    // [units][n_score_max][NL] (id, key, len, -) local candidates
-    int32_t* cand_count;           // [units][n_score_max]
-    int n_score_max;               // SCORE items of the unit with the most sentences
-};
-
-bool layer_enabled();
-int layer_score_items(int d, int S_b);
-int layer_attend_items(int tau);
-int layer_item_sentences(int d);
-std::vector<int2> layer_schedule(const std::vector<int>& S_host, int G, int d, int tau, int group);
-size_t layer_smem_bytes(int d, int Smax, int tau);
-cudaError_t launch_layer(const LayerArgs& a, int grp, int d, cudaStream_t st);
-
-
-// D3 + D4 on tensor cores (mma.sync m16n8k16, decode_attend_mma.cu), both residencies; default
-// (SKV_ATTEND=fma selects the fp32-FMA kernels above).
-bool mma_enabled();
+// D3 + D4 on tensor cores (mma.sync m16n8k16, decode_attend_mma.cu) over the selection of the
+// last launch_select, both residencies.  Host residency: sentences also selected at the previous
+// step are re-read from the previous HBM working-set slot, the others from the mapped pinned host
+// store (PCIe); every row is written through to the current slot; host bytes are added to *ledger.
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
                               SelBufs sel, unsigned long long* ledger, QsState qs, float* out, cudaStream_t st);
 
-// D2 + D3 + D4 fused (one cluster per unit), reading the scores of launch_score.  Opt-in
-// (SKV_FUSED=1): on B200 the cluster-wide selection phases cost more than the separate select
-// kernel (profiles/r01_notes.md).
-bool fused_enabled();
-bool fused_supported(int d, int grp, int Smax, int tau);
-cudaError_t launch_fused_select_attend(const float* scores, const int32_t* off, int off_stride, const int32_t* S,
-                                       int B, int G, int grp, int d, int Smax, int tau, const __nv_bfloat16* q,
-                                       const int32_t* input_token, const int32_t* bset, int nb, float* Sq,
-                                       int32_t* cnt, KvSrc kv, SelBufs sel, int32_t* out_ids, int32_t* out_count,
-                                       int32_t* out_tokens, float* out, cudaStream_t st);
+// Opt-in dynamic shared memory of `func` on the current device (the attribute is per device
+// context; cached per (device, function), thread-safe).
+cudaError_t ensure_smem(const void* func, size_t smem);
 
 // ---- one launch per layer and step (decode_unit.cu): D1-D4 in one cluster per (b, g) unit ----
 // Host residency (P3 + D3): the HBM working set of a unit is a page cache of `slots` pages of
@@ -294,14 +201,12 @@ struct UnitArgs {
     HostCache hc;                  // host residency (hc.Kh == nullptr in device residency)
     int4* cand;                    // [unit_cand_entries] overflow scratch of the candidate lists
     uint2* hint;                   // [units] selection band of the previous step (klo, khi ordered keys)
-    int prefetch;                  // L2 prefetch of the previous step's selection
-    const __nv_bfloat16* E_next;   // nullable: the next layer's E, prefetched into L2 while HBM idles
+    bool pdl;                      // launch with programmatic stream serialization
     float* out;                    // [B][Hq][d]
     int32_t* out_ids;              // optional [B][G][tau]
     int32_t* out_count;            // optional [B][G]
     int32_t* out_tokens;           // optional [B][G]
 };
-bool unit_enabled();
 bool unit_supported(int d, int grp, int Smax, int tau, int slots);
 int unit_page_tokens();
 size_t unit_smem_bytes(int d, int tau);

@@ -81,7 +81,7 @@ def test_null_arguments_are_rejected():
     import paper_2504_00970_b200 as skv
 
     assert skv.lib.sentencekv_create(None, None) == 1
-    assert skv.lib.sentencekv_prefill_compress(None, 0, None, 1, None, 0, None, None, 2.0, 1, None) == 1
+    assert skv.lib.sentencekv_prefill_compress(None, 0, None, 1, None, 0, None, None, 2.0, 1, None, None) == 1
     assert skv.lib.sentencekv_decode_select(None, 0, None, None, None, None, None, None) == 1
     assert skv.lib.sentencekv_decode_attend(None, 0, None, None, None) == 1
     assert skv.lib.sentencekv_destroy(None) == 0

@@ -165,21 +165,6 @@ def test_one_token_sentences_zero_query(cuda_device, L):
     _custom_case(cuda_device, toks, K, V, [q0, q0, q1], np.array([[300], [13], [300]], np.int32), tau, Hq, G, d)
 
 
-def test_unit_step_kernel_off_parity_subprocess(cuda_device):
-    """decode_step with the one-launch step kernel switched off (SKV_UNIT=0: score, select and attend
-    kernels) must pass the same decode_step parity cases."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, SKV_UNIT="0")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
-                        "-k", "(step or ties or all_equal or tau_cap or one_token) and not subprocess"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
 @pytest.mark.parametrize("band_log2", ["0", "12", "30"])
 def test_step_kernel_selection_paths_subprocess(cuda_device, band_log2):
     """The one-launch step kernel ranks either the band around the previous crossing point or, when
@@ -246,22 +231,6 @@ def test_deterministic_run_to_run(cuda_device, mode):
         assert np.array_equal(i1, i2) and np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
 
 
-def test_fused_select_attend_kernel_parity_subprocess(cuda_device):
-    """The opt-in fused select+attend cluster kernel (SKV_FUSED=1, read once per process) must give
-    the same bit-exact selections and 2e-3 outputs: rerun the decode_step parity cases in a child
-    process with the switch on."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, SKV_FUSED="1", SKV_LAYER="0", SKV_UNIT="0")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
-                        "-k", "(step or ties or all_equal or tau_cap or many_one) and not subprocess"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
 # --------------------------------------------------------------------------- host residency (P3 + D3)
 
 
@@ -316,32 +285,20 @@ def test_host_residency_transfer_ledger(cuda_device):
     assert skv.host_fetch_bytes(0) > first
 
 
-def test_fma_attend_kernels_parity_subprocess(cuda_device):
-    """The fp32-FMA attend kernels (SKV_ATTEND=fma; default is the tensor-core kernel) must pass the
-    same parity cases in both residencies."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("mode", ["split", "step"])
+@pytest.mark.parametrize("L,tau,median", [
+    (40000, 4096, 25.0),   # configs[3]'s budget: ~400 pages of 16 rows per selection
+    (12000, 2048, 3.0),    # short sentences: a selection touches ~1000 pages
+])
+def test_host_residency_large_selections(cuda_device, mode, L, tau, median):
+    """Host residency with selections spanning more pages than the step kernel's cache plan tracks
+    (pages past the plan must never be evicted while they are read): selections and
+    outputs equal the oracle over topic switches."""
+    import paper_2504_00970_b200 as skvlib
 
-    env = dict(os.environ, SKV_ATTEND="fma")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
-                        "-k", "(tiny_config or host_residency or ties or tau_cap or many_one) and not subprocess"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
-def test_persistent_layer_kernel_parity_subprocess(cuda_device):
-    """The opt-in persistent per-layer kernel (SKV_LAYER=1; work queue of SCORE / SELECT / ATTEND
-    items with per-unit dependency counters) must reproduce the decode_step parity cases."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, SKV_LAYER="1", SKV_UNIT="0")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
-                        "tests/test_gpu_fullsize.py",
-                        "-k", "(step or ties or all_equal or tau_cap or many_one or config2) and not subprocess"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    B, M, Hq, G, d, steps = 1, 1, 8, 2, 128, 16
+    toks, _, Ks, Vs, qs, script = make_case(21, B, M, Hq, G, d, L, tau, steps, median=median)
+    skv = _skv(B, M, Hq, G, d, L, tau, residency=skvlib.SKV_KV_HOST)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
+    st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
+    assert st["max_abs"] <= ATOL
