@@ -301,7 +301,7 @@ def main():
 
     # ---------------- decode script: one fresh step of queries + input tokens per executed step
     n_cold, n_eager = (1 if host else 0), 2
-    n_split = 0 if args.no_split else max(3, args.warmup) + min(args.steps, 100)
+    n_split = 0 if args.no_split else 1 + max(2, args.warmup) + min(args.steps, 100)  # eager + warm-up + timed
     n_prof = 4
     NQ = n_cold + n_eager + max(1, args.warmup) + args.steps + 1 + n_prof + n_split
     script, target = synth.decode_script(SEED, GB, NQ)
