@@ -44,8 +44,9 @@ typedef enum {
                                      K/V not 16-byte aligned, semantic_factor/token_budget != cfg */
     SKV_ERR_STATE = 2,            /* layer out of range, decode before that layer's prefill, prefill of
                                      layer > 0 before layer 0 of the same prompt */
-    SKV_ERR_UNSUPPORTED = 3,      /* head_dim not in {64, 128}; obs_window != 0 (importance retention
-                                     is not built yet) */
+    SKV_ERR_UNSUPPORTED = 3,      /* head_dim not in {64, 128}; grp not in {1, 2, 4, 8}; obs_window N > 0
+                                     with N * grp not a multiple of 16 or above 256 (the window rows of
+                                     one KV head form the N side of one tensor-core MMA) */
     SKV_ERR_CUDA = 4,             /* CUDA launch / asynchronous failure (sticky; see last_error) */
     SKV_ERR_OUT_OF_MEMORY = 5     /* device or pinned-host allocation failed */
 } skv_status;
@@ -73,7 +74,8 @@ typedef struct {
                                 the previous and the current selection, 2*tau <= floor(r*tau) tokens per
                                 (sequence, layer, KV head) (A19, A20) */
     int32_t obs_window;      /* N: observation-window size of the importance retention (SURVEY 8(f)
-                                NEXT-1); 0 = no retention (every token of a sentence is kept, reading A6) */
+                                NEXT-1, see sentencekv_prefill_compress); 0 = no retention (every token of a
+                                sentence is kept, reading A6) */
     int32_t residency;       /* skv_residency */
     int32_t device;          /* CUDA device ordinal */
     int32_t kv_head_begin;   /* this rank's KV-head shard [begin, begin+count); 0, G = all */
@@ -121,10 +123,25 @@ skv_status sentencekv_sync(skv_ctx* ctx);
  * semantic_factor, token_budget  must equal cfg values (checked; the paper's REQUIRE line, Alg. 1
  *               "Prompt tokens, token budget tau, semantic keeping factor r, observation window
  *               size N")
- * q_window      device bf16 [batch_count][N][kv_head_count*grp][d] or NULL: queries of the last
- *               N = cfg.obs_window prompt tokens (the observation window, Sec. 4.1).  NULL: no
- *               importance retention (reading A6).  Non-NULL with cfg.obs_window == 0:
- *               INVALID_ARGUMENT.
+ * q_window      device bf16 [batch_count][N][kv_head_count*grp][d], 16-byte aligned, or NULL: queries of
+ *               the last N = cfg.obs_window prompt tokens (the observation window, Sec. 4.1).
+ *               cfg.obs_window == 0: must be NULL (no retention, reading A6; non-NULL is
+ *               INVALID_ARGUMENT).  cfg.obs_window = N > 0: required, and L > N (else INVALID_ARGUMENT);
+ *               the layer is prefilled with importance-filtered retention:
+ *                 alpha_j = sum over window tokens w and all query heads h of the softmax, over w's
+ *                   causal prefix, of q_{w,h} . k_j / sqrt(d), for j < L - N (reading A21;
+ *                   two tcgen05 tensor-core passes, fp32 -- within the tolerance of reading A24);
+ *                 the global top m = min(floor(r * tau), L - N) tokens by alpha are retained (ties ->
+ *                   lowest index), the rest discarded;
+ *                 each sentence keeps its retained tokens as a bucket (sentences with none are dropped,
+ *                   reading A25); Eq. 1 runs over the retained tokens only;
+ *                 the retained K/V form a ctx-owned pool in HBM ([B][G][m][d], token order) that every
+ *                 decode call of the layer ranks and attends (the HBM working set of floor(r*tau)
+ *                 tokens holds all of it), and K/V are not borrowed: the caller may free them after
+ *                 sentencekv_sync.  SKV_KV_HOST: P3 offloads the pool, not the full K/V (Alg. 1 l.7,
+ *                 P:580 "Offload a small subset (r*tau) of tokens to CPU").
+ *               Decode outputs (sel_ids) stay the prompt's sentence ids; sel_tokens count retained
+ *               tokens.  Introspection: sentencekv_copy_importance / sentencekv_copy_retained.
  */
 skv_status sentencekv_prefill_compress(skv_ctx* ctx, int32_t layer, const int32_t* token_ids, int32_t L,
                                        const int32_t* boundary_ids, int32_t n_boundary, const void* K,
@@ -208,6 +225,19 @@ skv_status sentencekv_copy_scores(skv_ctx* ctx, int32_t layer, float* scores_out
  * since its prompt's prefill (synchronous).  0 in device residency. */
 skv_status sentencekv_host_fetch_bytes(skv_ctx* ctx, int32_t layer, uint64_t* bytes_out);
 
+/* NEXT-1 retention of `layer` (cfg.obs_window > 0): m = retained tokens per sequence (0 if the layer
+ * has no retention). */
+int32_t sentencekv_retained_tokens(const skv_ctx* ctx, int32_t layer);
+
+/* alpha_out device fp32 [batch_count][L - N]: the token importance of the layer's prefill. */
+skv_status sentencekv_copy_importance(skv_ctx* ctx, int32_t layer, float* alpha_out, skv_stream_t stream);
+
+/* The layer's retained pool (each output nullable, device int32): keep_out [batch_count][m] retained token
+ * indices ascending; off_out [batch_count][m+1] bucket offsets into the pool (row b: off[0..S'_b]);
+ * sid_out [batch_count][m] the prompt sentence id of each bucket; S_out [batch_count] buckets S'_b. */
+skv_status sentencekv_copy_retained(skv_ctx* ctx, int32_t layer, int32_t* keep_out, int32_t* off_out,
+                                    int32_t* sid_out, int32_t* S_out, skv_stream_t stream);
+
 /* Number of CUDA kernel launches this context has enqueued since creation. */
 int64_t sentencekv_launch_count(const skv_ctx* ctx);
 
@@ -220,7 +250,7 @@ typedef enum {
     SKV_K_SCORE = 2,   /* D1 */
     SKV_K_SELECT = 3,  /* D2 */
     SKV_K_ATTEND = 4,  /* D3 + D4 */
-    SKV_K_FUSED = 5,   /* reserved (r01 opt-in fused kernels, removed) */
+    SKV_K_RETAIN = 5,  /* NEXT-1 retention: window importance (2 tcgen05 passes), top-k, pool gather */
     SKV_K_STEP = 6,    /* D1 + D2 + D3 + D4 in one launch (decode_step, default) */
     SKV_K_OFFLOAD = 7, /* P3: the D2H copies of a layer's K and V on the ctx's copy stream (host residency) */
     SKV_K_COUNT = 8

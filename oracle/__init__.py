@@ -60,6 +60,12 @@ def lib():
         L.skvref_select.restype = i32
         L.skvref_attend.argtypes = [P, i32, P, P, i32, P, P, i32, P]
         L.skvref_attend.restype = None
+        L.skvref_window_importance.argtypes = [P, P, i32, i32, i32, i32, i32, P]
+        L.skvref_window_importance.restype = None
+        L.skvref_retain.argtypes = [P, i32, i32, P]
+        L.skvref_retain.restype = i32
+        L.skvref_retained_buckets.argtypes = [P, i32, P, i32, P, P]
+        L.skvref_retained_buckets.restype = i32
         L.skvref_kv_bytes.argtypes = [i64, i64, i64, i64, i64]
         L.skvref_kv_bytes.restype = i64
         L.skvref_f32_to_bf16.argtypes = [f32]
@@ -164,6 +170,45 @@ def full_attend(q_bits, K_bits, V_bits) -> np.ndarray:
     return attend(q_bits, K_bits, V_bits, np.array([0, L], np.int32), np.array([0], np.int32))
 
 
+def window_importance(qw_bits, K_bits) -> np.ndarray:
+    """NEXT-1 token importance: alpha fp64 [L-N] of one sequence from the window queries
+    qw_bits [N][Hq][d] and the keys K_bits [G][L][d] (reading A21)."""
+    qw_bits = _c(qw_bits, np.uint16)
+    K_bits = _c(K_bits, np.uint16)
+    N, Hq, d = qw_bits.shape
+    G, L, _ = K_bits.shape
+    assert L > N >= 1
+    alpha = np.zeros(L - N, dtype=np.float64)
+    lib().skvref_window_importance(_p(qw_bits), _p(K_bits), N, Hq, G, L, d, _p(alpha))
+    return alpha
+
+
+def retain(alpha, k: int) -> np.ndarray:
+    """NEXT-1 global top-k tokens by alpha, ascending indices (int32)."""
+    alpha = _c(alpha, np.float64)
+    keep = np.zeros(max(1, min(int(k), len(alpha))), dtype=np.int32)
+    m = lib().skvref_retain(_p(alpha), len(alpha), int(k), _p(keep))
+    return keep[:m].copy()
+
+
+def retained_buckets(off, keep):
+    """NEXT-1 sentence buckets over the retained pool (reading A25): (off2 [S'+1], sid [S'])."""
+    off = _c(off, np.int32)
+    keep = _c(keep, np.int32)
+    S = len(off) - 1
+    off2 = np.zeros(S + 1, dtype=np.int32)
+    sid = np.zeros(max(1, S), dtype=np.int32)
+    S2 = lib().skvref_retained_buckets(_p(off), S, _p(keep), len(keep), _p(off2), _p(sid))
+    return off2[: S2 + 1].copy(), sid[:S2].copy()
+
+
+def retained_count(r: float, tau: int) -> int:
+    """floor(r * tau) (reading A20), the number of tokens the retention keeps."""
+    import math
+
+    return int(math.floor(float(np.float32(r)) * int(tau)))
+
+
 def kv_bytes(M, H, d, tokens, elem_bytes=2) -> int:
     """App. Cost(t) written out: M*H*(L+t)*d*2*elem_bytes."""
     return int(lib().skvref_kv_bytes(M, H, d, tokens, elem_bytes))
@@ -183,7 +228,8 @@ class Oracle:
     per decode step and layer q bf16 bits [B][Hq][d] and the input token ids [B].
     """
 
-    def __init__(self, tokens, boundary_ids, tau: int, layers: int, q_heads: int, kv_heads: int, d: int):
+    def __init__(self, tokens, boundary_ids, tau: int, layers: int, q_heads: int, kv_heads: int, d: int,
+                 obs_window: int = 0, semantic_factor: float = 2.0):
         self.tokens = np.asarray(tokens, dtype=np.int32)
         self.B = self.tokens.shape[0]
         self.bset = np.asarray(boundary_ids, dtype=np.int32)
@@ -192,16 +238,44 @@ class Oracle:
         self.grp = q_heads // kv_heads
         # P1: segmentation, shared by all layers and heads (Alg. 1 line 2).
         self.off = [segment(self.tokens[b], self.bset, self.tau) for b in range(self.B)]
+        self.N, self.r = int(obs_window), float(semantic_factor)
         self.E = {}  # layer -> list[b][g] of E bits
         self.K = {}
         self.V = {}
+        # NEXT-1 retention (obs_window > 0): per layer, per b: alpha, retained token ids, bucket
+        # offsets over the pool and the sentence id of each bucket; K/V above are then the pools
+        self.alpha, self.keep, self.loff, self.sid = {}, {}, {}, {}
         self.Sq = np.zeros((layers, self.B, q_heads, d), dtype=np.float32)
         self.cnt = np.zeros((layers, self.B), dtype=np.int32)
 
-    def prefill_layer(self, layer: int, K_bits, V_bits):
-        """Alg. 1 lines 3-8 for one layer: Eq. 1 mean keys; K/V kept whole (A6, A19)."""
-        self.K[layer], self.V[layer] = K_bits, V_bits
-        self.E[layer] = [[embed(K_bits[b, g], self.off[b]) for g in range(self.G)] for b in range(self.B)]
+    def offsets(self, layer: int, b: int) -> np.ndarray:
+        """Sentence offsets the decode of (layer, b) ranks: the prompt's, or the retained buckets'."""
+        return self.loff[layer][b] if layer in self.loff else self.off[b]
+
+    def prefill_layer(self, layer: int, K_bits, V_bits, q_window=None):
+        """Alg. 1 lines 3-8 for one layer: Eq. 1 mean keys.  Without a window (reading A6) every
+        token of a sentence is kept (A19); with one (NEXT-1, q_window bf16 bits [B][N][Hq][d]):
+        alpha (line 4), global top-floor(r*tau) retention (line 5), Eq. 1 over the retained tokens
+        of each sentence (line 6), and the retained pool kept for retrieval (line 7)."""
+        if q_window is None:
+            self.K[layer], self.V[layer] = K_bits, V_bits
+            self.E[layer] = [[embed(K_bits[b, g], self.off[b]) for g in range(self.G)] for b in range(self.B)]
+            return
+        k = retained_count(self.r, self.tau)
+        al, kp, lo, sd, Kp, Vp = [], [], [], [], [], []
+        for b in range(self.B):
+            a = window_importance(q_window[b], K_bits[b])
+            keep = retain(a, k)
+            off2, sid = retained_buckets(self.off[b], keep)
+            al.append(a)
+            kp.append(keep)
+            lo.append(off2)
+            sd.append(sid)
+            Kp.append(np.ascontiguousarray(K_bits[b][:, keep]))
+            Vp.append(np.ascontiguousarray(V_bits[b][:, keep]))
+        self.alpha[layer], self.keep[layer], self.loff[layer], self.sid[layer] = al, kp, lo, sd
+        self.K[layer], self.V[layer] = Kp, Vp  # [b] -> [G][m][d]
+        self.E[layer] = [[embed(Kp[b][g], lo[b]) for g in range(self.G)] for b in range(self.B)]
 
     def decode_select(self, layer: int, q_bits, input_token):
         """Alg. 1 lines 14-17: append q_t, qbar (Eq. 2), similarity, budgeted retrieval.
@@ -217,7 +291,7 @@ class Oracle:
             for g in range(self.G):
                 qt = group_query(qbar, self.grp, g)
                 sc = score(qt, self.E[layer][b][g])
-                sel, n = select(sc, self.off[b], self.tau)
+                sel, n = select(sc, self.offsets(layer, b), self.tau)
                 sb.append(sc)
                 ib.append(sel)
                 nb.append(n)
@@ -235,6 +309,6 @@ class Oracle:
             for g in range(self.G):
                 h0 = g * self.grp
                 O[b, h0 : h0 + self.grp] = attend(
-                    q_bits[b, h0 : h0 + self.grp], self.K[layer][b, g], self.V[layer][b, g], self.off[b], ids[b][g]
-                )
+                    q_bits[b, h0 : h0 + self.grp], self.K[layer][b][g], self.V[layer][b][g], self.offsets(layer, b),
+                    ids[b][g])
         return O

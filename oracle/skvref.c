@@ -271,6 +271,120 @@ void skvref_attend(const uint16_t* q, int32_t grp, const uint16_t* K, const uint
     free(z);
 }
 
+/* ------------------------------- NEXT-1: importance-filtered retention (Sec. 4.1) */
+
+/*
+ * Token importance, Sec. 4.1 "Token importance measurement" (Alg. 1 line 4):
+ * the last N prompt tokens are the observation window; every window token attends to the
+ * tokens before it and "for each token i in the preceding positions, we calculate its
+ * importance score alpha_i by summing the attention scores it receives from all tokens in the
+ * observation window, across all the attention heads".
+ * Reading A21: window token w sits at position p = L-N+w and its attention is the softmax of
+ * q_w . k_j / sqrt(d) over its causal prefix j = 0..p (the window tokens before it included,
+ * as in a forward pass); alpha_j sums those probabilities over every window token and every
+ * query head h (KV head h / grp under GQA, reading A9) for the candidates j in [0, L-N).
+ * Evaluated in fp64.
+ *
+ * qw: bf16 bits [N][Hq][d] (window queries); K: bf16 bits [G][L][d] (keys of one sequence,
+ * all KV heads); alpha: fp64 out [L-N].  Requires L > N >= 1.
+ */
+void skvref_window_importance(const uint16_t* qw, const uint16_t* K, int32_t N, int32_t Hq, int32_t G,
+                              int32_t L, int32_t d, double* alpha) {
+    const int32_t grp = Hq / G, n_cand = L - N;
+    double* z = (double*)malloc(sizeof(double) * (size_t)L);
+    double scale = 1.0 / sqrt((double)d);
+    for (int32_t j = 0; j < n_cand; ++j) alpha[j] = 0.0;
+    for (int32_t w = 0; w < N; ++w) {
+        int32_t p = L - N + w; /* position of the window token; it sees keys 0..p */
+        for (int32_t h = 0; h < Hq; ++h) {
+            const uint16_t* q = qw + ((int64_t)w * Hq + h) * d;
+            const uint16_t* Kg = K + (int64_t)(h / grp) * L * d;
+            double zmax = -INFINITY;
+            for (int32_t j = 0; j <= p; ++j) {
+                double acc = 0.0;
+                for (int32_t c = 0; c < d; ++c)
+                    acc += (double)bf16_to_f32(q[c]) * (double)bf16_to_f32(Kg[(int64_t)j * d + c]);
+                z[j] = acc * scale;
+                if (z[j] > zmax) zmax = z[j];
+            }
+            double denom = 0.0;
+            for (int32_t j = 0; j <= p; ++j) {
+                z[j] = exp(z[j] - zmax);
+                denom += z[j];
+            }
+            for (int32_t j = 0; j < n_cand; ++j) alpha[j] += z[j] / denom;
+        }
+    }
+    free(z);
+}
+
+typedef struct {
+    double a;
+    int32_t i;
+} skvref_alpha_idx;
+
+static int cmp_alpha_desc(const void* x, const void* y) {
+    const skvref_alpha_idx* a = (const skvref_alpha_idx*)x;
+    const skvref_alpha_idx* b = (const skvref_alpha_idx*)y;
+    if (a->a > b->a) return -1;
+    if (a->a < b->a) return 1;
+    return (a->i > b->i) - (a->i < b->i); /* ties: lowest token index first */
+}
+
+/*
+ * Token selection, Sec. 4.1 "Token selection within sentence buckets": "we select
+ * the top floor(r*tau) tokens with the highest alpha_i values across all sentence buckets"
+ * (global, App. "Effect of Sentence Length"; Alg. 1 line 5).  Readings: A20
+ * k = floor(r*tau) is computed by the caller; A21 ties -> lowest token index first.
+ *
+ * alpha: [n] (fp64 here; the GPU decides in fp32, reading A24); keep: out, the
+ * retained token indices in ascending order (room for min(k, n)).  Returns min(k, n).
+ */
+int32_t skvref_retain(const double* alpha, int32_t n, int32_t k, int32_t* keep) {
+    int32_t m = k < n ? k : n;
+    if (m <= 0) return 0;
+    skvref_alpha_idx* v = (skvref_alpha_idx*)malloc(sizeof(skvref_alpha_idx) * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        v[i].a = alpha[i];
+        v[i].i = i;
+    }
+    qsort(v, (size_t)n, sizeof(skvref_alpha_idx), cmp_alpha_desc);
+    for (int32_t i = 0; i < m; ++i) keep[i] = v[i].i;
+    qsort(keep, (size_t)m, sizeof(int32_t), cmp_i32_asc);
+    free(v);
+    return m;
+}
+
+/*
+ * Sentence buckets after retention ("S_s contains the indices of retained tokens in
+ * sentence s"; the retained tokens and their K/V are kept, the rest discarded).  The
+ * retained tokens form a pool in token order; sentence s owns the pool range of its retained
+ * tokens.  Reading A25: a sentence with no retained token has nothing to embed or retrieve and
+ * is dropped from the ranking.
+ *
+ * off: [S+1] sentence offsets of the prompt; keep: [m] ascending retained token indices;
+ * off2: out [S'+1] pool offsets of the surviving sentences; sid: out [S'] their sentence ids
+ * (room for S).  Returns S'.
+ */
+int32_t skvref_retained_buckets(const int32_t* off, int32_t S, const int32_t* keep, int32_t m, int32_t* off2,
+                                int32_t* sid) {
+    int32_t S2 = 0, pos = 0;
+    off2[0] = 0;
+    for (int32_t s = 0; s < S; ++s) {
+        int32_t c = 0;
+        while (pos < m && keep[pos] < off[s + 1]) {
+            if (keep[pos] >= off[s]) c += 1;
+            pos += 1;
+        }
+        if (c > 0) {
+            sid[S2] = s;
+            off2[S2 + 1] = off2[S2] + c;
+            S2 += 1;
+        }
+    }
+    return S2;
+}
+
 /* ------------------------------------------------------------ accounting */
 
 /*

@@ -75,6 +75,9 @@ def _load():
         "sentencekv_set_profiling": (i32, [P, i32]),
         "sentencekv_host_fetch_bytes": (i32, [P, i32, P]),
         "sentencekv_profile_read": (i32, [P, P, P]),
+        "sentencekv_retained_tokens": (i32, [P, i32]),
+        "sentencekv_copy_importance": (i32, [P, i32, P, P]),
+        "sentencekv_copy_retained": (i32, [P, i32, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -174,12 +177,13 @@ class SentenceKV:
 
     def __init__(self, batch, layers, q_heads, kv_heads, head_dim, max_context, token_budget,
                  semantic_factor=2.0, residency=SKV_KV_DEVICE, device=0, kv_head_begin=0, kv_head_count=0,
-                 batch_begin=0, batch_count=0):
+                 batch_begin=0, batch_count=0, obs_window=0):
         self.cfg = sentencekv_config_default(
             batch=batch, layers=layers, q_heads=q_heads, kv_heads=kv_heads, head_dim=head_dim,
             max_context=max_context, token_budget=token_budget, semantic_factor=semantic_factor,
             residency=residency, device=device, kv_head_begin=kv_head_begin, kv_head_count=kv_head_count,
-            batch_begin=batch_begin, batch_count=batch_count)
+            batch_begin=batch_begin, batch_count=batch_count, obs_window=obs_window)
+        self.N = obs_window
         self.ctx = sentencekv_create(self.cfg)
         self.B = batch_count or (batch - batch_begin)
         self.G = kv_head_count or (kv_heads - kv_head_begin)
@@ -254,7 +258,28 @@ class SentenceKV:
     def launch_count(self) -> int:
         return int(lib.sentencekv_launch_count(self.ctx))
 
-    KERNELS = ("segment", "compress", "score", "select", "attend", "fused", "step", "offload")
+    # NEXT-1 retention (obs_window > 0)
+    def retained_tokens(self, layer) -> int:
+        return int(lib.sentencekv_retained_tokens(self.ctx, int(layer)))
+
+    def importance(self, layer, L, stream=None):
+        """alpha fp32 [B][L - N] of the layer's prefill."""
+        out = torch.empty((self.B, L - self.N), dtype=torch.float32, device=self.device)
+        _check(self.ctx, lib.sentencekv_copy_importance(self.ctx, int(layer), _ptr(out), _stream(stream)))
+        return out
+
+    def retained(self, layer, stream=None):
+        """(keep [B][m] token ids, bucket offsets [B][m+1], bucket sentence ids [B][m], buckets [B])."""
+        m = self.retained_tokens(layer)
+        keep = torch.empty((self.B, m), dtype=torch.int32, device=self.device)
+        off = torch.empty((self.B, m + 1), dtype=torch.int32, device=self.device)
+        sid = torch.empty((self.B, m), dtype=torch.int32, device=self.device)
+        S = torch.empty((self.B,), dtype=torch.int32, device=self.device)
+        _check(self.ctx, lib.sentencekv_copy_retained(self.ctx, int(layer), _ptr(keep), _ptr(off), _ptr(sid), _ptr(S),
+                                                      _stream(stream)))
+        return keep, off, sid, S
+
+    KERNELS = ("segment", "compress", "score", "select", "attend", "retain", "step", "offload")
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))

@@ -8,14 +8,18 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build_trace" if os.environ.get("SKV_TRACE", "") == "1" else "build")
 TRACE = os.environ.get("SKV_TRACE", "") == "1"  # phase-timestamp build for kernel studies
-LIB = os.path.join(HERE, "libsentencekv_trace.so" if TRACE else "libsentencekv.so")
-SOURCES = ["prefill.cu", "decode_select.cu", "decode_attend_mma.cu", "decode_unit.cu", "abi.cu"]
+# A/B experiments: SKV_VARIANT=<name> SKV_DEFS="-DX=1 ..." builds libsentencekv_<name>.so beside the
+# product library (selected at run time with SKV_LIB); never the product path
+VARIANT = os.environ.get("SKV_VARIANT", "trace" if TRACE else "")
+DEFS = os.environ.get("SKV_DEFS", "").split()
+BUILD = os.path.join(HERE, f"build_{VARIANT}" if VARIANT else "build")
+LIB = os.path.join(HERE, f"libsentencekv_{VARIANT}.so" if VARIANT else "libsentencekv.so")
+SOURCES = ["prefill.cu", "retain.cu", "decode_select.cu", "decode_attend_mma.cu", "decode_unit.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v"] + (
-    ["-DSKV_TRACE"] if TRACE else [])
+    ["-DSKV_TRACE"] if TRACE else []) + DEFS
 
 
 def _stale() -> bool:

@@ -92,6 +92,19 @@ void free_layer_prompt(skv::LayerState& ls) {
     dfree(ls.pc_hand);
 }
 
+void free_retention(skv::LayerState& ls) {
+    dfree(ls.PK);
+    dfree(ls.PV);
+    dfree(ls.alpha);
+    dfree(ls.keep);
+    dfree(ls.roff);
+    dfree(ls.rsid);
+    dfree(ls.rS);
+    ls.ret_bytes = 0;
+    ls.retained = false;
+    ls.ret_m = 0;
+}
+
 void free_host_store(skv::LayerState& ls) {
     if (ls.Kh) cudaFreeHost(ls.Kh);
     if (ls.Vh) cudaFreeHost(ls.Vh);
@@ -180,8 +193,9 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         cfg.batch_begin < 0 || cfg.batch_count < 1 || cfg.batch_begin + cfg.batch_count > cfg.batch)
         return SKV_ERR_INVALID_ARGUMENT;
     const int grp = cfg.q_heads / cfg.kv_heads;
+    if (cfg.obs_window < 0) return SKV_ERR_INVALID_ARGUMENT;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
-        cfg.obs_window != 0)
+        (cfg.obs_window > 0 && !skv::retain_supported(cfg.head_dim, cfg.obs_window, grp)))
         return SKV_ERR_UNSUPPORTED;
     // host residency keeps the previous and the current selection in HBM: 2*tau <= floor(r*tau)
     if (cfg.residency == SKV_KV_HOST && !(cfg.semantic_factor >= 2.0f)) return SKV_ERR_INVALID_ARGUMENT;
@@ -235,11 +249,13 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
         dfree(ls.cnt);
         dfree(ls.ledger);
         free_host_store(ls);
+        free_retention(ls);
         if (ls.offload_done) cudaEventDestroy(ls.offload_done);
     }
     dfree(c->S_dev);
     dfree(c->bset);
     dfree(c->unit_cand);
+    dfree(c->ret_scratch);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -267,6 +283,24 @@ SKV_API skv_status sentencekv_sync(skv_ctx* c) {
 static int cache_slots(const skv_ctx* c) {
     const long long cap = (long long)std::floor((double)c->cfg.semantic_factor * (double)c->tau);
     return (int)std::max(1LL, cap / skv::unit_page_tokens());
+}
+
+// What the decode of a layer ranks and attends: the prompt's sentences over the context K/V, or
+// (NEXT-1 retention) the retained buckets over the layer's HBM pool.
+struct LayerView {
+    const int32_t* off;
+    int off_stride;
+    const int32_t* S;
+    const __nv_bfloat16* K;
+    const __nv_bfloat16* V;
+    long long stride;      // K/V rows per (b, g) unit
+    const int32_t* sid;    // bucket -> sentence id (retention), else nullptr
+    int sid_stride;
+    bool host;             // rows come from the host store through the HBM working set
+};
+static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
+    if (ls.retained) return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false};
+    return {c->off, c->off_stride, c->S_dev, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST};
 }
 
 // Empties the page cache of a layer (every page -> host).
@@ -344,10 +378,12 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "K/V must be non-NULL and 16-byte aligned");
     if (semantic_factor != c->cfg.semantic_factor || token_budget != c->tau)
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "semantic_factor/token_budget differ from the context config");
-    if (q_window != nullptr && c->cfg.obs_window < 1)
+    const int N = c->cfg.obs_window;
+    if (q_window != nullptr && N < 1)
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "q_window given but cfg.obs_window (N) is 0");
-    if (q_window != nullptr)
-        return fail(c, SKV_ERR_UNSUPPORTED, "importance retention (q_window, SURVEY 8(f) NEXT-1) is not built yet");
+    if (N > 0 && (q_window == nullptr || !aligned16(q_window)))
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "cfg.obs_window = %d needs the window queries (16-byte aligned)", N);
+    if (N > 0 && L <= N) return fail(c, SKV_ERR_INVALID_ARGUMENT, "L=%d must exceed the observation window N=%d", L, N);
     if (layer == 0) {
         if (!token_ids) return fail(c, SKV_ERR_INVALID_ARGUMENT, "token_ids is NULL");
         if (!boundary_ids || n_boundary < 1 || n_boundary > skv::kMaxBoundary)
@@ -400,17 +436,65 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         }
     }
 
-    // ---- P2: Eq. 1 sentence embeddings of this layer ----
     skv::LayerState& ls = c->layer[layer];
     const auto* Kb = static_cast<const __nv_bfloat16*>(K);
     const auto* Vb = static_cast<const __nv_bfloat16*>(V);
-    cudaEvent_t pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
-    prof_end(c, SKV_K_COMPRESS, pa, st);
-    c->launches += 1;
-    if (c->cfg.residency == SKV_KV_HOST) {
-        // P3: full K/V of this layer -> ctx-owned pinned, mapped host memory, on the copy stream
-        const size_t bytes = sizeof(__nv_bfloat16) * (size_t)c->B * c->G * L * c->d;
+    const bool host = c->cfg.residency == SKV_KV_HOST;
+    size_t store_elems = (size_t)c->B * c->G * L * c->d;  // P3: what goes to the host store
+    const __nv_bfloat16 *srcK = Kb, *srcV = Vb;
+    if (N > 0) {
+        // ---- NEXT-1: alpha, global top-floor(r*tau), retained pool + buckets (retain.cu), then Eq. 1
+        // over the retained tokens of every sentence (Alg. 1 lines 4-7)
+        const long long k = (long long)std::floor((double)c->cfg.semantic_factor * (double)c->tau);
+        const int m = (int)std::min<long long>(k, (long long)(L - N));
+        const size_t key = ((size_t)m << 32) ^ (size_t)(L - N);
+        if (ls.ret_bytes != key || !ls.PK) {
+            free_retention(ls);
+            const size_t U = (size_t)c->B * c->G;
+            SKV_CUDA(c, dalloc(&ls.PK, U * m * c->d));
+            SKV_CUDA(c, dalloc(&ls.PV, U * m * c->d));
+            SKV_CUDA(c, dalloc(&ls.alpha, (size_t)c->B * (L - N)));
+            SKV_CUDA(c, dalloc(&ls.keep, (size_t)c->B * m));
+            SKV_CUDA(c, dalloc(&ls.roff, (size_t)c->B * (m + 1)));
+            SKV_CUDA(c, dalloc(&ls.rsid, (size_t)c->B * m));
+            SKV_CUDA(c, dalloc(&ls.rS, (size_t)c->B));
+            ls.ret_bytes = key;
+        }
+        const size_t need = skv::retain_scratch_floats(c->B, c->G, L, N, c->grp);
+        if (c->ret_scratch_n < need) {
+            dfree(c->ret_scratch);
+            c->ret_scratch_n = 0;
+            SKV_CUDA(c, dalloc(&c->ret_scratch, need));
+            c->ret_scratch_n = need;
+        }
+        skv::RetainArgs ra{static_cast<const __nv_bfloat16*>(q_window), Kb, Vb, c->B, c->G, c->grp, c->d, L, N, m,
+                           c->off, c->off_stride, c->S_dev, ls.alpha, c->ret_scratch, ls.keep, ls.roff, ls.rsid, ls.rS,
+                           ls.PK, ls.PV};
+        cudaEvent_t pr = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_retain(ra, st));
+        prof_end(c, SKV_K_RETAIN, pr, st);
+        c->launches += 5;
+        cudaEvent_t pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_compress(ls.PK, c->B, c->G, m, c->d, ls.roff, m + 1, ls.rS, c->Smax, ls.E, st));
+        prof_end(c, SKV_K_COMPRESS, pa, st);
+        c->launches += 1;
+        ls.retained = true;
+        ls.ret_m = m;
+        store_elems = (size_t)c->B * c->G * m * c->d;  // the paper offloads the retained tokens (Alg. 1 l.7)
+        srcK = ls.PK;
+        srcV = ls.PV;
+    } else {
+        // ---- P2: Eq. 1 sentence embeddings of this layer ----
+        cudaEvent_t pa = prof_begin(c, st);
+        SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
+        prof_end(c, SKV_K_COMPRESS, pa, st);
+        c->launches += 1;
+        ls.retained = false;
+    }
+    if (host) {
+        // P3: this layer's K/V (full, or the retained pool) -> ctx-owned pinned, mapped host memory, on
+        // the copy stream
+        const size_t bytes = sizeof(__nv_bfloat16) * store_elems;
         if (ls.host_bytes != bytes) {
             free_host_store(ls);
             void *hk = nullptr, *hv = nullptr;
@@ -428,14 +512,16 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         SKV_CUDA(c, cudaEventRecord(c->copy_event, st));
         SKV_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->copy_event, 0));
         cudaEvent_t po = prof_begin(c, c->copy_stream);
-        SKV_CUDA(c, cudaMemcpyAsync(ls.Kh, Kb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
-        SKV_CUDA(c, cudaMemcpyAsync(ls.Vh, Vb, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.Kh, srcK, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.Vh, srcV, bytes, cudaMemcpyDeviceToHost, c->copy_stream));
         prof_end(c, SKV_K_OFFLOAD, po, c->copy_stream);
         SKV_CUDA(c, cudaEventRecord(ls.offload_done, c->copy_stream));
         ls.host_ready = false;
         ls.K = ls.V = nullptr;  // the caller may free its K/V after sentencekv_sync
         if (layer == 0)
             for (auto& l2 : c->layer) SKV_CUDA(c, cudaMemsetAsync(l2.ledger, 0, sizeof(unsigned long long), st));
+    } else if (N > 0) {
+        ls.K = ls.V = nullptr;  // the ctx keeps its own pool
     } else {
         ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
         ls.V = Vb;
@@ -458,16 +544,17 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
-    {
+    const LayerView v = layer_view(c, ls);
+    if (v.host) {
         skv_status ps = switch_host_path(c, ls, 2, st);
         if (ps != SKV_OK) return ps;
     }
     cudaEvent_t pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, c->S_dev, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
+    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, v.S, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
     prof_end(c, SKV_K_SCORE, pa, st);
     pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_select(ls.scores, c->off, c->off_stride, c->S_dev, c->B, c->G, c->Smax, c->tau, ls.sel,
-                                   false, sel_ids, sel_count, sel_tokens, st));
+    SKV_CUDA(c, skv::launch_select(ls.scores, v.off, v.off_stride, v.S, c->B, c->G, c->Smax, c->tau, ls.sel, false,
+                                   sel_ids, sel_count, sel_tokens, v.sid, v.sid_stride, st));
     prof_end(c, SKV_K_SELECT, pa, st);
     c->launches += 2;
     ls.selected = true;
@@ -487,7 +574,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
-    const bool host = c->cfg.residency == SKV_KV_HOST;
+    const LayerView v = layer_view(c, ls);
+    const bool host = v.host;
     if (skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
@@ -508,15 +596,17 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.Sq = ls.Sq;
         a.cnt = ls.cnt;
         a.E = ls.E;
-        a.S = c->S_dev;
-        a.off = c->off;
-        a.off_stride = c->off_stride;
+        a.S = v.S;
+        a.off = v.off;
+        a.off_stride = v.off_stride;
+        a.sid = v.sid;
+        a.sid_stride = v.sid_stride;
         a.B = c->B;
         a.G = c->G;
         a.Smax = c->Smax;
         a.scores = ls.scores;
         a.sel = ls.sel;
-        a.kv = skv::KvSrc{ls.K, ls.V, c->L, 0};
+        a.kv = skv::KvSrc{v.K, v.V, v.stride, 0};
         a.cand = c->unit_cand;
         a.hint = ls.unit_hint;
         // the step kernel reads prefill outputs (S, offsets, E) before its programmatic-launch wait:
@@ -555,8 +645,9 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
     DeviceGuard dg(c->cfg.device);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
     const skv::QsState qs{ls.input_token, c->bset, c->n_bset, ls.Sq, ls.cnt};
+    const LayerView v = layer_view(c, ls);
     cudaEvent_t pa = nullptr;
-    if (c->cfg.residency == SKV_KV_HOST) {
+    if (v.host) {
         if (!ls.host_ready) {  // first decode of the layer after its prefill: the offload must be done
             SKV_CUDA(c, cudaEventSynchronize(ls.offload_done));
             ls.host_ready = true;
@@ -566,8 +657,8 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
                                            true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, st));
     } else {
         pa = prof_begin(c, st);
-        const skv::KvSrc kv{ls.K, ls.V, c->L, 0};
-        SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, c->L, nullptr, nullptr, false, c->B, c->G,
+        const skv::KvSrc kv{v.K, v.V, v.stride, 0};
+        SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, (int)v.stride, nullptr, nullptr, false, c->B, c->G,
                                            c->grp, c->d, ls.sel, nullptr, qs, out, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
@@ -615,6 +706,37 @@ SKV_API skv_status sentencekv_copy_scores(skv_ctx* c, int32_t layer, float* out,
 }
 
 SKV_API int64_t sentencekv_launch_count(const skv_ctx* c) { return c ? c->launches : 0; }
+
+SKV_API int32_t sentencekv_retained_tokens(const skv_ctx* c, int32_t layer) {
+    if (!c || layer < 0 || layer >= c->cfg.layers || !c->layer[layer].retained) return 0;
+    return c->layer[layer].ret_m;
+}
+
+SKV_API skv_status sentencekv_copy_importance(skv_ctx* c, int32_t layer, float* alpha_out, skv_stream_t stream_) {
+    if (!c || !alpha_out) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers || !c->layer[layer].retained)
+        return fail(c, SKV_ERR_STATE, "layer %d has no retention", layer);
+    DeviceGuard dg(c->cfg.device);
+    SKV_CUDA(c, cudaMemcpyAsync(alpha_out, c->layer[layer].alpha, sizeof(float) * c->B * (c->L - c->cfg.obs_window),
+                                cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream_)));
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_copy_retained(skv_ctx* c, int32_t layer, int32_t* keep_out, int32_t* off_out,
+                                            int32_t* sid_out, int32_t* S_out, skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers || !c->layer[layer].retained)
+        return fail(c, SKV_ERR_STATE, "layer %d has no retention", layer);
+    DeviceGuard dg(c->cfg.device);
+    const skv::LayerState& ls = c->layer[layer];
+    const size_t m = ls.ret_m;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    if (keep_out) SKV_CUDA(c, cudaMemcpyAsync(keep_out, ls.keep, sizeof(int32_t) * c->B * m, cudaMemcpyDeviceToDevice, st));
+    if (off_out) SKV_CUDA(c, cudaMemcpyAsync(off_out, ls.roff, sizeof(int32_t) * c->B * (m + 1), cudaMemcpyDeviceToDevice, st));
+    if (sid_out) SKV_CUDA(c, cudaMemcpyAsync(sid_out, ls.rsid, sizeof(int32_t) * c->B * m, cudaMemcpyDeviceToDevice, st));
+    if (S_out) SKV_CUDA(c, cudaMemcpyAsync(S_out, ls.rS, sizeof(int32_t) * c->B, cudaMemcpyDeviceToDevice, st));
+    return SKV_OK;
+}
 
 SKV_API skv_status sentencekv_host_fetch_bytes(skv_ctx* c, int32_t layer, uint64_t* bytes_out) {
     if (!c || !bytes_out) return SKV_ERR_INVALID_ARGUMENT;

@@ -197,7 +197,8 @@ template <bool SMEM>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(
     const float* __restrict__ scores, const int32_t* __restrict__ off, int off_stride,
     const int32_t* __restrict__ S, int G, int Smax, int tau, SelBufs sel, bool src_gathered,
-    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens) {
+    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count, int32_t* __restrict__ out_tokens,
+    const int32_t* __restrict__ sid, int sid_stride) {
     __shared__ uint32_t hist[kBins];  // length-weighted histogram
     __shared__ unsigned long long cand_key[kCandCap];
     __shared__ uint32_t cand_len[kCandCap];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
                 ids[pos] = s;
                 tokoff[pos] = (int32_t)toff;
                 src[pos] = src_gathered ? (int32_t)toff : off_of(s);
-                if (out_ids) out_ids[(size_t)(b * G + g) * tau + pos] = s;
+                if (out_ids) out_ids[(size_t)(b * G + g) * tau + pos] = sid ? sid[(size_t)b * sid_stride + s] : s;
                 ++pos;
                 toff += len_of(s);
             }
@@ -425,17 +426,18 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(
 
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
                           int G, int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids,
-                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st) {
+                          int32_t* out_count, int32_t* out_tokens, const int32_t* sid, int sid_stride,
+                          cudaStream_t st) {
     dim3 grid(G, B);
     if (Smax <= kSelSmemCap && tau <= 65535) {
         const size_t smem = (size_t)Smax * 10 + 16;
         cudaError_t e = ensure_smem((const void*)select_kernel<true>, (size_t)(kSelSmemCap * 10 + 16));
         if (e != cudaSuccess) return e;
         return launch_pdl_if(false, select_kernel<true>, grid, dim3(kSelThreads), smem, st, scores, off, off_stride, S, G, Smax,
-                          tau, sel, src_gathered, out_ids, out_count, out_tokens);
+                          tau, sel, src_gathered, out_ids, out_count, out_tokens, sid, sid_stride);
     }
     return launch_pdl_if(false, select_kernel<false>, grid, dim3(kSelThreads), 0, st, scores, off, off_stride, S, G, Smax, tau,
-                      sel, src_gathered, out_ids, out_count, out_tokens);
+                      sel, src_gathered, out_ids, out_count, out_tokens, sid, sid_stride);
 }
 
 }  // namespace skv

@@ -52,7 +52,7 @@ namespace skv {
 SKV_TRACE_DEFINE(unit)
 #ifdef SKV_TRACE
 // per CTA (unit * kUC + rank < 1024): SM id + globaltimer (ns) at the phase boundaries
-__device__ unsigned long long g_unit_t[1024][24];
+__device__ unsigned long long g_unit_t[1024][32];
 extern "C" __attribute__((visibility("default"))) int sentencekv_debug_unit(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_unit_t, sizeof(g_unit_t));
 }
@@ -85,6 +85,7 @@ __device__ __forceinline__ void unit_stamp(int cta, int ph) {
             unsigned int sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             g_unit_t[cta][23] = sm;
+            g_unit_t[cta][24] = 0;
         }
     }
 }
@@ -215,7 +216,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, float* __restrict__ out,
                  int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
-                 int32_t* __restrict__ out_tokens, float scale_log2, int trace_idx) {
+                 int32_t* __restrict__ out_tokens, const int32_t* __restrict__ sid, int sid_stride, float scale_log2,
+                 int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
     constexpr int GPW = 32 / TPS;               // sentences per warp step
@@ -987,6 +989,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         rowtab[t - T0] = r;
     }
     const bool any_miss = __syncthreads_or(my_miss) != 0;  // (always false in device residency)
+#ifdef SKV_TRACE
+    SKV_USTAMP(25);
+    if (tid == 0 && unit * kUC + rank < 1024) g_unit_t[unit * kUC + rank][24] = any_miss ? 1 : 0;
+#endif
     if (HOST && any_miss) {
         cache_plan();
         // write-through targets of the rows read from host
@@ -1090,7 +1096,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 gids[i] = sel_id[i];
                 gtok[i] = sel_tok[i];
                 gsrc[i] = sel_src[i];
-                if (out_ids) out_ids[(size_t)unit * tau + i] = sel_id[i];
+                if (out_ids) out_ids[(size_t)unit * tau + i] = sid ? sid[(size_t)b * sid_stride + sel_id[i]] : sel_id[i];
             }
             if (out_ids) {
                 const int pad = (tau - count + kUC - 1) / kUC;
@@ -1190,7 +1196,7 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), a.out, a.out_ids,
-                      a.out_count, a.out_tokens, scale_log2, trace_counter++);
+                      a.out_count, a.out_tokens, a.sid, a.sid_stride, scale_log2, trace_counter++);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {

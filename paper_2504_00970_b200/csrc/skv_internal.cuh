@@ -81,6 +81,17 @@ struct LayerState {
     int32_t* pc_hand = nullptr;        // [units]
     int pc_pages = 0;
     int last_path = 0;                 // host residency: 1 = one-launch kernel (page cache), 2 = split kernels
+    // NEXT-1 importance retention (cfg.obs_window > 0): the layer's retained pool and its buckets
+    bool retained = false;
+    int ret_m = 0;                     // pool tokens per sequence: min(floor(r*tau), L - N)
+    __nv_bfloat16* PK = nullptr;       // [B][G][m][d] retained keys / values, token order (ctx-owned, HBM)
+    __nv_bfloat16* PV = nullptr;
+    float* alpha = nullptr;            // [B][L-N] token importance (Sec. 4.1)
+    int32_t* keep = nullptr;           // [B][m]   retained token indices, ascending
+    int32_t* roff = nullptr;           // [B][m+1] bucket offsets into the pool
+    int32_t* rsid = nullptr;           // [B][m]   sentence id of each bucket
+    int32_t* rS = nullptr;             // [B]      buckets (sentences with a retained token)
+    size_t ret_bytes = 0;              // allocation key (B, G, m, L, N)
 };
 
 }  // namespace skv
@@ -104,6 +115,8 @@ struct skv_ctx {
 
     std::vector<skv::LayerState> layer;
     int4* unit_cand = nullptr;         // overflow scratch of the per-unit step kernel's candidate lists
+    float* ret_scratch = nullptr;      // NEXT-1 pass A partials + row stats
+    size_t ret_scratch_n = 0;
 
     // kernel profiler: (kind, start, stop) event triples awaiting a read
     bool profiling = false;
@@ -154,7 +167,8 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
 // D2: budgeted selection + Q_s state update (Sq += q or reset).
 cudaError_t launch_select(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B,
                           int G, int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids,
-                          int32_t* out_count, int32_t* out_tokens, cudaStream_t st);
+                          int32_t* out_count, int32_t* out_tokens, const int32_t* sid, int sid_stride,
+                          cudaStream_t st);
 
 // D3 + D4 on tensor cores (mma.sync m16n8k16, decode_attend_mma.cu) over the selection of the
 // last launch_select, both residencies.  Host residency: sentences also selected at the previous
@@ -206,11 +220,35 @@ struct UnitArgs {
     int32_t* out_ids;              // optional [B][G][tau]
     int32_t* out_count;            // optional [B][G]
     int32_t* out_tokens;           // optional [B][G]
+    const int32_t* sid;            // optional [B][sid_stride]: output ids = sid[b][selected bucket] (retention)
+    int sid_stride;
 };
 bool unit_supported(int d, int grp, int Smax, int tau, int slots);
 int unit_page_tokens();
 size_t unit_smem_bytes(int d, int tau);
 size_t unit_cand_entries(int units);
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st);
+
+// ---- NEXT-1 importance-filtered retention at prefill (retain.cu) ----
+struct RetainArgs {
+    const __nv_bfloat16* q_window;  // [B][N][Hq][d] queries of the last N prompt tokens
+    const __nv_bfloat16* K;         // [B][G][L][d]
+    const __nv_bfloat16* V;
+    int B, G, grp, d, L, N, m;      // m = retained tokens per sequence
+    const int32_t* off;             // prompt sentence offsets [B][off_stride], S [B]
+    int off_stride;
+    const int32_t* S;
+    float* alpha;                   // [B][L-N]
+    float* scratch;                 // retain_scratch_floats(B, G, L, N, grp)
+    int32_t* keep;                  // [B][m]
+    int32_t* roff;                  // [B][m+1]
+    int32_t* rsid;                  // [B][m]
+    int32_t* rS;                    // [B]
+    __nv_bfloat16* PK;              // [B][G][m][d]
+    __nv_bfloat16* PV;
+};
+bool retain_supported(int d, int N, int grp);
+size_t retain_scratch_floats(int B, int G, int L, int N, int grp);
+cudaError_t launch_retain(const RetainArgs& a, cudaStream_t st);
 
 }  // namespace skv

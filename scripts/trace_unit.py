@@ -25,7 +25,7 @@ tgt = torch.zeros(B, dtype=torch.int32, device=dev)
 out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
 it = torch.full((B,), 300, dtype=torch.int32, device=dev)
 n = B * G * 8
-buf = (ctypes.c_ulonglong * (1024 * 24))()
+buf = (ctypes.c_ulonglong * (1024 * 32))()
 names = ["start", "scored", "csyncA", "bandpath", "general", "selected", "rowtab", "attended", "csync2", "end"]
 if SCRIPT:
     script, target = synth.decode_script(0, B, 8)
@@ -61,7 +61,7 @@ for step in range(24 if SCRIPT else 10):
         skv.decode_step(l, q, it, out)
     torch.cuda.synchronize()
     skvlib.lib.sentencekv_debug_unit(buf)
-    T = np.array(buf, dtype=np.float64).reshape(1024, 24)[:n]
+    T = np.array(buf, dtype=np.float64).reshape(1024, 32)[:n]
     sm = T[:, 23].astype(int)
     gen_path = T[:, 4] > T[:, 3]  # the general path stamps phase 4 after the band attempt
     T[~gen_path, 4] = T[~gen_path, 3]

@@ -161,3 +161,30 @@ def queries_torch(gen, centroids_g, target, Hq: int, G: int, d: int):
     c = centroids_g[:, target.long(), :]                  # [G][B][d]
     c = c.permute(1, 0, 2).repeat_interleave(grp, dim=1)  # [B][Hq][d]
     return (c + torch.randn((B, Hq, d), generator=gen, device=c.device)).to(torch.bfloat16)
+
+
+def window_queries(seed: int, layer: int, target: np.ndarray, Hq: int, G: int, d: int, scale: float = 1.0) -> np.ndarray:
+    """NEXT-1 observation-window queries: bf16 bits [B][N][Hq][d], row w of sequence b
+    = scale * c[layer, g(h), target[b][w]] + N(0, 1).  target = the topics of the last N prompt
+    tokens (the window asks about its own content), or any topics a test wants to emphasise."""
+    c = centroids(seed, layer, G, d)
+    grp = Hq // G
+    rng = _rng(seed, 0x0B5E, layer)
+    B, N = target.shape
+    q = np.empty((B, N, Hq, d), dtype=np.float32)
+    for b in range(B):
+        for w in range(N):
+            for h in range(Hq):
+                q[b, w, h] = scale * c[h // grp, target[b, w]] + rng.standard_normal(d, dtype=np.float32)
+    return f32_to_bf16_bits(q)
+
+
+def window_queries_torch(gen, centroids_g, target, Hq: int, G: int, d: int, scale: float = 1.0):
+    """GPU twin of window_queries for the full-size bench: bf16 [B][N][Hq][d] from the layer's
+    centroids [G][T][d] and the target topics [B][N] (seeded torch generator)."""
+    import torch
+
+    grp = Hq // G
+    c = centroids_g[:, target.long(), :]                      # [G][B][N][d]
+    c = c.permute(1, 2, 0, 3).repeat_interleave(grp, dim=2)   # [B][N][Hq][d]
+    return (scale * c + torch.randn(c.shape, generator=gen, device=c.device)).to(torch.bfloat16)

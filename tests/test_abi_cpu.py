@@ -70,7 +70,9 @@ def _create_status(**kw):
     (dict(batch_begin=1), 1),
     (dict(head_dim=96), 3),                    # unsupported head dim
     (dict(q_heads=24, kv_heads=2), 3),         # grp = 12 unsupported
-    (dict(obs_window=32), 3),                  # NEXT-1 not built
+    (dict(obs_window=-1), 1),                  # N < 0
+    (dict(obs_window=3), 3),                   # NEXT-1: window rows N * grp must be a multiple of 16
+    (dict(obs_window=300), 3),                 # NEXT-1: N * grp <= 256
     (dict(residency=1, semantic_factor=1.5), 1),  # host residency needs r >= 2
 ])
 def test_create_rejects_bad_configs(kw, status):
