@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--no-check", action="store_true", help="skip the end-of-run oracle check")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--shard", choices=["heads", "batch"], default="heads")
+    ap.add_argument("--retention", action="store_true",
+                    help="NEXT-1: importance-filtered retention at prefill (observation window of --obs-window "
+                         "queries, top floor(r*tau) tokens kept in an HBM pool); decode ranks and attends the pool")
+    ap.add_argument("--obs-window", type=int, default=32)
     ap.add_argument("--residency", choices=["device", "host"], default=None,
                     help="K/V residency (default: host for 8b-128k, which configs[2] specifies, else device)")
     return ap.parse_args()
@@ -80,7 +84,7 @@ def peaks():
 
 
 def config_dict(args, cfg, GB, extra=None):
-    d = {"workload": args.config, "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
+    d = {"workload": args.config + ("+retention" if getattr(args, "retention", False) else ""), "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
          "kv_heads": cfg["G"], "head_dim": cfg["d"], "context": cfg["L"], "token_budget": cfg["tau"],
          "median_sentence_tokens": cfg["median"]}
     d.update(extra or {})
@@ -214,7 +218,7 @@ def time_oracle(ost, qsteps, itoks, n_steps, budget_s=None):
 
 def main():
     args = parse()
-    residency = args.residency or ("host" if args.config in ("8b-128k",) else "device")
+    residency = args.residency or ("host" if args.config in ("8b-128k",) and not args.retention else "device")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -235,6 +239,8 @@ def main():
 
     import synth
 
+    if args.retention and world > 1 and args.shard != "batch":
+        raise SystemExit("--retention sums alpha over all heads (P:394): shard by batch (--shard batch)")
     if args.shard == "batch" and residency == "host" and world > 1:
         raise SystemExit("--shard batch with host residency would pin world x the host store; use --shard heads")
     if world > 1:
@@ -252,8 +258,9 @@ def main():
     plan = parallel.plan(GB, G, Hq, world, rank, "batch" if args.shard == "batch" else "heads")
     Bl, Gl, Hl = plan.batch_count, plan.kv_head_count, plan.q_head_count
     b0, g0, h0 = plan.batch_begin, plan.kv_head_begin, plan.q_head_begin
-    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline
-    check = rank == 0 and world == 1 and not args.no_check
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline and not args.retention
+    check = rank == 0 and world == 1 and not args.no_check and not args.retention
+    N = args.obs_window if args.retention else 0
     keep_layers = [0, 1][:M] if (cpu_leg or check) else []
 
     # ---------------- inputs (seeded, synthetic; this rank's shard of sequences and heads)
@@ -263,7 +270,9 @@ def main():
     top_dev = torch.from_numpy(topics).to(dev)
     host = residency == "host"
     skv = skvlib.SentenceKV(layers=M, head_dim=d, max_context=L, token_budget=tau, device=local,
-                            residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE, **plan.ctx_kwargs())
+                            residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE, obs_window=N,
+                            **plan.ctx_kwargs())
+    wgen = torch.Generator(device=dev)
     # ---------------- K/V generation + prefill (P1 segmentation, P2 embeddings, P3 offload in host
     # residency), per layer; in host residency the device K/V of a layer is freed once offloaded
     # (layers 0, 1 are copied to the host for the CPU oracle's baseline and end-of-run check).
@@ -279,8 +288,12 @@ def main():
         pf1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         pf0.record()
+        qw = None
+        if N:  # the window's own queries: about the topics of the last N prompt tokens
+            wgen.manual_seed(4242 + 7919 * l)
+            qw = synth.window_queries_torch(wgen, c, top_dev[:, L - N:], Hq, G, d)[:, :, h0:h0 + Hl].contiguous()
         skv.prefill_compress(l, K, V, token_ids=tok_dev if l == 0 else None,
-                             boundary_ids=synth.BOUNDARY_IDS if l == 0 else None)
+                             boundary_ids=synth.BOUNDARY_IDS if l == 0 else None, q_window=qw)
         pf1.record()
         if host:
             skv.sync()  # D2H copies of this layer done
@@ -290,14 +303,22 @@ def main():
         if l in keep_layers:
             Kh.append(K.view(torch.int16).cpu().numpy().view(np.uint16))
             Vh.append(V.view(torch.int16).cpu().numpy().view(np.uint16))
-        Ks.append(None if host else K)
-        Vs.append(None if host else V)
+        Ks.append(None if (host or N) else K)  # host store / retained pool: the ctx keeps its own copy
+        Vs.append(None if (host or N) else V)
         Cs.append(c)
         del K, V
     prof_prefill = skv.profile_read()
     skv.set_profiling(False)
     S = skv.sentence_counts()
     kv_bytes_total = 2 * Bl * Gl * L * d * 2 * M
+    ret = None
+    if N:  # buckets per layer (sentences with a retained token) replace the prompt's sentences
+        Sl = [skv.retained(l)[3].cpu().numpy() for l in range(M)]
+        ret = {"obs_window": N, "retained_tokens_per_seq": skv.retained_tokens(0),
+               "buckets_mean_per_seq": round(float(np.mean([x.mean() for x in Sl])), 1),
+               "retain_ms_per_layer": round(prof_prefill["retain"][0] / max(1, prof_prefill["retain"][1]), 4),
+               "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4)}
+        S = [int(round(float(np.mean([x[b] for x in Sl])))) for b in range(Bl)]
 
     # ---------------- decode script: one fresh step of queries + input tokens per executed step
     n_cold, n_eager = (1 if host else 0), 2
@@ -611,7 +632,7 @@ def main():
             "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(Bl * Gl * L * d * 2 * M),
                         "segment_ms": round(prof_prefill["segment"][0], 3),
                         "compress_ms_per_layer": round(prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]), 4),
-                        "compress_gbs": round(Bl * Gl * L * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
+                        "compress_gbs": round(Bl * Gl * (skv.retained_tokens(0) if N else L) * d * 2 / (prof_prefill["compress"][0] / max(1, prof_prefill["compress"][1]) / 1e3) / 1e9, 1)},
             "host_residency": {"host_bytes_per_step": int(host_step_bytes),
                                "host_rows_per_step": round(host_step_bytes / (d * 2 * 2), 1),
                                "host_link_gbs_in_step": round(host_step_bytes / (ms_step / 1e3) / 1e9, 2),
@@ -623,6 +644,7 @@ def main():
                                "paper_onload": "PAPER.md P:740: onload 1024 tokens 0.0038 s (H100 NVL, per step)"}
             if host else None,
             "end_check": chk,
+            "retention": ret,
             "cpu_baseline": cpu,
             "kv_gen_s": round(t_gen, 2),
         }

@@ -30,12 +30,19 @@ namespace skv {
 namespace {
 
 constexpr int kKT = 128;             // keys per tile
-constexpr int kStages = 4;           // K-tile ring
+constexpr int kStages = 2;           // K-tile ring (2 stages: two CTAs per SM, 8 epilogue warps)
 constexpr int kHalf = 128 * 128;     // one TMA box: 128 rows x 64 bf16 (128 B, swizzled) = 16 KB
 constexpr int kThreads = 192;        // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
-constexpr int kMaxTiles = 32;        // pass B: key tiles per CTA (alpha kept in shared memory)
+constexpr int kMaxTiles = 16;        // pass B: key tiles per CTA (alpha kept in shared memory)
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// 2^x on the SFU, flush-to-zero (x <= 0 here: results below 2^-126 are far below the tolerance)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // mbarrier wait that traps (a launch error, not a hung GPU) if the pipeline ever stalls for seconds
 __device__ __forceinline__ void wait_or_trap(uint64_t* bar, uint32_t parity) {
@@ -52,7 +59,7 @@ __device__ __forceinline__ void wait_or_trap(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------------------- pass A: row stats
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 alpha_rowstats_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, int L, int N,
                       int grp, int G, int R, int nrb, int wbox, int chunk_tiles, float scale_log2,
                       float2* __restrict__ part) {
@@ -129,25 +136,30 @@ alpha_rowstats_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_cons
             wait_or_trap(&tfull[acc], (i >> 1) & 1);
             umma::fence_after();
             const int jb = (t0 + i) * kKT;
+            const bool masked = jb + kKT - 1 > L - N;  // only tiles reaching the window need the causal mask
 #pragma unroll 1
             for (int c4 = 0; c4 < 4; ++c4) {
                 float v[32];
                 umma::ld32(tbase + ((uint32_t)(quarter * 32) << 16) + acc * kKT + c4 * 32, v);
                 float cm = -INFINITY;
+                if (masked) {
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    v[c] = (jb + c4 * 32 + c <= p) ? v[c] * scale_log2 : -INFINITY;
-                    cm = fmaxf(cm, v[c]);
+                    for (int c = 0; c < 32; ++c) v[c] = (jb + c4 * 32 + c <= p) ? v[c] * scale_log2 : -INFINITY;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] *= scale_log2;
                 }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) cm = fmaxf(cm, v[c]);
                 if (cm == -INFINITY) continue;
                 if (cm > m) {
-                    l *= exp2f(m - cm);
+                    l *= ex2(m - cm);
                     m = cm;
                 }
-                float s = 0.0f;
+                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-                for (int c = 0; c < 32; ++c) s += exp2f(v[c] - m);
-                l += s;
+                for (int c = 0; c < 32; ++c) s4[c & 3] += ex2(v[c] - m);
+                l += (s4[0] + s4[1]) + (s4[2] + s4[3]);
             }
             umma::fence_before();
             __syncwarp();
@@ -182,17 +194,17 @@ __global__ void alpha_rowcombine_kernel(const float2* __restrict__ part, int G, 
 
 // ---------------------------------------------------------------------------- pass B: alpha
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, int L, int N,
-                    int grp, int G, int R, int Lc, int tiles_per_cta, float scale_log2,
+                    int grp, int G, int R, int Lc, int tiles_per_cta, int qhalf, float scale_log2,
                     const float2* __restrict__ stats, float* __restrict__ alpha) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    unsigned char* sQ = sm;                     // DH halves of R rows, 32 KB apart
-    unsigned char* sK = sm + DH * 2 * kHalf;    // kStages x DH boxes
+    unsigned char* sQ = sm;                     // DH halves of R rows, qhalf bytes apart
+    unsigned char* sK = sm + DH * qhalf;        // kStages x DH boxes
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qfull, qempty;
     __shared__ uint32_t tmem_base;
-    __shared__ float2 sstat[2][256];
+    __shared__ __align__(16) float2 sstat[2][256];
     __shared__ float salpha[kMaxTiles][kKT];
 
     const int b = blockIdx.y;
@@ -226,7 +238,7 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         for (int g = 0; g < G; ++g) {
             if (g > 0) wait_or_trap(&qempty, (g - 1) & 1);
             mbar_arrive_expect_tx(&qfull, (uint32_t)(DH * R * 128));
-            for (int h = 0; h < DH; ++h) umma::tma_load_3d(sQ + h * 2 * kHalf, &tmQ, h * 64, g * grp, b * N, &qfull);
+            for (int h = 0; h < DH; ++h) umma::tma_load_3d(sQ + h * qhalf, &tmQ, h * 64, g * grp, b * N, &qfull);
             for (int i = 0; i < nt; ++i) {
                 const int it = g * nt + i, s = it % kStages;
                 if (it >= kStages) wait_or_trap(&empty[s], ((it / kStages) - 1) & 1);
@@ -249,7 +261,7 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                 for (int kk = 0; kk < DH * 4; ++kk) {
                     const int h = kk >> 2, k4 = kk & 3;
                     const uint64_t a = umma::desc_k128(smem_addr(sK + (s * DH + h) * kHalf) + k4 * 32);
-                    const uint64_t bq = umma::desc_k128(smem_addr(sQ + h * 2 * kHalf) + k4 * 32);
+                    const uint64_t bq = umma::desc_k128(smem_addr(sQ + h * qhalf) + k4 * 32);
                     umma::mma_bf16(tbase + acc * rc, a, bq, idesc, kk > 0 ? 1u : 0u);
                 }
                 umma::commit(&empty[s]);
@@ -261,27 +273,28 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         // thread = key of the tile: alpha_j += sum over rows (ascending) of exp2(z - m) / l
         const int et = threadIdx.x - 64, quarter = warp & 3, row = quarter * 32 + lane;
         for (int g = 0; g < G; ++g) {
-            for (int r = et; r < R; r += 128) sstat[g & 1][r] = stats[(size_t)(b * G + g) * R + r];
+            // rows R..rc-1 (TMEM columns past the window rows) get (m = +inf, 1/l = 0): they add 0
+            for (int r = et; r < rc; r += 128)
+                sstat[g & 1][r] = r < R ? stats[(size_t)(b * G + g) * R + r] : make_float2(INFINITY, 0.0f);
             epi_bar();
-            const float2* st = sstat[g & 1];
+            const float4* st4 = reinterpret_cast<const float4*>(sstat[g & 1]);
             for (int i = 0; i < nt; ++i) {
                 const int it = g * nt + i, acc = it & 1;
                 wait_or_trap(&tfull[acc], (it >> 1) & 1);
                 umma::fence_after();
-                float a = 0.0f;
+                float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // fixed order: (a0 + a1) + (a2 + a3) at the end
 #pragma unroll 1
                 for (int cc = 0; cc < rc / 32; ++cc) {
                     float v[32];
                     umma::ld32(tbase + ((uint32_t)(quarter * 32) << 16) + acc * rc + cc * 32, v);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const int r = cc * 32 + c;
-                        if (r < R) {
-                            const float2 ml = st[r];
-                            a += exp2f(fmaf(v[c], scale_log2, -ml.x)) * ml.y;
-                        }
+                    for (int c = 0; c < 32; c += 2) {
+                        const float4 ml = st4[(cc * 32 + c) >> 1];  // (m, 1/l) of rows c, c+1
+                        a4[c & 3] += ex2(fmaf(v[c], scale_log2, -ml.x)) * ml.y;
+                        a4[(c + 1) & 3] += ex2(fmaf(v[c + 1], scale_log2, -ml.z)) * ml.w;
                     }
                 }
+                const float a = (a4[0] + a4[1]) + (a4[2] + a4[3]);
                 umma::fence_before();
                 __syncwarp();
                 if (lane == 0) umma::mbar_arrive(&tempty[acc]);
@@ -303,28 +316,43 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 // ---------------------------------------------------------------------------- top-k + buckets
 // One CTA per sequence.  Keys: ordered(alpha) (NaN ranks last, reading A14's rule); the m-th largest
 // key T by a 4-pass 8-bit radix select; kept = key > T, or key == T among the first (m - #greater)
-// in index order (ties -> lowest index, A21).  Then the retained buckets: sentence s keeps the pool
-// range [#kept before off_s, #kept before off_{s+1}); empty ones are dropped (A25).
-__global__ void __launch_bounds__(1024) retain_topk_kernel(const float* __restrict__ alpha, int Lc, int m,
-                                                          const int32_t* __restrict__ off, int off_stride,
-                                                          const int32_t* __restrict__ S, int32_t* __restrict__ keep,
-                                                          int32_t* __restrict__ roff, int32_t* __restrict__ rsid,
-                                                          int32_t* __restrict__ rS) {
+// in index order (ties -> lowest index, A21).  Then the retained buckets: kept token i lies in
+// sentence s_i; a bucket starts wherever s_i changes (sentences without a kept token vanish, A25).
+// Every pass reads alpha coalesced: warp w owns the contiguous range [w*C, (w+1)*C), lane = element.
+constexpr int kTopThreads = 1024;
+constexpr int kTopWarps = kTopThreads / 32;
+
+__global__ void __launch_bounds__(kTopThreads) retain_topk_kernel(const float* __restrict__ alpha, int Lc, int m,
+                                                                 const int32_t* __restrict__ off, int off_stride,
+                                                                 const int32_t* __restrict__ S, int32_t* __restrict__ keep,
+                                                                 int32_t* __restrict__ roff, int32_t* __restrict__ rsid,
+                                                                 int32_t* __restrict__ rS, int off_cap) {
     __shared__ uint32_t hist[256];
     __shared__ uint32_t ws32[32];
-    __shared__ uint32_t s_prefix, s_need, s_digit;
-    const int b = blockIdx.x, tid = threadIdx.x;
+    __shared__ uint32_t s_need, s_digit;
+    __shared__ uint32_t wgt[kTopWarps], weq[kTopWarps];
+    __shared__ int32_t s_last[kTopWarps];
+    const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float* a = alpha + (size_t)b * Lc;
     int32_t* kp = keep + (size_t)b * m;
+    const int C = (Lc + kTopWarps - 1) / kTopWarps;  // elements per warp
+    const int w0 = min(Lc, warp * C), w1 = min(Lc, w0 + C);
     uint32_t prefix = 0, need = (uint32_t)m;  // keys >= T must number m
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
-        for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0u;
+        for (int i = tid; i < 256; i += kTopThreads) hist[i] = 0u;
         __syncthreads();
-        for (int j = tid; j < Lc; j += blockDim.x) {
-            const uint32_t k = ordered_key(a[j]);
-            if ((k & hmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        for (int j0 = w0; j0 < w1; j0 += 32 * 8) {
+            uint32_t k[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j0 + u * 32 + lane;
+                k[u] = j < w1 ? ordered_key(a[j]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (j0 + u * 32 + lane < w1 && (k[u] & hmask) == prefix) atomicAdd(&hist[(k[u] >> shift) & 255u], 1u);
         }
         __syncthreads();
         if (tid < 32) {
@@ -357,58 +385,133 @@ __global__ void __launch_bounds__(1024) retain_topk_kernel(const float* __restri
         __syncthreads();
     }
     const uint32_t T = prefix;  // the m-th largest key; `need` of the keys equal to T are kept
-    // ordered compaction over contiguous index chunks
-    const int per = (Lc + blockDim.x - 1) / blockDim.x;
-    const int j0 = min(Lc, tid * per), j1 = min(Lc, j0 + per);
-    uint32_t eq = 0;
-    for (int j = j0; j < j1; ++j) eq += ordered_key(a[j]) == T ? 1u : 0u;
-    uint32_t tot;
-    uint32_t eq_before = block_incl_sum<uint32_t>(eq, ws32, &tot) - eq;
-    uint32_t mine = 0;
+    // counts per warp, then each warp's first output position in closed form
     {
-        uint32_t e = eq_before;
-        for (int j = j0; j < j1; ++j) {
-            const uint32_t k = ordered_key(a[j]);
-            if (k > T || (k == T && e++ < need)) ++mine;
+        uint32_t gt = 0, eq = 0;
+        for (int j0 = w0; j0 < w1; j0 += 32 * 8) {
+            uint32_t k[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j0 + u * 32 + lane;
+                k[u] = j < w1 ? ordered_key(a[j]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool in = j0 + u * 32 + lane < w1;
+                gt += __popc(__ballot_sync(0xffffffffu, in && k[u] > T));
+                eq += __popc(__ballot_sync(0xffffffffu, in && k[u] == T));
+            }
         }
-    }
-    uint32_t pos = block_incl_sum<uint32_t>(mine, ws32, &tot) - mine;
-    {
-        uint32_t e = eq_before;
-        for (int j = j0; j < j1; ++j) {
-            const uint32_t k = ordered_key(a[j]);
-            if (k > T || (k == T && e++ < need)) kp[pos++] = j;
+        if (lane == 0) {
+            wgt[warp] = gt;
+            weq[warp] = eq;
         }
     }
     __syncthreads();
-    __threadfence_block();
-    // retained buckets
+    uint32_t gt_before = 0, eq_before = 0;
+    for (int w = 0; w < warp; ++w) {
+        gt_before += wgt[w];
+        eq_before += weq[w];
+    }
+    uint32_t pos = gt_before + min(eq_before, need);
+    {
+        const unsigned lt = (1u << lane) - 1u;
+        uint32_t e = eq_before;
+        for (int j00 = w0; j00 < w1; j00 += 32 * 8) {
+            uint32_t kk[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j00 + u * 32 + lane;
+                kk[u] = j < w1 ? ordered_key(a[j]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j00 + u * 32 + lane;
+                const uint32_t k = kk[u];
+                const unsigned em = __ballot_sync(0xffffffffu, j < w1 && k == T);
+                const bool kept = j < w1 && (k > T || (k == T && e + __popc(em & lt) < need));
+                const unsigned km = __ballot_sync(0xffffffffu, kept);
+                if (kept) kp[pos + __popc(km & lt)] = j;
+                pos += __popc(km);
+                e += __popc(em);
+            }
+        }
+    }
+    __syncthreads();
+    // buckets: sentence of every kept token (binary search in the prompt offsets), starts where it changes
     const int Sb = S[b];
     const int32_t* o = off + (size_t)b * off_stride;
-    auto lower = [&](int x) {  // #kept tokens < x
-        int lo = 0, hi = m;
+    extern __shared__ int32_t soff[];  // the prompt's offsets, when they fit (dynamic smem sized by the launcher)
+    if (Sb + 1 <= off_cap) {
+        for (int i = tid; i <= Sb; i += kTopThreads) soff[i] = o[i];
+        __syncthreads();
+        o = soff;
+    }
+    const int Cm = (m + kTopWarps - 1) / kTopWarps;
+    const int i0 = min(m, warp * Cm), i1 = min(m, i0 + Cm);
+    auto sent_of = [&](int t) {  // largest s with o[s] <= t
+        int lo = 0, hi = Sb - 1;
         while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (kp[mid] < x) lo = mid + 1; else hi = mid;
+            const int mid = (lo + hi + 1) >> 1;
+            if (o[mid] <= t) lo = mid; else hi = mid - 1;
         }
         return lo;
     };
-    const int pers = (Sb + blockDim.x - 1) / blockDim.x;
-    const int s0 = min(Sb, tid * pers), s1 = min(Sb, s0 + pers);
-    uint32_t ne = 0;
-    for (int s = s0; s < s1; ++s) ne += lower(o[s + 1]) > lower(o[s]) ? 1u : 0u;
-    uint32_t sp = block_incl_sum<uint32_t>(ne, ws32, &tot) - ne;
+    uint32_t nstart = 0;
+    int32_t last = -1;
+    for (int x0 = i0; x0 < i1; x0 += 32) {
+        const int x = x0 + lane;
+        const int s = x < i1 ? sent_of(kp[x]) : -1;
+        int prev = __shfl_up_sync(0xffffffffu, s, 1);
+        if (lane == 0) prev = last;
+        nstart += __popc(__ballot_sync(0xffffffffu, x < i1 && s != prev));
+        last = __shfl_sync(0xffffffffu, s, 31);
+        const int nv = min(32, i1 - x0);
+        last = __shfl_sync(0xffffffffu, s, nv - 1);
+    }
+    if (lane == 0) {
+        wgt[warp] = nstart;
+        s_last[warp] = last;
+    }
+    __syncthreads();
+    // a warp's first token starts a bucket unless the previous non-empty warp ended in the same sentence
+    uint32_t sp = 0;
+    int32_t carry = -1;
+    for (int w = 0; w < warp; ++w) {
+        if (s_last[w] >= 0) carry = s_last[w];
+    }
+    for (int w = 0; w < warp; ++w) sp += wgt[w];
+    // (the per-warp counts above treated each warp's first token as a start; subtract the duplicates)
+    __shared__ uint32_t s_dup[kTopWarps];
+    if (lane == 0) {
+        int32_t first = i0 < i1 ? sent_of(kp[i0]) : -2;
+        s_dup[warp] = (i0 < i1 && first == carry) ? 1u : 0u;
+    }
+    __syncthreads();
+    for (int w = 0; w <= warp; ++w) sp -= (w < warp) ? s_dup[w] : 0u;
     int32_t* ro = roff + (size_t)b * (m + 1);
     int32_t* rs = rsid + (size_t)b * m;
-    for (int s = s0; s < s1; ++s) {
-        const int lo = lower(o[s]), hi = lower(o[s + 1]);
-        if (hi > lo) {
-            ro[sp] = lo;
-            rs[sp] = s;
-            ++sp;
+    last = s_dup[warp] ? carry : -1;
+    for (int x0 = i0; x0 < i1; x0 += 32) {
+        const int x = x0 + lane;
+        const int s = x < i1 ? sent_of(kp[x]) : -1;
+        int prev = __shfl_up_sync(0xffffffffu, s, 1);
+        if (lane == 0) prev = last;
+        const bool start = x < i1 && s != prev;
+        const unsigned sm_ = __ballot_sync(0xffffffffu, start);
+        if (start) {
+            const uint32_t q = sp + __popc(sm_ & ((1u << lane) - 1u));
+            ro[q] = x;
+            rs[q] = s;
         }
+        sp += __popc(sm_);
+        const int nv = min(32, i1 - x0);
+        last = __shfl_sync(0xffffffffu, s, nv - 1);
     }
-    if (tid == 0) {
+    __syncthreads();
+    if (tid == kTopThreads - 1) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kTopWarps; ++w) tot += wgt[w] - s_dup[w];
         ro[tot] = m;
         rS[b] = (int32_t)tot;
     }
@@ -506,7 +609,8 @@ cudaError_t launch_retain(const RetainArgs& a, cudaStream_t st) {
     float2* part = reinterpret_cast<float2*>(a.scratch);
     float2* stats = part + (size_t)a.B * a.G * nrb * nchunk * 128;
     const size_t smemA = 1024 + (size_t)DH * kHalf * (1 + kStages);
-    const size_t smemB = 1024 + (size_t)DH * 2 * kHalf + (size_t)DH * kHalf * kStages;
+    const int qhalf = (R * 128 + 1023) / 1024 * 1024;
+    const size_t smemB = 1024 + (size_t)DH * qhalf + (size_t)DH * kHalf * kStages;
     cudaError_t e;
     if (DH == 2) {
         if ((e = ensure_smem((const void*)alpha_rowstats_kernel<2>, smemA)) != cudaSuccess) return e;
@@ -522,20 +626,24 @@ cudaError_t launch_retain(const RetainArgs& a, cudaStream_t st) {
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // pass B: every SM one CTA, each a run of key tiles of one sequence, all KV heads
     const int ntc = (Lc + kKT - 1) / kKT;
-    const int per_b = std::max(1, kNumSMs / a.B);
+    const int per_b = std::max(1, 2 * kNumSMs / a.B);  // two CTAs per SM
     const int tiles_per_cta = std::min(kMaxTiles, std::max(1, (ntc + per_b - 1) / per_b));
     const int nctb = (ntc + tiles_per_cta - 1) / tiles_per_cta;
     if (DH == 2) {
         if ((e = ensure_smem((const void*)alpha_colsum_kernel<2>, smemB)) != cudaSuccess) return e;
         alpha_colsum_kernel<2><<<dim3(nctb, a.B), kThreads, smemB, st>>>(tmQb, tmK, a.L, a.N, a.grp, a.G, R, Lc,
-                                                                          tiles_per_cta, scale_log2, stats, a.alpha);
+                                                                          tiles_per_cta, qhalf, scale_log2, stats, a.alpha);
     } else {
         if ((e = ensure_smem((const void*)alpha_colsum_kernel<1>, smemB)) != cudaSuccess) return e;
         alpha_colsum_kernel<1><<<dim3(nctb, a.B), kThreads, smemB, st>>>(tmQb, tmK, a.L, a.N, a.grp, a.G, R, Lc,
-                                                                          tiles_per_cta, scale_log2, stats, a.alpha);
+                                                                          tiles_per_cta, qhalf, scale_log2, stats, a.alpha);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    retain_topk_kernel<<<a.B, 1024, 0, st>>>(a.alpha, Lc, a.m, a.off, a.off_stride, a.S, a.keep, a.roff, a.rsid, a.rS);
+    // the prompt's sentence offsets go to shared memory when they fit in 96 KB
+    const int off_cap = std::min(a.off_stride, 96 * 1024 / 4);
+    if ((e = ensure_smem((const void*)retain_topk_kernel, (size_t)off_cap * 4)) != cudaSuccess) return e;
+    retain_topk_kernel<<<a.B, kTopThreads, (size_t)off_cap * 4, st>>>(a.alpha, Lc, a.m, a.off, a.off_stride, a.S, a.keep,
+                                                                     a.roff, a.rsid, a.rS, off_cap);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int blocks = std::max(1, std::min(64, (a.m * a.d / 8 + 255) / 256));
     retain_gather_kernel<<<dim3(blocks, a.G, a.B), 256, 0, st>>>(a.K, a.V, a.G, a.L, a.d, a.m, a.keep, a.PK, a.PV);

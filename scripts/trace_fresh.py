@@ -10,20 +10,26 @@ import numpy as np, torch
 import paper_2504_00970_b200 as skvlib, synth
 
 HOST = (sys.argv[1] if len(sys.argv) > 1 else "host") == "host"
+RET = (sys.argv[1] if len(sys.argv) > 1 else "") == "ret"  # device residency + NEXT-1 retention (N = 32)
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 STEPS = int(sys.argv[3]) if len(sys.argv) > 3 else 60
 B, Hq, G, d, L, tau = 4, 32, 8, 128, 131072, 2048
 dev = torch.device("cuda:0")
 toks, topics = synth.prompts(0, B, L, 25.0)
 skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
-                        residency=skvlib.SKV_KV_HOST if HOST else skvlib.SKV_KV_DEVICE)
+                        residency=skvlib.SKV_KV_HOST if HOST else skvlib.SKV_KV_DEVICE, obs_window=32 if RET else 0)
+wg = torch.Generator(device=dev)
 top = torch.from_numpy(topics).to(dev)
 KV = []
 for l in range(M):
     K, V, c = synth.kv_layer_torch(0, l, top, G, d, device=dev)
-    skv.prefill_compress(l, K, V, torch.from_numpy(toks).to(dev) if l == 0 else None, synth.BOUNDARY_IDS if l == 0 else None)
+    qw = None
+    if RET:
+        wg.manual_seed(4242 + 7919 * l)
+        qw = synth.window_queries_torch(wg, c, top[:, L - 32:], Hq, G, d).contiguous()
+    skv.prefill_compress(l, K, V, torch.from_numpy(toks).to(dev) if l == 0 else None, synth.BOUNDARY_IDS if l == 0 else None, q_window=qw)
     skv.sync()
-    KV.append((None, None, c) if HOST else (K, V, c))
+    KV.append((None, None, c) if (HOST or RET) else (K, V, c))
 script, target = synth.decode_script(0, B, STEPS + 1)
 gen = torch.Generator(device=dev); gen.manual_seed(1)
 out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
@@ -58,11 +64,15 @@ for step in range(STEPS):
                          att_hit=np.median(t(7)[~miss] - t(6)[~miss]) if (~miss).any() else 0.0))
 import statistics as st
 keys = ["span", "scored", "selected", "rowtab", "planned", "attended", "csync2", "miss_ctas", "gen_ctas", "host_mb", "plan_miss", "att_miss", "att_hit"]
-print(f"residency={'host' if HOST else 'device'} layers={M} steps={STEPS}: per launch (max over CTAs of phase end, us since first CTA start)")
+print(f"residency={'host' if HOST else 'device'}{' +retention' if RET else ''} layers={M} steps={STEPS}: per launch (max over CTAs of phase end, us since first CTA start)")
 print("  all  : " + " ".join(f"{k}={st.median([r[k] for r in rows]):.2f}" for k in keys))
 for sel, name in ((lambda r: r["miss_ctas"] == 0, "nomiss"), (lambda r: 0 < r["miss_ctas"] and r["host_mb"] < 1, "fewmiss"), (lambda r: r["host_mb"] >= 1, "bigmiss")):
     rs = [r for r in rows if sel(r)]
     if rs:
         print(f"  {name:6s} n={len(rs):4d}: " + " ".join(f"{k}={st.median([r[k] for r in rs]):.2f}" for k in keys))
-print("general-path units (step, layer, unit, reason bits 1 ovf/2 above>tau/4 below band, listed):", why[:40])
+from collections import Counter
+late = [w for w in why if w[0] > 0]
+print("general-path units after step 0:", len(late), "of", (STEPS - 1) * M * B * G, "unit-launches; reasons (1 ovf, 2 above>tau, 4 below band):",
+      dict(Counter(w[3] for w in late)), "; units per launch:", dict(Counter(Counter((w[0], w[1]) for w in late).values())))
+print("  first 30:", late[:30])
 print("per step span sum (us):", [round(sum(r["span"] for r in rows if r["step"] == s), 1) for s in range(STEPS)])

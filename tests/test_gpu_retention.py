@@ -13,7 +13,7 @@ from tests.gpu_harness import ATOL, from_bits, to_bits
 
 pytestmark = pytest.mark.gpu
 
-ALPHA_RTOL = 2e-3   # DESIGN.md reading A24: bf16 operands, fp32 tensor-core accumulation, exp2.approx
+ALPHA_RTOL = 5e-4   # DESIGN.md reading A24: worst-case fp32 budget at L <= 4096 (bf16 operands, fp32 sums, exp2.approx)
 ALPHA_ATOL = 1e-6   # x max(alpha): terms far below the largest
 
 
