@@ -1121,7 +1121,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 uint2 h = make_uint2(0u, 0xffffffffu);  // everything fits: the band is everything
                 if (ctl.kc_set) {
                     const uint32_t kc = ctl.kc, ks = ctl.ks, w = (uint32_t)band_w;
-                    h.x = kc > w ? kc - w : 0u;
+                    const uint32_t wl = w << SKV_BAND_LO_SHIFT;
+                    h.x = kc > wl ? kc - wl : 0u;
                     h.y = ks < 0xffffffffu - w ? ks + w : 0xffffffffu;
                 }
                 hint[unit] = h;
@@ -1175,14 +1176,7 @@ bool unit_supported(int d, int grp, int Smax, int tau, int slots) {
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
 
 
-static int band_width() {
-    static const int w = [] {
-        const char* e = getenv("SKV_BAND_LOG2");  // half-width of the band in ordered-key units (2^19 ~ 6%)
-        const int l = e ? atoi(e) : 19;
-        return l <= 0 ? 0 : (1 << std::min(l, 30));
-    }();
-    return w;
-}
+static int band_width() { return 1 << 19; }  // half-width of the band in ordered-key units
 
 static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
 
