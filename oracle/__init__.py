@@ -66,6 +66,16 @@ def lib():
         L.skvref_retain.restype = i32
         L.skvref_retained_buckets.argtypes = [P, i32, P, i32, P, P]
         L.skvref_retained_buckets.restype = i32
+        L.skvref_equal_chunks.argtypes = [i32, i32, i32, P]
+        L.skvref_equal_chunks.restype = i32
+        L.skvref_outlier_threshold.argtypes = [P, i32, ctypes.c_double]
+        L.skvref_outlier_threshold.restype = i32
+        L.skvref_select_skip.argtypes = [P, P, i32, i32, P, P]
+        L.skvref_select_skip.restype = i32
+        L.skvref_quest_meta.argtypes = [P, i32, i32, i32, P, P]
+        L.skvref_quest_meta.restype = None
+        L.skvref_quest_score.argtypes = [P, i32, P, P, i32, i32, P]
+        L.skvref_quest_score.restype = None
         L.skvref_kv_bytes.argtypes = [i64, i64, i64, i64, i64]
         L.skvref_kv_bytes.restype = i64
         L.skvref_f32_to_bf16.argtypes = [f32]
@@ -202,6 +212,52 @@ def retained_buckets(off, keep):
     return off2[: S2 + 1].copy(), sid[:S2].copy()
 
 
+def equal_chunks(L: int, S: int, tau: int) -> np.ndarray:
+    """NEXT-3 equal-size chunks (Sec. 6.1; reading A26): offsets of as many chunks as sentences."""
+    off = np.zeros(L + 1, dtype=np.int32)
+    n = lib().skvref_equal_chunks(int(L), int(S), int(tau), _p(off))
+    return off[: n + 1].copy()
+
+
+def outlier_threshold(off, n: float) -> int:
+    """NEXT-3 outlier split (reading A27): T = floor(mean + n * std) of the sentence lengths."""
+    off = _c(off, np.int32)
+    return int(lib().skvref_outlier_threshold(_p(off), len(off) - 1, float(np.float32(n))))
+
+
+def select_skip(scores, off, tau: int):
+    """NEXT-3 skip-and-continue budget fill (alternative to A13): ascending ids and selected tokens."""
+    scores = _c(scores, np.float32)
+    off = _c(off, np.int32)
+    S = len(off) - 1
+    ids = np.zeros(max(S, 1), dtype=np.int32)
+    ntok = np.zeros(1, dtype=np.int32)
+    n = lib().skvref_select_skip(_p(scores), _p(off), S, int(tau), _p(ids), _p(ntok))
+    return ids[:n].copy(), int(ntok[0])
+
+
+def quest_meta(K_bits, P: int):
+    """NEXT-4 Quest pages (App. Quest): per-page min / max keys, bf16 bits [np][d] each."""
+    K_bits = _c(K_bits, np.uint16)
+    L, d = K_bits.shape
+    npg = (L + P - 1) // P
+    mn = np.zeros((npg, d), dtype=np.uint16)
+    mx = np.zeros((npg, d), dtype=np.uint16)
+    lib().skvref_quest_meta(_p(K_bits), L, d, int(P), _p(mn), _p(mx))
+    return mn, mx
+
+
+def quest_score(q_bits, mn, mx) -> np.ndarray:
+    """NEXT-4 Quest bound sum_h sum_j max(q_j mn_j, q_j mx_j) per page (reading A28), q_bits [grp][d]."""
+    q_bits = _c(q_bits, np.uint16)
+    mn = _c(mn, np.uint16)
+    mx = _c(mx, np.uint16)
+    grp, d = q_bits.shape
+    out = np.zeros(mn.shape[0], dtype=np.float32)
+    lib().skvref_quest_score(_p(q_bits), grp, _p(mn), _p(mx), mn.shape[0], d, _p(out))
+    return out
+
+
 def retained_count(r: float, tau: int) -> int:
     """floor(r * tau) (reading A20), the number of tokens the retention keeps."""
     import math
@@ -212,6 +268,11 @@ def retained_count(r: float, tau: int) -> int:
 def kv_bytes(M, H, d, tokens, elem_bytes=2) -> int:
     """App. Cost(t) written out: M*H*(L+t)*d*2*elem_bytes."""
     return int(lib().skvref_kv_bytes(M, H, d, tokens, elem_bytes))
+
+
+def synth_free_bf16_to_f32(bits) -> np.ndarray:
+    """bf16 bit patterns -> fp32 (exact widening)."""
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
 
 
 def f32_to_bf16_bits(x: float) -> int:
@@ -228,16 +289,33 @@ class Oracle:
     per decode step and layer q bf16 bits [B][Hq][d] and the input token ids [B].
     """
 
+    BUCKETS_SENTENCE, BUCKETS_EQUAL, BUCKETS_QUEST = 0, 1, 2
+
     def __init__(self, tokens, boundary_ids, tau: int, layers: int, q_heads: int, kv_heads: int, d: int,
-                 obs_window: int = 0, semantic_factor: float = 2.0):
+                 obs_window: int = 0, semantic_factor: float = 2.0, bucket_mode: int = 0, chunk_size: int = 0,
+                 outlier_n: float = 0.0, query_mode: int = 0, fill_mode: int = 0):
         self.tokens = np.asarray(tokens, dtype=np.int32)
         self.B = self.tokens.shape[0]
         self.bset = np.asarray(boundary_ids, dtype=np.int32)
         self.tau = int(tau)
         self.M, self.Hq, self.G, self.d = layers, q_heads, kv_heads, d
         self.grp = q_heads // kv_heads
-        # P1: segmentation, shared by all layers and heads (Alg. 1 line 2).
-        self.off = [segment(self.tokens[b], self.bset, self.tau) for b in range(self.B)]
+        # P1: segmentation, shared by all layers and heads (Alg. 1 line 2), or a NEXT-3 / NEXT-4 variant
+        self.bucket_mode, self.chunk_size, self.outlier_n = bucket_mode, chunk_size, outlier_n
+        self.query_mode, self.fill_mode = query_mode, fill_mode
+        L = self.tokens.shape[1]
+        self.off = []
+        for b in range(self.B):
+            off = segment(self.tokens[b], self.bset, self.tau)
+            if bucket_mode == self.BUCKETS_EQUAL:
+                off = equal_chunks(L, len(off) - 1, self.tau)
+            elif bucket_mode == self.BUCKETS_QUEST:
+                off = np.minimum(np.arange(0, L + chunk_size, chunk_size), L).astype(np.int32)
+                off = np.unique(off)
+            elif outlier_n > 0:
+                T = outlier_threshold(off, outlier_n)
+                off = segment(self.tokens[b], self.bset, min(self.tau, T))
+            self.off.append(off)
         self.N, self.r = int(obs_window), float(semantic_factor)
         self.E = {}  # layer -> list[b][g] of E bits
         self.K = {}
@@ -259,7 +337,10 @@ class Oracle:
         of each sentence (line 6), and the retained pool kept for retrieval (line 7)."""
         if q_window is None:
             self.K[layer], self.V[layer] = K_bits, V_bits
-            self.E[layer] = [[embed(K_bits[b, g], self.off[b]) for g in range(self.G)] for b in range(self.B)]
+            if self.bucket_mode == self.BUCKETS_QUEST:  # page bounds instead of Eq. 1 means
+                self.E[layer] = [[quest_meta(K_bits[b, g], self.chunk_size) for g in range(self.G)] for b in range(self.B)]
+            else:
+                self.E[layer] = [[embed(K_bits[b, g], self.off[b]) for g in range(self.G)] for b in range(self.B)]
             return
         k = retained_count(self.r, self.tau)
         al, kp, lo, sd, Kp, Vp = [], [], [], [], [], []
@@ -287,11 +368,18 @@ class Oracle:
             Sq = self.Sq[layer, b]
             cnt = self.cnt[layer, b : b + 1]
             qbar = qs_append_mean(Sq, cnt, q_bits[b])
+            if self.query_mode == 1:  # NEXT-3 current-token query (Sec. 6.2)
+                qbar = synth_free_bf16_to_f32(q_bits[b])
             sb, ib, nb = [], [], []
             for g in range(self.G):
-                qt = group_query(qbar, self.grp, g)
-                sc = score(qt, self.E[layer][b][g])
-                sel, n = select(sc, self.offsets(layer, b), self.tau)
+                if self.bucket_mode == self.BUCKETS_QUEST:  # Quest ranks by the current query's bound
+                    mn, mx = self.E[layer][b][g]
+                    sc = quest_score(q_bits[b, g * self.grp:(g + 1) * self.grp], mn, mx)
+                else:
+                    qt = group_query(qbar, self.grp, g)
+                    sc = score(qt, self.E[layer][b][g])
+                fn = select_skip if self.fill_mode == 1 else select
+                sel, n = fn(sc, self.offsets(layer, b), self.tau)
                 sb.append(sc)
                 ib.append(sel)
                 nb.append(n)

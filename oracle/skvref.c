@@ -385,6 +385,134 @@ int32_t skvref_retained_buckets(const int32_t* off, int32_t S, const int32_t* ke
     return S2;
 }
 
+/* ---------------------------------------- NEXT-3: paper variants on the same path */
+
+/*
+ * Equal-size chunking, Sec. 6.1 "Sentence chunking": "perform equal-sized chunking based on
+ * the total number of sentences, dividing the text uniformly".  Reading A26: as many chunks as the
+ * prompt has sentences, each of len = min(tau, ceil(L / S)) tokens (the last one shorter).
+ * off: out [L+1]; returns the number of chunks.
+ */
+int32_t skvref_equal_chunks(int32_t L, int32_t S, int32_t tau, int32_t* off) {
+    int32_t len = (L + S - 1) / S;
+    if (len > tau) len = tau;
+    if (len < 1) len = 1;
+    int32_t n = 0;
+    off[0] = 0;
+    for (int32_t a = 0; a < L; a += len) {
+        n += 1;
+        off[n] = (a + len < L) ? a + len : L;
+    }
+    return n;
+}
+
+/*
+ * Outlier split, App. "Effect of Sentence Length": "compute the mean and standard deviation
+ * of sentence lengths in the input, and if a sentence exceeds mean + n x std, split it into smaller
+ * sub-spans".  Reading A27: population statistics over the prompt's S sentences; the threshold is
+ * T = floor(mean + n * std), evaluated as floor((L + n * sqrt(S * sum(len^2) - L^2)) / S) in IEEE
+ * fp64 from exact integer sums (the same value as mean + n*std, in one written order); sentences
+ * longer than T are cut into pieces of T tokens (the last piece shorter) -- segmentation with a cap
+ * of min(tau, T).  Returns T (>= 1).
+ */
+int32_t skvref_outlier_threshold(const int32_t* off, int32_t S, double n) {
+    int64_t L = off[S] - off[0], sq = 0;
+    for (int32_t s = 0; s < S; ++s) {
+        int64_t len = off[s + 1] - off[s];
+        sq += len * len;
+    }
+    double var_s2 = (double)(S * sq - L * L); /* S^2 * variance, exact in int64 for these sizes */
+    double t = floor(((double)L + n * sqrt(var_s2)) / (double)S);
+    if (t < 1.0) t = 1.0;
+    if (t > 2147483647.0) t = 2147483647.0;
+    return (int32_t)t;
+}
+
+/*
+ * Skip-and-continue budget fill (reading A13's alternative to the maximal prefix
+ * of P:444): walk the ranking (score desc, index asc, A14); take every sentence that still fits the
+ * remaining budget, skip the ones that do not, continue to the end.  Outputs as skvref_select.
+ */
+int32_t skvref_select_skip(const float* score, const int32_t* off, int32_t S, int32_t tau, int32_t* ids,
+                           int32_t* ntok) {
+    uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(S > 0 ? S : 1));
+    for (int32_t s = 0; s < S; ++s)
+        keys[s] = ((uint64_t)ordered_u32(score[s]) << 32) | (uint64_t)(0xffffffffu - (uint32_t)s);
+    qsort(keys, (size_t)S, sizeof(uint64_t), cmp_key_desc);
+    int32_t count = 0, tot = 0;
+    for (int32_t r = 0; r < S; ++r) {
+        int32_t s = (int32_t)(0xffffffffu - (uint32_t)(keys[r] & 0xffffffffu));
+        int32_t n = off[s + 1] - off[s];
+        if (tot + n > tau) continue;
+        tot += n;
+        ids[count++] = s;
+    }
+    qsort(ids, (size_t)count, sizeof(int32_t), cmp_i32_asc);
+    free(keys);
+    *ntok = tot;
+    return count;
+}
+
+/* --------------------------------------- NEXT-4: Quest fixed pages (App. Quest) */
+
+/*
+ * Quest page metadata (the comparison system of App. "Quest Sensitivity to Chunk Size", P:653-660:
+ * "divides the context into fixed-length chunks"; per-dimension min/max keys as in Quest,
+ * SURVEY 8(f) NEXT-4): page p = tokens [p*P, min(L, (p+1)*P)); mn/mx[p][j] = min/max over the page's
+ * keys of dimension j (exact: bf16 in, bf16 out).  K: bf16 bits [L][d]; mn, mx: bf16 bits [npages][d].
+ */
+void skvref_quest_meta(const uint16_t* K, int32_t L, int32_t d, int32_t P, uint16_t* mn, uint16_t* mx) {
+    int32_t np = (L + P - 1) / P;
+    for (int32_t p = 0; p < np; ++p) {
+        int32_t a = p * P, b = (a + P < L) ? a + P : L;
+        for (int32_t j = 0; j < d; ++j) {
+            uint16_t lo = K[(int64_t)a * d + j], hi = lo;
+            for (int32_t t = a + 1; t < b; ++t) {
+                uint16_t v = K[(int64_t)t * d + j];
+                if (bf16_to_f32(v) < bf16_to_f32(lo)) lo = v;
+                if (bf16_to_f32(v) > bf16_to_f32(hi)) hi = v;
+            }
+            mn[(int64_t)p * d + j] = lo;
+            mx[(int64_t)p * d + j] = hi;
+        }
+    }
+}
+
+/*
+ * Quest criticality bound of every page for the query heads of one KV head (SPEC quest_rank_pages:
+ * "page score = sum_h sum_dim max(q.min_key, q.max_key) per coordinate"), with the current token's
+ * query (Quest ranks by q_t).  Canonical fp32 order (reading A28): t_j = max(q_j * mn_j, q_j * mx_j)
+ * (IEEE products); per head: d/8 lanes, lane l: p = t[8l], then p = p + t[8l+i] for i = 1..7; then
+ * for w = d/16, ..., 1: p_l = p_l + p_{l+w}; u_h = p_0; the heads summed in ascending h.
+ * q: bf16 bits [grp][d]; mn, mx: bf16 bits [np][d]; score: fp32 [np].
+ */
+void skvref_quest_score(const uint16_t* q, int32_t grp, const uint16_t* mn, const uint16_t* mx, int32_t np,
+                        int32_t d, float* score) {
+    float p[64];
+    int32_t lanes = d / 8;
+    for (int32_t s = 0; s < np; ++s) {
+        float U = 0.0f;
+        for (int32_t h = 0; h < grp; ++h) {
+            for (int32_t l = 0; l < lanes; ++l) {
+                float acc = 0.0f;
+                for (int32_t i = 0; i < 8; ++i) {
+                    int32_t j = 8 * l + i;
+                    float qj = bf16_to_f32(q[(int64_t)h * d + j]);
+                    float a = qj * bf16_to_f32(mn[(int64_t)s * d + j]);
+                    float b = qj * bf16_to_f32(mx[(int64_t)s * d + j]);
+                    float t = a > b ? a : b;
+                    acc = (i == 0) ? t : acc + t;
+                }
+                p[l] = acc;
+            }
+            for (int32_t w = lanes / 2; w >= 1; w /= 2)
+                for (int32_t l = 0; l < w; ++l) p[l] = p[l] + p[l + w];
+            U = (h == 0) ? p[0] : U + p[0];
+        }
+        score[s] = U;
+    }
+}
+
 /* ------------------------------------------------------------ accounting */
 
 /*
