@@ -41,10 +41,13 @@ typedef enum {
     SKV_OK = 0,
     SKV_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, non-positive size, Hq % G != 0, shard out of range,
                                      tau < 1, r < 1, L < 1 or L > max_context, n_boundary < 1 or > 64,
-                                     K/V not 16-byte aligned, semantic_factor/token_budget != cfg */
+                                     K/V not 16-byte aligned, semantic_factor/token_budget != cfg, an unknown
+                                     bucket/query/fill mode, a Quest page outside [1, tau], outlier_n < 0 or
+                                     outlier_n > 0 with non-sentence buckets */
     SKV_ERR_STATE = 2,            /* layer out of range, decode before that layer's prefill, prefill of
                                      layer > 0 before layer 0 of the same prompt */
-    SKV_ERR_UNSUPPORTED = 3,      /* head_dim not in {64, 128}; grp not in {1, 2, 4, 8}; obs_window N > 0
+    SKV_ERR_UNSUPPORTED = 3,      /* head_dim not in {64, 128}; grp not in {1, 2, 4, 8}; retention with Quest
+                                     pages; obs_window N > 0
                                      with N * grp not a multiple of 16 or above 256 (the window rows of
                                      one KV head form the N side of one tensor-core MMA) */
     SKV_ERR_CUDA = 4,             /* CUDA launch / asynchronous failure (sticky; see last_error) */
@@ -61,6 +64,24 @@ typedef enum {
                           previous and the current selection (2*tau rows); sentences selected again are
                           re-read from HBM, the others fetched from host memory. */
 } skv_residency;
+
+/* what a bucket is, which query ranks them, how the budget is filled */
+typedef enum {
+    SKV_BUCKETS_SENTENCE = 0, /* sentences at the boundary tokens (P1) */
+    SKV_BUCKETS_EQUAL = 1,    /* NEXT-3 equal-size chunks, as many as the prompt has sentences, each
+                                 min(tau, ceil(L / S)) tokens (Sec. 6.1 ablation; reading A26) */
+    SKV_BUCKETS_QUEST = 2     /* NEXT-4 Quest: fixed pages of chunk_size tokens ranked by the bound
+                                 sum_h sum_j max(q_j min_j, q_j max_j) of the current query over each
+                                 page's per-dimension min / max keys (App. Quest; reading A28) */
+} skv_bucket_mode;
+typedef enum {
+    SKV_QUERY_MEAN = 0,       /* Eq. 2 mean of the sentence cache Q_s */
+    SKV_QUERY_CURRENT = 1     /* NEXT-3 current token's query (Sec. 6.2 ablation) */
+} skv_query_mode;
+typedef enum {
+    SKV_FILL_PREFIX = 0,      /* maximal prefix of the ranking that fits tau (reading A13) */
+    SKV_FILL_SKIP = 1         /* NEXT-3 skip-and-continue: walk the whole ranking, take what still fits */
+} skv_fill_mode;
 
 typedef struct {
     int32_t batch;           /* B: sequences in the global batch */
@@ -82,6 +103,13 @@ typedef struct {
     int32_t kv_head_count;
     int32_t batch_begin;     /* this rank's batch shard [begin, begin+count); 0, B = all */
     int32_t batch_count;
+    int32_t bucket_mode;     /* skv_bucket_mode (default SKV_BUCKETS_SENTENCE) */
+    int32_t chunk_size;      /* SKV_BUCKETS_QUEST: page size in tokens, 1 <= chunk_size <= tau (16, 32 in the paper) */
+    float outlier_n;         /* NEXT-3 outlier split (App. "Effect of Sentence Length"; reading A27):
+                                > 0 cuts every sentence longer than T = floor(mean + outlier_n * std) of the
+                                prompt's sentence lengths into pieces of T tokens; 0 = off (SENTENCE buckets only) */
+    int32_t query_mode;      /* skv_query_mode (default SKV_QUERY_MEAN; Quest always ranks by the current query) */
+    int32_t fill_mode;       /* skv_fill_mode (default SKV_FILL_PREFIX) */
 } skv_config;
 
 /* Fills cfg with defaults (shard = everything, device residency, r = 2, obs_window = 0). */
@@ -115,7 +143,10 @@ skv_status sentencekv_sync(skv_ctx* ctx);
  *      on an internal copy stream ordered after the caller's stream; the caller may free K/V
  *      after sentencekv_sync().  SKV_KV_DEVICE: the ctx borrows K and V (no copy).
  *
- * token_ids     device int32 [batch_count][L]  (layer 0 only; ignored for layer > 0, may be NULL)
+ * token_ids     device int32 [batch_count][L]  (layer 0 only; ignored for layer > 0 and for Quest pages,
+ *               may then be NULL).  NEXT-3 / NEXT-4 bucket variants replace P1 by equal chunks, outlier-split
+ *               sentences or Quest pages (see skv_config.bucket_mode / outlier_n); Quest replaces P2's
+ *               Eq. 1 means by the pages' min / max keys.
  * L             prompt length, 1 <= L <= max_context; identical for every layer of a prompt
  * boundary_ids  host int32 [n_boundary], 1 <= n_boundary <= 64: the punctuation token-id set
  *               (layer 0 only; ignored for layer > 0)

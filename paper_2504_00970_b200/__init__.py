@@ -28,6 +28,9 @@ LIB_PATH = os.environ.get("SKV_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 SKV_OK, SKV_ERR_INVALID_ARGUMENT, SKV_ERR_STATE, SKV_ERR_UNSUPPORTED, SKV_ERR_CUDA, SKV_ERR_OUT_OF_MEMORY = range(6)
 SKV_KV_DEVICE, SKV_KV_HOST = 0, 1
+SKV_BUCKETS_SENTENCE, SKV_BUCKETS_EQUAL, SKV_BUCKETS_QUEST = 0, 1, 2
+SKV_QUERY_MEAN, SKV_QUERY_CURRENT = 0, 1
+SKV_FILL_PREFIX, SKV_FILL_SKIP = 0, 1
 _STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "STATE", 3: "UNSUPPORTED", 4: "CUDA", 5: "OUT_OF_MEMORY"}
 
 
@@ -40,6 +43,8 @@ class SkvConfig(ctypes.Structure):
         ("token_budget", ctypes.c_int32), ("semantic_factor", ctypes.c_float), ("obs_window", ctypes.c_int32),
         ("residency", ctypes.c_int32), ("device", ctypes.c_int32), ("kv_head_begin", ctypes.c_int32),
         ("kv_head_count", ctypes.c_int32), ("batch_begin", ctypes.c_int32), ("batch_count", ctypes.c_int32),
+        ("bucket_mode", ctypes.c_int32), ("chunk_size", ctypes.c_int32), ("outlier_n", ctypes.c_float),
+        ("query_mode", ctypes.c_int32), ("fill_mode", ctypes.c_int32),
     ]
 
 
@@ -177,12 +182,15 @@ class SentenceKV:
 
     def __init__(self, batch, layers, q_heads, kv_heads, head_dim, max_context, token_budget,
                  semantic_factor=2.0, residency=SKV_KV_DEVICE, device=0, kv_head_begin=0, kv_head_count=0,
-                 batch_begin=0, batch_count=0, obs_window=0):
+                 batch_begin=0, batch_count=0, obs_window=0, bucket_mode=0, chunk_size=0, outlier_n=0.0,
+                 query_mode=0, fill_mode=0):
         self.cfg = sentencekv_config_default(
             batch=batch, layers=layers, q_heads=q_heads, kv_heads=kv_heads, head_dim=head_dim,
             max_context=max_context, token_budget=token_budget, semantic_factor=semantic_factor,
             residency=residency, device=device, kv_head_begin=kv_head_begin, kv_head_count=kv_head_count,
-            batch_begin=batch_begin, batch_count=batch_count, obs_window=obs_window)
+            batch_begin=batch_begin, batch_count=batch_count, obs_window=obs_window, bucket_mode=bucket_mode,
+            chunk_size=chunk_size, outlier_n=outlier_n, query_mode=query_mode, fill_mode=fill_mode)
+        self.quest = bucket_mode == SKV_BUCKETS_QUEST
         self.N = obs_window
         self.ctx = sentencekv_create(self.cfg)
         self.B = batch_count or (batch - batch_begin)
@@ -238,8 +246,10 @@ class SentenceKV:
         return out
 
     def embeddings(self, layer, stream=None):
+        """[B][G][S_max][d] Eq. 1 means, or (Quest) [B][G][S_max][2][d] page (min, max) keys."""
         S = self.capacity()
-        out = torch.empty((self.B, self.G, S, self.d), dtype=torch.bfloat16, device=self.device)
+        shape = (self.B, self.G, S, 2, self.d) if self.quest else (self.B, self.G, S, self.d)
+        out = torch.empty(shape, dtype=torch.bfloat16, device=self.device)
         _check(self.ctx, lib.sentencekv_copy_embeddings(self.ctx, layer, _ptr(out), _stream(stream)))
         return out
 

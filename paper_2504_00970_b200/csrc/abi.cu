@@ -194,6 +194,14 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         return SKV_ERR_INVALID_ARGUMENT;
     const int grp = cfg.q_heads / cfg.kv_heads;
     if (cfg.obs_window < 0) return SKV_ERR_INVALID_ARGUMENT;
+    // NEXT-3 / NEXT-4 modes
+    if (cfg.bucket_mode < SKV_BUCKETS_SENTENCE || cfg.bucket_mode > SKV_BUCKETS_QUEST ||
+        (cfg.bucket_mode == SKV_BUCKETS_QUEST && (cfg.chunk_size < 1 || cfg.chunk_size > cfg.token_budget)) ||
+        !(cfg.outlier_n >= 0.0f) || (cfg.outlier_n > 0.0f && cfg.bucket_mode != SKV_BUCKETS_SENTENCE) ||
+        (cfg.query_mode != SKV_QUERY_MEAN && cfg.query_mode != SKV_QUERY_CURRENT) ||
+        (cfg.fill_mode != SKV_FILL_PREFIX && cfg.fill_mode != SKV_FILL_SKIP))
+        return SKV_ERR_INVALID_ARGUMENT;
+    if (cfg.obs_window > 0 && cfg.bucket_mode == SKV_BUCKETS_QUEST) return SKV_ERR_UNSUPPORTED;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
         (cfg.obs_window > 0 && !skv::retain_supported(cfg.head_dim, cfg.obs_window, grp)))
         return SKV_ERR_UNSUPPORTED;
@@ -256,6 +264,7 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     dfree(c->bset);
     dfree(c->unit_cand);
     dfree(c->ret_scratch);
+    dfree(c->cap_dev);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -336,7 +345,8 @@ static skv_status switch_host_path(skv_ctx* c, skv::LayerState& ls, int path, cu
 static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
     const size_t B = c->B, G = c->G, d = c->d, tau = c->tau, U = B * G;
     for (auto& ls : c->layer) {
-        SKV_CUDA(c, dalloc(&ls.E, B * G * Smax * d));
+        // Quest pages keep (min, max) per page instead of one mean
+        SKV_CUDA(c, dalloc(&ls.E, B * G * Smax * d * (c->cfg.bucket_mode == SKV_BUCKETS_QUEST ? 2 : 1)));
         SKV_CUDA(c, dalloc(&ls.scores, B * G * Smax));
         skv::SelBufs& sb = ls.sel;
         sb.units = (int)U;
@@ -384,9 +394,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
     if (N > 0 && (q_window == nullptr || !aligned16(q_window)))
         return fail(c, SKV_ERR_INVALID_ARGUMENT, "cfg.obs_window = %d needs the window queries (16-byte aligned)", N);
     if (N > 0 && L <= N) return fail(c, SKV_ERR_INVALID_ARGUMENT, "L=%d must exceed the observation window N=%d", L, N);
+    const bool quest = c->cfg.bucket_mode == SKV_BUCKETS_QUEST;
     if (layer == 0) {
-        if (!token_ids) return fail(c, SKV_ERR_INVALID_ARGUMENT, "token_ids is NULL");
-        if (!boundary_ids || n_boundary < 1 || n_boundary > skv::kMaxBoundary)
+        if (!quest && !token_ids) return fail(c, SKV_ERR_INVALID_ARGUMENT, "token_ids is NULL");
+        if ((!quest || boundary_ids) && (!boundary_ids || n_boundary < 1 || n_boundary > skv::kMaxBoundary))
             return fail(c, SKV_ERR_INVALID_ARGUMENT, "boundary set must hold 1..%d ids", skv::kMaxBoundary);
     } else if (c->L != L || !c->layer[0].prefilled) {
         return fail(c, SKV_ERR_STATE, "prefill of layer %d before layer 0 of a prompt of length %d", layer, L);
@@ -401,13 +412,33 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             c->L = L;
             c->off_stride = L + 1;
         }
-        SKV_CUDA(c, cudaMemcpyAsync(c->bset, boundary_ids, sizeof(int32_t) * n_boundary, cudaMemcpyHostToDevice, st));
-        c->n_bset = n_boundary;
+        if (boundary_ids && n_boundary > 0) {
+            SKV_CUDA(c, cudaMemcpyAsync(c->bset, boundary_ids, sizeof(int32_t) * n_boundary, cudaMemcpyHostToDevice, st));
+            c->n_bset = n_boundary;
+        } else {  // Quest without a boundary set: no input token resets Q_s (Quest does not use it)
+            c->n_bset = 0;
+        }
         cudaEvent_t pa = prof_begin(c, st);
-        SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off, c->off_stride,
-                                        c->S_dev, st));
+        if (quest) {  // NEXT-4: fixed pages of chunk_size tokens
+            SKV_CUDA(c, skv::launch_chunks(c->B, L, c->tau, c->cfg.chunk_size, c->off, c->off_stride, c->S_dev, st));
+            c->launches += 1;
+        } else {
+            SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off, c->off_stride,
+                                            c->S_dev, nullptr, st));
+            c->launches += 1;
+            if (c->cfg.outlier_n > 0.0f) {  // NEXT-3 outlier split: re-segment under the per-prompt cap T
+                if (!c->cap_dev) SKV_CUDA(c, dalloc(&c->cap_dev, (size_t)c->B));
+                SKV_CUDA(c, skv::launch_outlier_cap(c->off, c->off_stride, c->S_dev, c->B, (double)c->cfg.outlier_n,
+                                                    c->cap_dev, st));
+                SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off,
+                                                c->off_stride, c->S_dev, c->cap_dev, st));
+                c->launches += 2;
+            } else if (c->cfg.bucket_mode == SKV_BUCKETS_EQUAL) {  // NEXT-3 equal chunks, as many as sentences
+                SKV_CUDA(c, skv::launch_chunks(c->B, L, c->tau, 0, c->off, c->off_stride, c->S_dev, st));
+                c->launches += 1;
+            }
+        }
         prof_end(c, SKV_K_SEGMENT, pa, st);
-        c->launches += 1;
         SKV_CUDA(c, cudaMemcpyAsync(c->S_host.data(), c->S_dev, sizeof(int32_t) * c->B, cudaMemcpyDeviceToHost, st));
         SKV_CUDA(c, cudaStreamSynchronize(st));
         int Smax = 1;
@@ -463,6 +494,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         const size_t need = skv::retain_scratch_floats(c->B, c->G, L, N, c->grp);
         if (c->ret_scratch_n < need) {
             dfree(c->ret_scratch);
+    dfree(c->cap_dev);
             c->ret_scratch_n = 0;
             SKV_CUDA(c, dalloc(&c->ret_scratch, need));
             c->ret_scratch_n = need;
@@ -484,9 +516,12 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         srcK = ls.PK;
         srcV = ls.PV;
     } else {
-        // ---- P2: Eq. 1 sentence embeddings of this layer ----
+        // ---- P2: Eq. 1 sentence embeddings of this layer (Quest: the pages' min / max keys) ----
         cudaEvent_t pa = prof_begin(c, st);
-        SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
+        if (quest)
+            SKV_CUDA(c, skv::launch_quest_meta(Kb, c->B, c->G, L, c->d, c->cfg.chunk_size, c->S_dev, c->Smax, ls.E, st));
+        else
+            SKV_CUDA(c, skv::launch_compress(Kb, c->B, c->G, L, c->d, c->off, c->off_stride, c->S_dev, c->Smax, ls.E, st));
         prof_end(c, SKV_K_COMPRESS, pa, st);
         c->launches += 1;
         ls.retained = false;
@@ -550,13 +585,22 @@ SKV_API skv_status sentencekv_decode_select(skv_ctx* c, int32_t layer, const voi
         if (ps != SKV_OK) return ps;
     }
     cudaEvent_t pa = prof_begin(c, st);
-    SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, v.S, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
+    if (c->cfg.bucket_mode == SKV_BUCKETS_QUEST)
+        SKV_CUDA(c, skv::launch_quest_score(qb, ls.E, v.S, c->B, c->G, c->grp, c->d, c->Smax, ls.scores, st));
+    else
+        SKV_CUDA(c, skv::launch_score(qb, ls.Sq, ls.cnt, ls.E, v.S, c->B, c->G, c->grp, c->d, c->Smax, ls.scores,
+                                      c->cfg.query_mode, st));
     prof_end(c, SKV_K_SCORE, pa, st);
     pa = prof_begin(c, st);
     SKV_CUDA(c, skv::launch_select(ls.scores, v.off, v.off_stride, v.S, c->B, c->G, c->Smax, c->tau, ls.sel, false,
                                    sel_ids, sel_count, sel_tokens, v.sid, v.sid_stride, st));
-    prof_end(c, SKV_K_SELECT, pa, st);
     c->launches += 2;
+    if (c->cfg.fill_mode == SKV_FILL_SKIP) {  // NEXT-3 skip-and-continue on top of the prefix
+        SKV_CUDA(c, skv::launch_skip_fill(ls.scores, v.off, v.off_stride, v.S, c->B, c->G, c->Smax, c->tau, ls.sel,
+                                          false, sel_ids, sel_count, sel_tokens, v.sid, v.sid_stride, st));
+        c->launches += 1;
+    }
+    prof_end(c, SKV_K_SELECT, pa, st);
     ls.selected = true;
     ls.input_token = input_token;
     return SKV_OK;
@@ -576,7 +620,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
     const LayerView v = layer_view(c, ls);
     const bool host = v.host;
-    if (skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
+    const bool unit_path = c->cfg.bucket_mode != SKV_BUCKETS_QUEST && c->cfg.fill_mode == SKV_FILL_PREFIX;
+    if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
         if (host) {
@@ -601,6 +646,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.off_stride = v.off_stride;
         a.sid = v.sid;
         a.sid_stride = v.sid_stride;
+        a.qmode = c->cfg.query_mode;
         a.B = c->B;
         a.G = c->G;
         a.Smax = c->Smax;
@@ -625,8 +671,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         ls.input_token = input_token;
         return SKV_OK;
     }
-    // capacity fallback (Smax > 16384 sentences or a selection too large for the step kernel's
-    // shared memory): the score, select and attend kernels of the split calls
+    // Quest pages, skip-and-continue fill, or the capacity fallback (Smax > 16384 sentences or a
+    // selection too large for the step kernel's shared memory): the kernels of the split calls
     skv_status s = sentencekv_decode_select(c, layer, q, input_token, sel_ids, sel_count, sel_tokens, stream_);
     if (s != SKV_OK) return s;
     return sentencekv_decode_attend(c, layer, q, out, stream_);
@@ -691,7 +737,9 @@ SKV_API skv_status sentencekv_copy_embeddings(skv_ctx* c, int32_t layer, void* E
     if (!c || !E_out) return SKV_ERR_INVALID_ARGUMENT;
     if (layer < 0 || layer >= c->cfg.layers || !c->layer[layer].prefilled) return fail(c, SKV_ERR_STATE, "layer not prefilled");
     DeviceGuard dg(c->cfg.device);
-    SKV_CUDA(c, cudaMemcpyAsync(E_out, c->layer[layer].E, sizeof(__nv_bfloat16) * c->B * c->G * c->Smax * c->d,
+    SKV_CUDA(c, cudaMemcpyAsync(E_out, c->layer[layer].E,
+                                sizeof(__nv_bfloat16) * c->B * c->G * c->Smax * c->d *
+                                    (c->cfg.bucket_mode == SKV_BUCKETS_QUEST ? 2 : 1),
                                 cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream_)));
     return SKV_OK;
 }

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kScThreads) score_kernel(const __nv_bfloat16* 
                                                            const int32_t* __restrict__ cnt,
                                                            const __nv_bfloat16* __restrict__ E,
                                                            const int32_t* __restrict__ S, int G, int Smax,
-                                                           int chunk, float* __restrict__ scores) {
+                                                           int chunk, float* __restrict__ scores, int qmode) {
     constexpr int LPS = D / 8;                   // lanes per sentence
     constexpr int GPW = 32 / LPS;                // sentences per warp step
     constexpr int TS = kScTileBytes / (D * 2);   // sentences per tile (64 or 128)
@@ -78,9 +78,10 @@ __global__ void __launch_bounds__(kScThreads) score_kernel(const __nv_bfloat16* 
             sv[h] = Sq[idx];
             qv[h] = __bfloat162float(q[idx]);
         }
-        float acc = __fdiv_rn(__fadd_rn(sv[0], qv[0]), c);
+        // qmode 1 (NEXT-3, Sec. 6.2): rank by the current token's query, qbar_h = q_h
+        float acc = qmode ? qv[0] : __fdiv_rn(__fadd_rn(sv[0], qv[0]), c);
 #pragma unroll
-        for (int h = 1; h < GRP; ++h) acc = __fadd_rn(acc, __fdiv_rn(__fadd_rn(sv[h], qv[h]), c));
+        for (int h = 1; h < GRP; ++h) acc = __fadd_rn(acc, qmode ? qv[h] : __fdiv_rn(__fadd_rn(sv[h], qv[h]), c));
         qt[tid] = acc;
     }
     __syncthreads();
@@ -122,16 +123,16 @@ __global__ void __launch_bounds__(kScThreads) score_kernel(const __nv_bfloat16* 
 template <int D, int GRP>
 static cudaError_t launch_score_t(dim3 grid, int chunk, cudaStream_t st, const __nv_bfloat16* q, const float* Sq,
                                   const int32_t* cnt, const __nv_bfloat16* E, const int32_t* S, int G, int Smax,
-                                  float* scores) {
+                                  float* scores, int qmode) {
     const size_t smem = (size_t)kScStages * kScTileBytes;
     cudaError_t e = ensure_smem((const void*)score_kernel<D, GRP>, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(false, score_kernel<D, GRP>, grid, dim3(kScThreads), smem, st, q, Sq, cnt, E, S, G, Smax, chunk,
-                      scores);
+                      scores, qmode);
 }
 
 cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t* cnt, const __nv_bfloat16* E,
-                         const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores,
+                         const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores, int qmode,
                          cudaStream_t st) {
     // ~3 CTAs per SM: split each (b, g) unit's sentences into `splits` tile-aligned ranges.
     const int TS = kScTileBytes / (d * 2);
@@ -141,7 +142,7 @@ cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t*
     chunk = max(TS, (chunk + TS - 1) / TS * TS);
     splits = (Smax + chunk - 1) / chunk;
     dim3 grid(splits, G, B);
-#define SKV_SC(DV, GV) return launch_score_t<DV, GV>(grid, chunk, st, q, Sq, cnt, E, S, G, Smax, scores)
+#define SKV_SC(DV, GV) return launch_score_t<DV, GV>(grid, chunk, st, q, Sq, cnt, E, S, G, Smax, scores, qmode)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_SC(128, 1);

@@ -222,8 +222,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  int off_stride, int G, int Smax, float* __restrict__ scores, SelBufs sel, KvSrc kv, HostCache hc,
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, float* __restrict__ out,
                  int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
-                 int32_t* __restrict__ out_tokens, const int32_t* __restrict__ sid, int sid_stride, float scale_log2,
-                 int trace_idx) {
+                 int32_t* __restrict__ out_tokens, const int32_t* __restrict__ sid, int sid_stride, int qmode,
+                 float scale_log2, int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
     constexpr int GPW = 32 / TPS;               // sentences per warp step
@@ -345,7 +345,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         for (int h = 0; h < GRP; ++h) {
             const float sum = __fadd_rn(sv[h], qv[h]);
             sqsum[h * D + tid] = sum;
-            const float qb = __fdiv_rn(sum, c);
+            const float qb = qmode ? qv[h] : __fdiv_rn(sum, c);  // qmode 1: current token's query (NEXT-3)
             acc = h == 0 ? qb : __fadd_rn(acc, qb);
         }
         qt[tid] = acc;
@@ -1196,7 +1196,7 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), a.out, a.out_ids,
-                      a.out_count, a.out_tokens, a.sid, a.sid_stride, scale_log2, trace_counter++);
+                      a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, scale_log2, trace_counter++);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {

@@ -15,10 +15,12 @@ namespace skv {
 __global__ void __launch_bounds__(1024) segment_kernel(const int32_t* __restrict__ tokens, int L,
                                                        const int32_t* __restrict__ bset, int nb, int tau,
                                                        int32_t* __restrict__ off, int off_stride,
-                                                       int32_t* __restrict__ S_out) {
+                                                       int32_t* __restrict__ S_out, const int32_t* __restrict__ cap_b) {
     __shared__ int32_t sb[kMaxBoundary];
     __shared__ int32_t ws[32];
     const int b = blockIdx.x;
+    // NEXT-3 outlier split: a per-prompt cap T below tau (reading A27); else the tau-cap (A5)
+    if (cap_b) tau = min(tau, max(1, cap_b[b]));
     const int32_t* tok = tokens + (size_t)b * L;
     int32_t* o = off + (size_t)b * off_stride;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = bset[i];
@@ -55,8 +57,8 @@ __global__ void __launch_bounds__(1024) segment_kernel(const int32_t* __restrict
 }
 
 cudaError_t launch_segment(const int32_t* tokens, int B, int L, const int32_t* bset, int nb, int tau,
-                           int32_t* off, int off_stride, int32_t* S, cudaStream_t st) {
-    segment_kernel<<<B, 1024, 0, st>>>(tokens, L, bset, nb, tau, off, off_stride, S);
+                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, cudaStream_t st) {
+    segment_kernel<<<B, 1024, 0, st>>>(tokens, L, bset, nb, tau, off, off_stride, S, cap_b);
     return cudaGetLastError();
 }
 

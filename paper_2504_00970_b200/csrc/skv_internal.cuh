@@ -115,6 +115,7 @@ struct skv_ctx {
 
     std::vector<skv::LayerState> layer;
     int4* unit_cand = nullptr;         // overflow scratch of the per-unit step kernel's candidate lists
+    int32_t* cap_dev = nullptr;        // NEXT-3 outlier split: per-prompt length cap [B]
     float* ret_scratch = nullptr;      // NEXT-1 pass A partials + row stats
     size_t ret_scratch_n = 0;
 
@@ -151,9 +152,27 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 bl
 }
 // ---- kernel launchers (each returns the cudaError_t of the launch) ----
 
-// P1: sentence offsets for B prompts.  tokens [B][L]; off [B][Smax_cap+1]; S [B].
+// P1: sentence offsets for B prompts.  tokens [B][L]; off [B][Smax_cap+1]; S [B]; cap_b [B] or
+// nullptr: a per-prompt length cap below tau (NEXT-3 outlier split).
 cudaError_t launch_segment(const int32_t* tokens, int B, int L, const int32_t* bset, int nb, int tau,
-                           int32_t* off, int off_stride, int32_t* S, cudaStream_t st);
+                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, cudaStream_t st);
+
+// ---- NEXT-3 / NEXT-4 bucket and ranking variants (variants.cu) ----
+// outlier split threshold T = floor((L + n * sqrt(S * sum len^2 - L^2)) / S) per prompt (reading A27)
+cudaError_t launch_outlier_cap(const int32_t* off, int off_stride, const int32_t* S, int B, double n, int32_t* cap,
+                               cudaStream_t st);
+// equal chunks (len = min(tau, ceil(L / S_b)), A26) or fixed pages (len = page > 0): off [B][stride], S [B]
+cudaError_t launch_chunks(int B, int L, int tau, int page, int32_t* off, int off_stride, int32_t* S, cudaStream_t st);
+// Quest page bounds: E [B][G][Smax][2][d] = (min, max) of each page's keys
+cudaError_t launch_quest_meta(const __nv_bfloat16* K, int B, int G, int L, int d, int page, const int32_t* S, int Smax,
+                              __nv_bfloat16* E, cudaStream_t st);
+// Quest scores [B][G][Smax]: sum_h sum_j max(q_j mn_j, q_j mx_j), current query (reading A28)
+cudaError_t launch_quest_score(const __nv_bfloat16* q, const __nv_bfloat16* E, const int32_t* S, int B, int G, int grp,
+                               int d, int Smax, float* scores, cudaStream_t st);
+// skip-and-continue fill on top of the prefix selection of launch_select (same outputs, rewritten)
+cudaError_t launch_skip_fill(const float* scores, const int32_t* off, int off_stride, const int32_t* S, int B, int G,
+                             int Smax, int tau, SelBufs sel, bool src_gathered, int32_t* out_ids, int32_t* out_count,
+                             int32_t* out_tokens, const int32_t* sid, int sid_stride, cudaStream_t st);
 
 // P2: E = bf16(mean of member keys).  K [B][G][L][d]; off [B][Smax+1]; E [B][G][Smax][d].
 cudaError_t launch_compress(const __nv_bfloat16* K, int B, int G, int L, int d, const int32_t* off,
@@ -161,7 +180,7 @@ cudaError_t launch_compress(const __nv_bfloat16* K, int B, int G, int L, int d, 
 
 // D1: scores [B][G][Smax] of qt_g against every sentence embedding.
 cudaError_t launch_score(const __nv_bfloat16* q, const float* Sq, const int32_t* cnt, const __nv_bfloat16* E,
-                         const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores,
+                         const int32_t* S, int B, int G, int grp, int d, int Smax, float* scores, int qmode,
                          cudaStream_t st);
 
 // D2: budgeted selection + Q_s state update (Sq += q or reset).
@@ -222,6 +241,7 @@ struct UnitArgs {
     int32_t* out_tokens;           // optional [B][G]
     const int32_t* sid;            // optional [B][sid_stride]: output ids = sid[b][selected bucket] (retention)
     int sid_stride;
+    int qmode;                     // 0 = Eq. 2 mean query, 1 = current token's query (NEXT-3)
 };
 bool unit_supported(int d, int grp, int Smax, int tau, int slots);
 int unit_page_tokens();
