@@ -69,6 +69,12 @@ def parse():
                     help="NEXT-1: importance-filtered retention at prefill (observation window of --obs-window "
                          "queries, top floor(r*tau) tokens kept in an HBM pool); decode ranks and attends the pool")
     ap.add_argument("--obs-window", type=int, default=32)
+    ap.add_argument("--buckets", choices=["sentence", "equal", "quest"], default="sentence",
+                    help="NEXT-3 equal-size chunks / NEXT-4 Quest pages instead of sentences")
+    ap.add_argument("--page", type=int, default=16, help="Quest page size (tokens)")
+    ap.add_argument("--outlier-n", type=float, default=0.0, help="NEXT-3 outlier split at mean + n*std (0 = off)")
+    ap.add_argument("--query", choices=["mean", "current"], default="mean", help="NEXT-3 current-token query")
+    ap.add_argument("--fill", choices=["prefix", "skip"], default="prefix", help="NEXT-3 skip-and-continue fill")
     ap.add_argument("--residency", choices=["device", "host"], default=None,
                     help="K/V residency (default: host for 8b-128k, which configs[2] specifies, else device)")
     return ap.parse_args()
@@ -84,7 +90,13 @@ def peaks():
 
 
 def config_dict(args, cfg, GB, extra=None):
-    d = {"workload": args.config + ("+retention" if getattr(args, "retention", False) else ""), "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
+    tags = [t for t, on in (("retention", getattr(args, "retention", False)),
+                            (f"{getattr(args, 'buckets', 'sentence')}" + (f"{args.page}" if getattr(args, "buckets", "") == "quest" else ""),
+                             getattr(args, "buckets", "sentence") != "sentence"),
+                            (f"outlier{getattr(args, 'outlier_n', 0)}", getattr(args, "outlier_n", 0) > 0),
+                            ("current-query", getattr(args, "query", "mean") == "current"),
+                            ("skip-fill", getattr(args, "fill", "prefix") == "skip")) if on]
+    d = {"workload": "+".join([args.config] + tags), "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
          "kv_heads": cfg["G"], "head_dim": cfg["d"], "context": cfg["L"], "token_budget": cfg["tau"],
          "median_sentence_tokens": cfg["median"]}
     d.update(extra or {})
@@ -258,8 +270,10 @@ def main():
     plan = parallel.plan(GB, G, Hq, world, rank, "batch" if args.shard == "batch" else "heads")
     Bl, Gl, Hl = plan.batch_count, plan.kv_head_count, plan.q_head_count
     b0, g0, h0 = plan.batch_begin, plan.kv_head_begin, plan.q_head_begin
-    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline and not args.retention
-    check = rank == 0 and world == 1 and not args.no_check and not args.retention
+    plain = (not args.retention and args.buckets == "sentence" and args.outlier_n == 0 and args.query == "mean"
+             and args.fill == "prefix")
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline and plain
+    check = rank == 0 and world == 1 and not args.no_check and plain
     N = args.obs_window if args.retention else 0
     keep_layers = [0, 1][:M] if (cpu_leg or check) else []
 
@@ -269,9 +283,12 @@ def main():
     tok_dev = torch.from_numpy(toks).to(dev)
     top_dev = torch.from_numpy(topics).to(dev)
     host = residency == "host"
+    variant = dict(bucket_mode={"sentence": 0, "equal": 1, "quest": 2}[args.buckets],
+                   chunk_size=args.page if args.buckets == "quest" else 0, outlier_n=args.outlier_n,
+                   query_mode=1 if args.query == "current" else 0, fill_mode=1 if args.fill == "skip" else 0)
     skv = skvlib.SentenceKV(layers=M, head_dim=d, max_context=L, token_budget=tau, device=local,
                             residency=skvlib.SKV_KV_HOST if host else skvlib.SKV_KV_DEVICE, obs_window=N,
-                            **plan.ctx_kwargs())
+                            **variant, **plan.ctx_kwargs())
     wgen = torch.Generator(device=dev)
     # ---------------- K/V generation + prefill (P1 segmentation, P2 embeddings, P3 offload in host
     # residency), per layer; in host residency the device K/V of a layer is freed once offloaded
@@ -467,43 +484,49 @@ def main():
     tok_hist = []
     torch.cuda.synchronize()
     torch.cuda._sleep(int(2e9 * 0.05))  # ~50 ms head start
+    lc0 = skv.launch_count()
     for _ in range(n_prof):
         load(take())
         body(with_tokens=True)
         tok_hist.append(sel_tok.sum())
     torch.cuda.synchronize()
+    launches_per_step = (skv.launch_count() - lc0) // n_prof
     ntok_sum = int(torch.stack(tok_hist).sum())
     prof = skv.profile_read()
     skv.set_profiling(False)
     S_tot = sum(S)
-    # algorithmic bytes per launch (one layer, this rank's Bl x Gl units); DESIGN.md section 9
-    kv_bytes = ntok_sum * d * 2 * 2 / max(1, prof["step"][1])  # selected K and V rows per launch
-    e_bytes = Gl * S_tot * d * 2                                 # bf16 sentence embeddings
+    unit_path = prof["step"][1] > 0  # one-launch step kernel; else the split kernels (Quest, skip fill)
+    # algorithmic bytes per layer (this rank's Bl x Gl units); DESIGN.md section 9
+    kv_bytes = ntok_sum * d * 2 * 2 / max(1, n_prof * M)        # selected K and V rows per layer
+    e_bytes = Gl * S_tot * d * 2 * (2 if args.buckets == "quest" else 1)  # bf16 embeddings (Quest: min + max)
     qo_bytes = Bl * Hl * d * (2 + 4 + 4 + 4)                     # q, Sq read + write, O
     unit_bytes = e_bytes + kv_bytes + Gl * S_tot * 4 * 2 + qo_bytes  # + scores written, offsets read
     kern = {}
-    ms_p, n_p = prof["step"]
-    kern["step"] = {"avg_us_isolated": round(ms_p / max(1, n_p) * 1e3, 3), "bytes_per_launch": int(unit_bytes)}
-    # achieved: algorithmic bytes per launch / average launch duration in the timed region = the
-    # graph replays' device time (CUDA events on the replay stream, input copies excluded) / launches
+    name = "step" if unit_path else "split(score+select+attend)"
+    iso = prof["step"] if unit_path else tuple(map(sum, zip(prof["score"], prof["select"], prof["attend"])))
+    kern[name] = {"avg_us_isolated": round(iso[0] / max(1, n_prof * M) * 1e3, 3), "bytes_per_launch": int(unit_bytes)}
+    # achieved: algorithmic bytes per layer / the layer's device time in the timed region = the graph
+    # replays' device time (CUDA events on the replay stream, input copies excluded) / (steps x layers)
     launches_timed = M * args.steps
     avg_us = kern_ms * 1e3 / launches_timed
-    kern["step"]["avg_us"] = round(avg_us, 3)
-    kern["step"]["gbs"] = round(unit_bytes / (avg_us / 1e6) / 1e9, 1)
-    kern["step"]["share"] = round(kern_ms / ms_total, 4)
+    kern[name]["avg_us"] = round(avg_us, 3)
+    kern[name]["gbs"] = round(unit_bytes / (avg_us / 1e6) / 1e9, 1)
+    kern[name]["share"] = round(kern_ms / ms_total, 4)
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and plain:
         # dram__bytes_read.sum + dram__bytes_write.sum per launch of the step kernel, from one
         # `ncu --set full` capture of this workload and residency (scripts/gpu_profile.sh)
         with open(tf) as f:
             traffic = json.load(f).get(f"step_{residency}")
-    roofline = {"bound": "hbm", "kernel": "unit_step_kernel (decode_unit.cu)", "achieved": kern["step"]["gbs"],
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(kern["step"]["gbs"] / hbm_peak, 4),
+    roofline = {"bound": "hbm", "kernel": "unit_step_kernel (decode_unit.cu)" if unit_path else
+                "score/quest_score + select (+ skip_fill) + attend_mma kernels per layer",
+                "achieved": kern[name]["gbs"],
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(kern[name]["gbs"] / hbm_peak, 4),
                 "traffic": traffic, "peak_kind": peak_kind,
                 "duration": "graph replays' device time in the timed region / (steps x layers)",
-                "per_unit": "per launch (one layer, all units): G*S*d*2 B (bf16 E) + sum(ntok)*d*2*2 B (selected "
-                            "K,V rows) + G*S*4*2 (scores written, offsets read) + B*Hq*d*14 (q, Sq r/w, O)"}
+                "per_unit": "per layer (all units): G*S*d*2 B (bf16 E; Quest pages: min + max) + sum(ntok)*d*2*2 B "
+                            "(selected K,V rows) + G*S*4*2 (scores written, offsets read) + B*Hq*d*14 (q, Sq r/w, O)"}
 
     # ---------------- the split call pair of SURVEY 8(b): decode_select + decode_attend per layer
     split = None
@@ -627,7 +650,7 @@ def main():
             "e2e": e2e,
             "split_calls": split,
             # kernels of this library per timed step: one unit_step_kernel per layer (decode_unit.cu)
-            "gpu_launches": M * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "prefill": {"ms": round(prefill_ms, 3), "K_bytes": int(Bl * Gl * L * d * 2 * M),
                         "segment_ms": round(prof_prefill["segment"][0], 3),

@@ -621,7 +621,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     const LayerView v = layer_view(c, ls);
     const bool host = v.host;
     const bool unit_path = c->cfg.bucket_mode != SKV_BUCKETS_QUEST && c->cfg.fill_mode == SKV_FILL_PREFIX;
-    if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0)) {
+    if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0, host ? ls.pc_pages : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
         if (host) {

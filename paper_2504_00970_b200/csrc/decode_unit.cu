@@ -109,7 +109,8 @@ constexpr int kUStages = 3;
 constexpr int kULocalCap = 2048;         // sentences per CTA (supported: Smax <= kUC * kULocalCap)
 constexpr int kUOwnCap = 256;            // own candidate list kept in shared memory (else global scratch)
 constexpr int kPage = 16;                // host residency: tokens per working-set page
-constexpr int kNeedCap = 256;            // host residency: pages of a selection tracked by the cache plan
+constexpr int kNeedCap = 384;            // host residency: pages of a selection tracked by the cache plan
+constexpr int kMaxPageWords = 512;       // host residency: page bitmap words (contexts up to 16384 pages)
 constexpr int kMaxSlots = 1024;          // host residency: working-set pages per unit
 constexpr uint32_t kEmpty = 0xffffffffu; // page-table entry of a page that is not resident
 constexpr int kUBins = 1024;
@@ -247,16 +248,18 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int32_t* sel_src = sel_tok + (tau + 1);                              // [tau]
     int32_t* sel_id = sel_src + tau;                                     // [tau]
     int2* rowtab = reinterpret_cast<int2*>(sel_tok + (3 * tau + 5) / 4 * 4);  // [rows per CTA] (source, write-through row)
-    // host residency: the page-cache plan of this step, in the ring behind the merge area
-    constexpr int kPlanOff = (int)((sizeof(USmemMerge<D>) + 127) / 128 * 128);
-    int* need = reinterpret_cast<int*>(smem_raw + kPlanOff);            // [kNeedCap] pages of the selection
+    // host residency: the page-cache plan of this step, in the keys / offsets area (local to this CTA
+    // and idle once the selection is made; the ring holds the merge area that other CTAs read)
+    int* need = reinterpret_cast<int*>(keys);                            // [kNeedCap] pages of the selection
     uint32_t* pslot = reinterpret_cast<uint32_t*>(need + kNeedCap);     // [kNeedCap] their page-table entries
     int* slotof = reinterpret_cast<int*>(pslot + kNeedCap);             // [kNeedCap] slot this step (-1 none)
     int* oldof = slotof + kNeedCap;                                     // [kNeedCap] page evicted for it
     uint32_t* rowbits = reinterpret_cast<uint32_t*>(oldof + kNeedCap);  // [kNeedCap] selected rows
     int* newj = reinterpret_cast<int*>(rowbits + kNeedCap);             // [kNeedCap] non-resident pages
     int* frees = newj + kNeedCap;                                       // [kNeedCap] their slots
-    static_assert(!HOST || kPlanOff + kNeedCap * 28 <= kUStages * kUTileBytes, "plan fits the ring");
+    uint32_t* pbits = reinterpret_cast<uint32_t*>(frees + kNeedCap);    // [kMaxPageWords] pages of the selection
+    uint32_t* pbase = pbits + kMaxPageWords;                            // [kMaxPageWords] rank of each word's first page
+    static_assert(kNeedCap * 28 + kMaxPageWords * 8 <= kULocalCap * 8, "plan fits the keys + offsets area");
 
     __shared__ uint64_t bar[kUStages];
     __shared__ float qt[D];
@@ -874,101 +877,123 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     // a CTA meets such a miss it plans the cache for the whole selection (identically in every CTA:
     // ascending page / clock order): pages that are not resident get a slot whose page this selection
     // does not use (clock order from the hand), and the rows read from host are written through.
+    // The plan is computed by the whole CTA in parallel (r02; the r01 version ran its page and slot
+    // scans on one warp: ~9.5 us per plan): the selection's pages are marked in a page bitmap, their
+    // ascending ranks come from one block scan over the bitmap words (rank(p) = word base + popcount
+    // of the lower bits -- also the O(1) lookup of a row's plan entry), new pages are compacted by a
+    // block scan, and the free slots in clock order from the hand by another.
+    auto page_rank = [&](int p) -> int {
+        return (int)pbase[p >> 5] + __popc(pbits[p >> 5] & ((1u << (p & 31)) - 1u));
+    };
     auto cache_plan = [&]() {
         uint32_t* ownc = hist;  // slot -> page, copied (the histogram is idle now)
         static_assert(kUBins >= kMaxSlots, "slot table fits the histogram");
-        if (warp == 0) {
-            for (int j = lane; j < kNeedCap; j += 32) rowbits[j] = 0u;
-            __syncwarp();
-            int n_need = 0, carry = -1;  // carry: last page of the previous sentence
-            for (int base = 0; base < count; base += 32) {
-                const int i = base + lane;
-                int p0 = 0, p1 = -1, r0 = 0, r1 = -1;
-                if (i < count) {
-                    r0 = sel_src[i];
-                    r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
-                    p0 = r0 / kPage;
-                    p1 = r1 / kPage;
-                }
-                int pp = __shfl_up_sync(0xffffffffu, p1, 1);
-                if (lane == 0) pp = carry;
-                const bool shared = p1 >= 0 && p0 == pp;  // first page already listed by the previous sentence
-                const int first = shared ? p0 + 1 : p0;
-                const int cntp = p1 >= first ? p1 - first + 1 : 0;
-                const int incl = warp_incl_sum<int>(cntp);
-                const int pos0 = n_need + incl - cntp;
-                for (int p = first, pos = pos0; p <= p1 && pos < kNeedCap; ++p, ++pos) need[pos] = p;
-                __syncwarp();
-                for (int p = p0; p <= p1; ++p) {  // this sentence's rows of page p
-                    const int j = (shared && p == p0) ? pos0 - 1 : pos0 + (p - first);
-                    const int lo = max(r0, p * kPage) - p * kPage, hi = min(r1, p * kPage + kPage - 1) - p * kPage;
-                    if (j >= 0 && j < kNeedCap) atomicOr(&rowbits[j], ((2u << hi) - 1u) & ~((1u << lo) - 1u));
-                }
-                n_need = min(kNeedCap, n_need + __shfl_sync(0xffffffffu, incl, 31));
-                const int last = __shfl_sync(0xffffffffu, p1, min(31, count - 1 - base));
-                carry = last >= 0 ? last : carry;
-            }
-            if (lane == 0) n_need_s = n_need;
-        }
+        const int nwords = (hc.pages + 31) >> 5;
+        for (int w = tid; w < nwords; w += kUT) pbits[w] = 0u;
         for (int j = tid; j < kMaxSlots / 32; j += kUT) inuse[j] = 0u;
-        __syncthreads();
-        const int n_need = n_need_s;
-        for (int j = tid; j < n_need; j += kUT) pslot[j] = hc.pt[(size_t)unit * hc.pages + need[j]];
         for (int j = tid; j < hc.slots; j += kUT) ownc[j] = (uint32_t)hc.own[(size_t)unit * hc.slots + j];
-        // slots holding a page of this selection -- ALL its pages, also those past the kNeedCap
-        // pages the plan tracks: such a slot is read by this step and must not be given away
+        __syncthreads();
+        SKV_USTAMP(26);
+        // pages of the selection (bitmap) and the slots this step reads -- ALL pages of the selection,
+        // also those past the kNeedCap pages the plan tracks: such a slot must not be given away
         for (int i = tid; i < count; i += kUT) {
             const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
             for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
+                atomicOr(&pbits[p >> 5], 1u << (p & 31));
                 const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + p];
                 if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
             }
         }
         __syncthreads();
-        if (warp == 0) {
-            // new pages (ascending) -> free slots (clock order from the hand): empty, or holding a page
-            // this selection does not use
-            const unsigned lt = (1u << lane) - 1u;
-            for (int j = lane; j < n_need; j += 32) {
-                const uint32_t e = pslot[j];
-                slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
-                oldof[j] = -1;
+        SKV_USTAMP(27);
+        {   // word bases: exclusive prefix of the popcounts (thread t owns words [4t, 4t + 4))
+            uint32_t c[4], sum = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int w = 4 * tid + k;
+                c[k] = w < nwords ? __popc(pbits[w]) : 0u;
+                sum += c[k];
             }
-            int n_new = 0;
-            for (int j0 = 0; j0 < n_need; j0 += 32) {
-                const int j = j0 + lane;
-                const bool nw = j < n_need && pslot[j] == kEmpty;
-                const unsigned m = __ballot_sync(0xffffffffu, nw);
-                if (nw) newj[n_new + __popc(m & lt)] = j;
-                n_new += __popc(m);
+            uint32_t total;
+            uint32_t base = block_incl_sum<uint32_t>(sum, ws32, &total) - sum;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int w = 4 * tid + k;
+                if (w < nwords) pbase[w] = base;
+                base += c[k];
             }
-            int n_free = 0;
-            const int hand = hc.hand[unit];
-            for (int t0 = 0; t0 < hc.slots && n_free < n_new; t0 += 32) {
-                const int t = t0 + lane;
-                bool fr = false;
-                int sl = 0;
-                if (t < hc.slots) {
-                    sl = (hand + t) % hc.slots;
-                    fr = (int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u);
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, fr);
-                if (fr) {
-                    const int k = n_free + __popc(m & lt);
-                    if (k < n_new) frees[k] = sl;
-                }
-                n_free += __popc(m);
-            }
-            const int n_asg = min(n_new, n_free);
-            __syncwarp();
-            for (int k = lane; k < n_asg; k += 32) {
-                const int j = newj[k], sl = frees[k];
-                slotof[j] = sl;
-                oldof[j] = (int)ownc[sl];
-            }
-            if (lane == 0) last_slot_s = n_asg > 0 ? frees[n_asg - 1] : -1;
+            if (tid == 0) n_need_s = (int)min(total, (uint32_t)kNeedCap);
         }
         __syncthreads();
+        const int n_need = n_need_s;
+        for (int w = tid; w < nwords; w += kUT) {
+            uint32_t m = pbits[w];
+            int j = (int)pbase[w];
+            while (m && j < kNeedCap) {
+                const int bit = __ffs(m) - 1;
+                need[j] = (w << 5) + bit;
+                rowbits[j] = 0u;
+                ++j;
+                m &= m - 1u;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < count; i += kUT) {  // the selected rows of every page
+            const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
+            for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
+                const int j = page_rank(p);
+                const int lo = max(r0, p * kPage) - p * kPage, hi = min(r1, p * kPage + kPage - 1) - p * kPage;
+                if (j < kNeedCap) atomicOr(&rowbits[j], ((2u << hi) - 1u) & ~((1u << lo) - 1u));
+            }
+        }
+        for (int j = tid; j < n_need; j += kUT) {
+            const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + need[j]];
+            pslot[j] = e;
+            slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
+            oldof[j] = -1;
+        }
+        __syncthreads();
+        SKV_USTAMP(28);
+        // new pages (ascending) and free slots (clock order from the hand: empty, or holding a page
+        // this selection does not use), both compacted by block scans (thread t owns 2 entries each)
+        const int hand = hc.hand[unit];
+        uint32_t nn = 0, nf = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int j = 2 * tid + k;
+            nn += (j < n_need && pslot[j] == kEmpty) ? 1u : 0u;
+            int sl = hand + 2 * tid + k;
+            sl = sl >= hc.slots ? sl - hc.slots : sl;
+            nf += (2 * tid + k < hc.slots && ((int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u))) ? 1u : 0u;
+        }
+        static_assert(2 * kUT >= kNeedCap && 2 * kUT >= kMaxSlots / 2, "two entries per thread cover the plan");
+        uint32_t tot_new, tot_free;
+        const uint32_t bn = block_incl_sum<uint32_t>(nn, ws32, &tot_new) - nn;
+        const uint32_t bf = block_incl_sum<uint32_t>(nf, ws32, &tot_free) - nf;
+        {
+            uint32_t pn = bn, pf = bf;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int j = 2 * tid + k;
+                if (j < n_need && pslot[j] == kEmpty) newj[pn++] = j;
+                int sl = hand + 2 * tid + k;
+                sl = sl >= hc.slots ? sl - hc.slots : sl;
+                if (2 * tid + k < hc.slots && ((int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u))) {
+                    if (pf < (uint32_t)kNeedCap) frees[pf] = sl;
+                    ++pf;
+                }
+            }
+        }
+        __syncthreads();
+        const int n_asg = (int)min(min(tot_new, tot_free), (uint32_t)kNeedCap);
+        for (int k = tid; k < n_asg; k += kUT) {
+            const int j = newj[k], sl = frees[k];
+            slotof[j] = sl;
+            oldof[j] = (int)ownc[sl];
+        }
+        if (tid == 0) last_slot_s = n_asg > 0 ? frees[n_asg - 1] : -1;
+        __syncthreads();
+        SKV_USTAMP(29);
     };
     int my_miss = 0;
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
@@ -1007,16 +1032,13 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             int2 r = rowtab[t - T0];
             if (r.x >= 0) continue;
             const int row = -(r.x + 1), p = row / kPage;
-            int lo = 0, hi = n_need;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (need[mid] < p) lo = mid + 1; else hi = mid;
-            }
-            if (lo < n_need && need[lo] == p && slotof[lo] >= 0) {
-                r.y = slotof[lo] * kPage + row % kPage;
+            const int j = page_rank(p);
+            if (j < n_need && slotof[j] >= 0) {
+                r.y = slotof[j] * kPage + row % kPage;
                 rowtab[t - T0] = r;
             }
         }
+        SKV_USTAMP(30);
         if (tid == 0) atomicOr(cluster.map_shared_rank(&ctl.any_miss, 0), 1);  // rank 0 updates the table
         __syncthreads();
     }
@@ -1174,9 +1196,9 @@ size_t unit_smem_bytes(int d, int tau) {
 
 int unit_page_tokens() { return kPage; }
 
-bool unit_supported(int d, int grp, int Smax, int tau, int slots) {
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages) {
     return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap && unit_smem_bytes(d, tau) <= 200 * 1024 &&
-           slots <= kMaxSlots;
+           slots <= kMaxSlots && pages <= kMaxPageWords * 32;
 }
 
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }

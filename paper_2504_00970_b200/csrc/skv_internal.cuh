@@ -243,7 +243,7 @@ struct UnitArgs {
     int sid_stride;
     int qmode;                     // 0 = Eq. 2 mean query, 1 = current token's query (NEXT-3)
 };
-bool unit_supported(int d, int grp, int Smax, int tau, int slots);
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages);
 int unit_page_tokens();
 size_t unit_smem_bytes(int d, int tau);
 size_t unit_cand_entries(int units);

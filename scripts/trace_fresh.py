@@ -61,9 +61,11 @@ for step in range(STEPS):
                          miss_ctas=int(miss.sum()), gen_ctas=int(gen_path.sum()), host_mb=hb / 1e6,
                          att_miss=np.median(t(7)[miss] - t(6)[miss]) if miss.any() else 0.0,
                          plan_miss=np.median(t(6)[miss] - t(25)[miss]) if miss.any() else 0.0,
-                         att_hit=np.median(t(7)[~miss] - t(6)[~miss]) if (~miss).any() else 0.0))
+                         att_hit=np.median(t(7)[~miss] - t(6)[~miss]) if (~miss).any() else 0.0,
+                         **({f"p{k}": float(np.median(t(k)[miss] - t(k - 1 if k > 26 else 25)[miss])) for k in (26, 27, 28, 29, 30)}
+                            if miss.any() else {f"p{k}": 0.0 for k in (26, 27, 28, 29, 30)})))
 import statistics as st
-keys = ["span", "scored", "selected", "rowtab", "planned", "attended", "csync2", "miss_ctas", "gen_ctas", "host_mb", "plan_miss", "att_miss", "att_hit"]
+keys = ["span", "scored", "selected", "rowtab", "planned", "attended", "csync2", "miss_ctas", "gen_ctas", "host_mb", "plan_miss", "att_miss", "att_hit", "p26", "p27", "p28", "p29", "p30"]
 print(f"residency={'host' if HOST else 'device'}{' +retention' if RET else ''} layers={M} steps={STEPS}: per launch (max over CTAs of phase end, us since first CTA start)")
 print("  all  : " + " ".join(f"{k}={st.median([r[k] for r in rows]):.2f}" for k in keys))
 for sel, name in ((lambda r: r["miss_ctas"] == 0, "nomiss"), (lambda r: 0 < r["miss_ctas"] and r["host_mb"] < 1, "fewmiss"), (lambda r: r["host_mb"] >= 1, "bigmiss")):
