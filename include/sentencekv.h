@@ -110,6 +110,10 @@ typedef struct {
                                 prompt's sentence lengths into pieces of T tokens; 0 = off (SENTENCE buckets only) */
     int32_t query_mode;      /* skv_query_mode (default SKV_QUERY_MEAN; Quest always ranks by the current query) */
     int32_t fill_mode;       /* skv_fill_mode (default SKV_FILL_PREFIX) */
+    int32_t max_generated;   /* NEXT-2 (reading A29): > 0 keeps a local segment and grows the context -- up to
+                                this many generated tokens per (sequence, layer) appended with
+                                sentencekv_decode_append; 0 = off.  Device residency, without retention or
+                                Quest pages (else UNSUPPORTED). */
 } skv_config;
 
 /* Fills cfg with defaults (shard = everything, device residency, r = 2, obs_window = 0). */
@@ -234,6 +238,23 @@ skv_status sentencekv_decode_step(skv_ctx* ctx, int32_t layer, const void* q, co
                                   float* out, int32_t* sel_ids, int32_t* sel_count, int32_t* sel_tokens,
                                   skv_stream_t stream);
 
+/*
+ * NEXT-2 (cfg.max_generated > 0; "After generating the next token, we append its query to Q_s
+ * and repeat"; reading A29), per layer per step, BEFORE that step's decode_select / decode_step:
+ *   - if the sentence being generated ended at the previous step's token (a boundary input, A11, or
+ *     tau tokens long, A5), it becomes a retrievable bucket of the layer: Eq. 1 mean of its keys
+ *     appended to the layer's embeddings, its rows appended to the layer's bucket offsets (rows
+ *     >= L are generated rows; sel_ids >= the prompt's sentence count name generated sentences);
+ *   - this step's k, v are appended to the generated store; the tokens of the sentence being
+ *     generated (this one included) form the local segment, which decode_attend / decode_step attend
+ *     in addition to the selection, not charged to tau.
+ * k, v         device bf16 [batch_count][kv_head_count][d], 16-byte aligned: this token's key / value
+ * input_token  device int32 [batch_count]: as in decode_select (the same array may be passed)
+ * More than max_generated appends: the token is dropped and sentencekv_sync returns STATE.
+ */
+skv_status sentencekv_decode_append(skv_ctx* ctx, int32_t layer, const void* k, const void* v,
+                                    const int32_t* input_token, skv_stream_t stream);
+
 /* ---- introspection (tests, bench; not on the per-token path) ---- */
 
 /* Sentence counts of the current prompt: S_out host int32 [batch_count]. */
@@ -284,7 +305,8 @@ typedef enum {
     SKV_K_RETAIN = 5,  /* NEXT-1 retention: window importance (2 tcgen05 passes), top-k, pool gather */
     SKV_K_STEP = 6,    /* D1 + D2 + D3 + D4 in one launch (decode_step, default) */
     SKV_K_OFFLOAD = 7, /* P3: the D2H copies of a layer's K and V on the ctx's copy stream (host residency) */
-    SKV_K_COUNT = 8
+    SKV_K_APPEND = 8,  /* NEXT-2 decode_append: close a generated sentence into a bucket, store k / v */
+    SKV_K_COUNT = 9
 } skv_kernel_kind;
 
 skv_status sentencekv_set_profiling(skv_ctx* ctx, int32_t on);

@@ -293,7 +293,7 @@ class Oracle:
 
     def __init__(self, tokens, boundary_ids, tau: int, layers: int, q_heads: int, kv_heads: int, d: int,
                  obs_window: int = 0, semantic_factor: float = 2.0, bucket_mode: int = 0, chunk_size: int = 0,
-                 outlier_n: float = 0.0, query_mode: int = 0, fill_mode: int = 0):
+                 outlier_n: float = 0.0, query_mode: int = 0, fill_mode: int = 0, max_generated: int = 0):
         self.tokens = np.asarray(tokens, dtype=np.int32)
         self.B = self.tokens.shape[0]
         self.bset = np.asarray(boundary_ids, dtype=np.int32)
@@ -323,12 +323,49 @@ class Oracle:
         # NEXT-1 retention (obs_window > 0): per layer, per b: alpha, retained token ids, bucket
         # offsets over the pool and the sentence id of each bucket; K/V above are then the pools
         self.alpha, self.keep, self.loff, self.sid = {}, {}, {}, {}
+        # NEXT-2 local segment and growth (max_generated > 0; reading A29): per layer, per b: the
+        # generated tokens' K/V, the start of the current (unfinished) generated sentence, whether the
+        # sentence ended at the last appended token, and the bucket offsets extended by the completed
+        # generated sentences (rows >= L are generated rows)
+        self.max_gen = int(max_generated)
+        self.gK, self.gV, self.ghot, self.gpend, self.goff = {}, {}, {}, {}, {}
         self.Sq = np.zeros((layers, self.B, q_heads, d), dtype=np.float32)
         self.cnt = np.zeros((layers, self.B), dtype=np.int32)
 
     def offsets(self, layer: int, b: int) -> np.ndarray:
-        """Sentence offsets the decode of (layer, b) ranks: the prompt's, or the retained buckets'."""
+        """Bucket offsets the decode of (layer, b) ranks: the prompt's sentences, the retained buckets,
+        or (NEXT-2) the prompt's sentences followed by the completed generated sentences."""
+        if layer in self.goff:
+            return self.goff[layer][b]
         return self.loff[layer][b] if layer in self.loff else self.off[b]
+
+    def decode_append(self, layer: int, k_bits, v_bits, input_token):
+        """NEXT-2 (P:456 'append ... and repeat'; reading A29), before the step's ranking: a sentence of
+        generated text that ended at the previous step becomes a retrievable bucket (Eq. 1 mean of its
+        keys appended to the layer's embeddings); then this step's token K/V (k_bits, v_bits bf16 bits
+        [B][G][d]) joins the local segment, and if the token is a boundary its sentence ends here."""
+        L = self.tokens.shape[1]
+        if layer not in self.gK:
+            self.gK[layer] = [np.zeros((self.G, 0, self.d), np.uint16) for _ in range(self.B)]
+            self.gV[layer] = [np.zeros((self.G, 0, self.d), np.uint16) for _ in range(self.B)]
+            self.ghot[layer] = [0] * self.B
+            self.gpend[layer] = [False] * self.B
+            self.goff[layer] = [self.off[b].copy() for b in range(self.B)]
+        for b in range(self.B):
+            n = self.gK[layer][b].shape[1]
+            if self.gpend[layer][b]:
+                h = self.ghot[layer][b]
+                for g in range(self.G):
+                    e = embed(self.gK[layer][b][g, h:n], np.array([0, n - h], np.int32))
+                    self.E[layer][b][g] = np.concatenate([self.E[layer][b][g], e])
+                self.goff[layer][b] = np.append(self.goff[layer][b], np.int32(L + n))
+                self.ghot[layer][b] = n
+                self.gpend[layer][b] = False
+            self.gK[layer][b] = np.concatenate([self.gK[layer][b], k_bits[b][:, None, :]], axis=1)
+            self.gV[layer][b] = np.concatenate([self.gV[layer][b], v_bits[b][:, None, :]], axis=1)
+            # the sentence ends at a boundary token (A11) or when it reaches tau tokens (the A5 cap)
+            if int(input_token[b]) in set(self.bset.tolist()) or n + 1 - self.ghot[layer][b] >= self.tau:
+                self.gpend[layer][b] = True
 
     def prefill_layer(self, layer: int, K_bits, V_bits, q_window=None):
         """Alg. 1 lines 3-8 for one layer: Eq. 1 mean keys.  Without a window (reading A6) every
@@ -391,12 +428,21 @@ class Oracle:
         return scores, ids, ntok
 
     def decode_attend(self, layer: int, q_bits, ids):
-        """Alg. 1 line 19 / Eq. 3 over the selection of this layer: O fp64 [B][Hq][d]."""
+        """Alg. 1 line 19 / Eq. 3 over the selection of this layer: O fp64 [B][Hq][d].  NEXT-2: the
+        selected buckets (prompt rows, then generated rows) plus the local segment -- the tokens of the
+        unfinished generated sentence, attended uncharged (reading A29)."""
         O = np.zeros((self.B, self.Hq, self.d), dtype=np.float64)
         for b in range(self.B):
             for g in range(self.G):
                 h0 = g * self.grp
+                K, V, off, sel = self.K[layer][b][g], self.V[layer][b][g], self.offsets(layer, b), list(ids[b][g])
+                if layer in self.gK:
+                    n = self.gK[layer][b].shape[1]
+                    K = np.concatenate([K, self.gK[layer][b][g]])
+                    V = np.concatenate([V, self.gV[layer][b][g]])
+                    if n > self.ghot[layer][b]:  # the local segment as one extra, always-attended range
+                        off = np.append(off, np.int32(K.shape[0]))
+                        sel = sel + [len(off) - 2]
                 O[b, h0 : h0 + self.grp] = attend(
-                    q_bits[b, h0 : h0 + self.grp], self.K[layer][b][g], self.V[layer][b][g], self.offsets(layer, b),
-                    ids[b][g])
+                    q_bits[b, h0 : h0 + self.grp], K, V, off, np.asarray(sel, np.int32))
         return O

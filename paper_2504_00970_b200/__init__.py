@@ -44,7 +44,7 @@ class SkvConfig(ctypes.Structure):
         ("residency", ctypes.c_int32), ("device", ctypes.c_int32), ("kv_head_begin", ctypes.c_int32),
         ("kv_head_count", ctypes.c_int32), ("batch_begin", ctypes.c_int32), ("batch_count", ctypes.c_int32),
         ("bucket_mode", ctypes.c_int32), ("chunk_size", ctypes.c_int32), ("outlier_n", ctypes.c_float),
-        ("query_mode", ctypes.c_int32), ("fill_mode", ctypes.c_int32),
+        ("query_mode", ctypes.c_int32), ("fill_mode", ctypes.c_int32), ("max_generated", ctypes.c_int32),
     ]
 
 
@@ -71,6 +71,7 @@ def _load():
         "sentencekv_decode_select": (i32, [P, i32, P, P, P, P, P, P]),
         "sentencekv_decode_attend": (i32, [P, i32, P, P, P]),
         "sentencekv_decode_step": (i32, [P, i32, P, P, P, P, P, P, P]),
+        "sentencekv_decode_append": (i32, [P, i32, P, P, P, P]),
         "sentencekv_sentence_counts": (i32, [P, P]),
         "sentencekv_sentence_capacity": (i32, [P]),
         "sentencekv_copy_offsets": (i32, [P, P, P]),
@@ -167,6 +168,11 @@ def sentencekv_decode_attend(ctx, layer, q, out, stream=None) -> None:
     _check(ctx, lib.sentencekv_decode_attend(ctx, int(layer), _ptr(q), _ptr(out), _stream(stream)))
 
 
+def sentencekv_decode_append(ctx, layer, k, v, input_token, stream=None) -> None:
+    """NEXT-2: close the generated sentence that ended at the last token, append this token's k / v."""
+    _check(ctx, lib.sentencekv_decode_append(ctx, int(layer), _ptr(k), _ptr(v), _ptr(input_token), _stream(stream)))
+
+
 def sentencekv_decode_step(ctx, layer, q, input_token, out, sel_ids=None, sel_count=None, sel_tokens=None,
                            stream=None) -> None:
     """D1 + D2 + D3 + D4 in one call (fused select + attend; same results as select then attend)."""
@@ -183,13 +189,14 @@ class SentenceKV:
     def __init__(self, batch, layers, q_heads, kv_heads, head_dim, max_context, token_budget,
                  semantic_factor=2.0, residency=SKV_KV_DEVICE, device=0, kv_head_begin=0, kv_head_count=0,
                  batch_begin=0, batch_count=0, obs_window=0, bucket_mode=0, chunk_size=0, outlier_n=0.0,
-                 query_mode=0, fill_mode=0):
+                 query_mode=0, fill_mode=0, max_generated=0):
         self.cfg = sentencekv_config_default(
             batch=batch, layers=layers, q_heads=q_heads, kv_heads=kv_heads, head_dim=head_dim,
             max_context=max_context, token_budget=token_budget, semantic_factor=semantic_factor,
             residency=residency, device=device, kv_head_begin=kv_head_begin, kv_head_count=kv_head_count,
             batch_begin=batch_begin, batch_count=batch_count, obs_window=obs_window, bucket_mode=bucket_mode,
-            chunk_size=chunk_size, outlier_n=outlier_n, query_mode=query_mode, fill_mode=fill_mode)
+            chunk_size=chunk_size, outlier_n=outlier_n, query_mode=query_mode, fill_mode=fill_mode,
+            max_generated=max_generated)
         self.quest = bucket_mode == SKV_BUCKETS_QUEST
         self.N = obs_window
         self.ctx = sentencekv_create(self.cfg)
@@ -223,6 +230,10 @@ class SentenceKV:
 
     def decode_attend(self, layer, q, out, stream=None):
         sentencekv_decode_attend(self.ctx, layer, q, out, stream)
+
+    def decode_append(self, layer, k, v, input_token, stream=None):
+        """NEXT-2: this step's key / value [B][G][d] into the local segment (before the step's decode)."""
+        sentencekv_decode_append(self.ctx, layer, k, v, input_token, stream)
 
     def decode_step(self, layer, q, input_token, out, sel_ids=None, sel_count=None, sel_tokens=None, stream=None):
         sentencekv_decode_step(self.ctx, layer, q, input_token, out, sel_ids, sel_count, sel_tokens, stream)
@@ -289,7 +300,7 @@ class SentenceKV:
                                                       _stream(stream)))
         return keep, off, sid, S
 
-    KERNELS = ("segment", "compress", "score", "select", "attend", "retain", "step", "offload")
+    KERNELS = ("segment", "compress", "score", "select", "attend", "retain", "step", "offload", "append")
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))

@@ -15,7 +15,7 @@ VARIANT = os.environ.get("SKV_VARIANT", "trace" if TRACE else "")
 DEFS = os.environ.get("SKV_DEFS", "").split()
 BUILD = os.path.join(HERE, f"build_{VARIANT}" if VARIANT else "build")
 LIB = os.path.join(HERE, f"libsentencekv_{VARIANT}.so" if VARIANT else "libsentencekv.so")
-SOURCES = ["prefill.cu", "retain.cu", "variants.cu", "decode_select.cu", "decode_attend_mma.cu", "decode_unit.cu", "abi.cu"]
+SOURCES = ["prefill.cu", "retain.cu", "variants.cu", "local.cu", "decode_select.cu", "decode_attend_mma.cu", "decode_unit.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v"] + (

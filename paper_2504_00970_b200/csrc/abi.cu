@@ -80,6 +80,14 @@ void free_sel(skv::SelBufs& s) {
     dfree(s.parity);
 }
 
+void free_local(skv::LayerState& ls) {
+    dfree(ls.genK);
+    dfree(ls.genV);
+    dfree(ls.gstat);
+    dfree(ls.goff);
+    dfree(ls.gS);
+}
+
 void free_layer_prompt(skv::LayerState& ls) {
     dfree(ls.E);
     dfree(ls.scores);
@@ -90,6 +98,7 @@ void free_layer_prompt(skv::LayerState& ls) {
     dfree(ls.pc_pt);
     dfree(ls.pc_own);
     dfree(ls.pc_hand);
+    free_local(ls);
 }
 
 void free_retention(skv::LayerState& ls) {
@@ -202,6 +211,11 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         (cfg.fill_mode != SKV_FILL_PREFIX && cfg.fill_mode != SKV_FILL_SKIP))
         return SKV_ERR_INVALID_ARGUMENT;
     if (cfg.obs_window > 0 && cfg.bucket_mode == SKV_BUCKETS_QUEST) return SKV_ERR_UNSUPPORTED;
+    if (cfg.max_generated < 0) return SKV_ERR_INVALID_ARGUMENT;
+    // NEXT-2 local segment: device residency, sentence / equal buckets, no retention (this build)
+    if (cfg.max_generated > 0 && (cfg.residency != SKV_KV_DEVICE || cfg.obs_window > 0 ||
+                                  cfg.bucket_mode == SKV_BUCKETS_QUEST))
+        return SKV_ERR_UNSUPPORTED;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
         (cfg.obs_window > 0 && !skv::retain_supported(cfg.head_dim, cfg.obs_window, grp)))
         return SKV_ERR_UNSUPPORTED;
@@ -285,6 +299,17 @@ SKV_API skv_status sentencekv_sync(skv_ctx* c) {
     if (e != cudaSuccess) return cuda_fail(c, e, "sentencekv_sync");
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "sentencekv_sync");
+    if (c->sticky == SKV_OK && c->cfg.max_generated > 0) {  // NEXT-2: a full generated store is a state error
+        std::vector<int32_t> st(4 * c->B);
+        for (size_t l = 0; l < c->layer.size(); ++l) {
+            if (!c->layer[l].gstat || !c->layer[l].prefilled) continue;
+            if (cudaMemcpy(st.data(), c->layer[l].gstat, sizeof(int32_t) * 4 * c->B, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return cuda_fail(c, cudaGetLastError(), "sentencekv_sync");
+            for (int b = 0; b < c->B; ++b)
+                if (st[4 * b + 3]) return fail(c, SKV_ERR_STATE, "layer %zu: more than max_generated = %d tokens appended",
+                                               l, c->cfg.max_generated);
+        }
+    }
     return c->sticky;
 }
 
@@ -306,10 +331,15 @@ struct LayerView {
     const int32_t* sid;    // bucket -> sentence id (retention), else nullptr
     int sid_stride;
     bool host;             // rows come from the host store through the HBM working set
+    skv::GenSrc gen;       // NEXT-2 generated rows + local segment (gen.Kg == nullptr: off)
 };
 static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
-    if (ls.retained) return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false};
-    return {c->off, c->off_stride, c->S_dev, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST};
+    const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0};
+    if (ls.retained) return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false, none};
+    if (ls.genK)
+        return {ls.goff, c->Smax + 1, ls.gS, ls.K, ls.V, c->L, nullptr, 0, false,
+                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated, c->L}};
+    return {c->off, c->off_stride, c->S_dev, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST, none};
 }
 
 // Empties the page cache of a layer (every page -> host).
@@ -368,6 +398,14 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
             SKV_CUDA(c, dalloc(&ls.pc_hand, U));
         }
         SKV_CUDA(c, dalloc(&ls.unit_hint, U));
+        if (c->cfg.max_generated > 0) {
+            const size_t mg = (size_t)c->cfg.max_generated;
+            SKV_CUDA(c, dalloc(&ls.genK, U * mg * d));
+            SKV_CUDA(c, dalloc(&ls.genV, U * mg * d));
+            SKV_CUDA(c, dalloc(&ls.gstat, B * 4));
+            SKV_CUDA(c, dalloc(&ls.goff, B * (size_t)(Smax + 1)));
+            SKV_CUDA(c, dalloc(&ls.gS, B));
+        }
     }
     dfree(c->unit_cand);
     SKV_CUDA(c, dalloc(&c->unit_cand, skv::unit_cand_entries((int)U)));
@@ -443,6 +481,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         SKV_CUDA(c, cudaStreamSynchronize(st));
         int Smax = 1;
         for (int b = 0; b < c->B; ++b) Smax = c->S_host[b] > Smax ? c->S_host[b] : Smax;
+        Smax += c->cfg.max_generated;  // NEXT-2: room for every sentence the decode may add
         if (Smax > c->Smax || !c->layer[0].E) {
             for (auto& ls : c->layer) free_layer_prompt(ls);
             skv_status s = alloc_prompt_buffers(c, Smax);
@@ -561,6 +600,14 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
         ls.V = Vb;
     }
+    if (c->cfg.max_generated > 0) {
+        // NEXT-2: the layer's buckets start as the prompt's sentences; no generated token yet
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.goff, sizeof(int32_t) * (c->Smax + 1), c->off, sizeof(int32_t) * c->off_stride,
+                                      sizeof(int32_t) * (std::min(c->off_stride, c->Smax + 1)), c->B,
+                                      cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.gS, c->S_dev, sizeof(int32_t) * c->B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemsetAsync(ls.gstat, 0, sizeof(int32_t) * 4 * c->B, st));
+    }
     ls.prefilled = true;
     ls.selected = false;
     c->after_prefill = true;
@@ -621,7 +668,8 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     const LayerView v = layer_view(c, ls);
     const bool host = v.host;
     const bool unit_path = c->cfg.bucket_mode != SKV_BUCKETS_QUEST && c->cfg.fill_mode == SKV_FILL_PREFIX;
-    if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0, host ? ls.pc_pages : 0)) {
+    if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0,
+                                         host ? ls.pc_pages : 0, v.gen.Kg != nullptr)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
         if (host) {
@@ -647,6 +695,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.sid = v.sid;
         a.sid_stride = v.sid_stride;
         a.qmode = c->cfg.query_mode;
+        a.gen = v.gen;
         a.B = c->B;
         a.G = c->G;
         a.Smax = c->Smax;
@@ -678,6 +727,28 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     return sentencekv_decode_attend(c, layer, q, out, stream_);
 }
 
+SKV_API skv_status sentencekv_decode_append(skv_ctx* c, int32_t layer, const void* k, const void* v,
+                                            const int32_t* input_token, skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    if (c->cfg.max_generated < 1) return fail(c, SKV_ERR_STATE, "decode_append needs cfg.max_generated > 0");
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (!ls.prefilled || !ls.genK) return fail(c, SKV_ERR_STATE, "decode_append before prefill of layer %d", layer);
+    if (!k || !v || !input_token || !aligned16(k) || !aligned16(v))
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "k / v (16-byte aligned) / input_token is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
+    DeviceGuard dg(c->cfg.device);
+    cudaEvent_t pa = prof_begin(c, st);
+    SKV_CUDA(c, skv::launch_gen_append(static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v),
+                                       ls.genK, ls.genV, c->cfg.max_generated, ls.gstat, ls.goff, c->Smax + 1, ls.gS,
+                                       c->Smax, ls.E, input_token, c->bset, c->n_bset, c->B, c->G, c->L, c->d, c->tau,
+                                       st));
+    prof_end(c, SKV_K_APPEND, pa, st);
+    c->launches += 2;
+    return SKV_OK;
+}
+
 SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const void* q, float* out,
                                             skv_stream_t stream_) {
     if (!c) return SKV_ERR_INVALID_ARGUMENT;
@@ -700,12 +771,12 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
         }
         pa = prof_begin(c, st);
         SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
-                                           true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, st));
+                                           true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, v.gen, st));
     } else {
         pa = prof_begin(c, st);
         const skv::KvSrc kv{v.K, v.V, v.stride, 0};
         SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, (int)v.stride, nullptr, nullptr, false, c->B, c->G,
-                                           c->grp, c->d, ls.sel, nullptr, qs, out, st));
+                                           c->grp, c->d, ls.sel, nullptr, qs, out, v.gen, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;

@@ -36,7 +36,8 @@ template <int D, int GRP, bool HOST>
 __global__ void __cluster_dims__(kMCL, 1, 1) __launch_bounds__(kMT, 2)
 attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bfloat16* Khost,
                   const __nv_bfloat16* Vhost, int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, int G, SelBufs sel,
-                  unsigned long long* __restrict__ ledger, QsState qs, float* __restrict__ out, float scale_log2) {
+                  unsigned long long* __restrict__ ledger, QsState qs, float* __restrict__ out, GenSrc gen,
+                  float scale_log2) {
     static_assert(GRP <= 8, "heads fill the N = 8 side");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MmaSmem<D>& sm = *reinterpret_cast<MmaSmem<D>*>(smem_raw);
@@ -92,14 +93,23 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     __syncthreads();
     SKV_TRACE_POINT(2);
     const int ntok = tok[count];
-    const int ntiles = (ntok + kTile - 1) / kTile;
+    // NEXT-2 local segment (device residency): the generated sentence's tokens follow the selection
+    int hot0 = 0, nhot = 0;
+    if (gen.Kg) {
+        hot0 = gen.gstat[b * 4 + 1];
+        nhot = gen.gstat[b * 4 + 0] - hot0;
+    }
+    const int natt = ntok + nhot;
+    const int ntiles = (natt + kTile - 1) / kTile;
     const int per = (ntiles + kMCL - 1) / kMCL;
     const int tb = min(ntiles, rank * per), te = min(ntiles, tb + per);
-    const int T0 = tb * kTile, T1 = min(ntok, te * kTile);
+    const int T0 = tb * kTile, T1 = min(natt, te * kTile);
     // row of every gathered token of this CTA (HOST: encoded as above)
     for (int t = T0 + tid; t < te * kTile; t += kMT) {
         int r = kInvalid;
-        if (t < T1) {
+        if (t < T1 && t >= ntok) {
+            r = gen.L + hot0 + (t - ntok);
+        } else if (t < T1) {
             int lo = 0, hi = count - 1;  // largest i with tok[i] <= t
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
@@ -122,12 +132,14 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     const __nv_bfloat16* Vp = HOST ? wsV + ((size_t)unit * 2 + prev) * tau * D : nullptr;
     __nv_bfloat16* Kc = HOST ? wsK + ((size_t)unit * 2 + cur) * tau * D : nullptr;
     __nv_bfloat16* Vc = HOST ? wsV + ((size_t)unit * 2 + cur) * tau * D : nullptr;
+    const __nv_bfloat16* Kgu = gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr;
+    const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
     auto rowK = [&](int r) -> const __nv_bfloat16* {
-        if (!HOST) return Kd + (size_t)r * D;
+        if (!HOST) return r >= gen.L ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
         return r >= 0 ? Kh + (size_t)r * D : Kp + (size_t)(-(r + 1)) * D;
     };
     auto rowV = [&](int r) -> const __nv_bfloat16* {
-        if (!HOST) return Vd + (size_t)r * D;
+        if (!HOST) return r >= gen.L ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
         return r >= 0 ? Vh + (size_t)r * D : Vp + (size_t)(-(r + 1)) * D;
     };
 
@@ -201,26 +213,28 @@ template <int D, int GRP, bool HOST>
 static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, KvSrc kv,
                                 const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L, __nv_bfloat16* wsK,
                                 __nv_bfloat16* wsV, int G, SelBufs sel, unsigned long long* ledger, QsState qs,
-                                float* out, float scale_log2) {
-    // metadata: tok[tau+1] + srcs[tau] (+ pids[tau] + ptok[tau+1]) + rowtab[per-CTA tokens]
-    const size_t tiles = ((size_t)sel.tau + kTile - 1) / kTile;
+                                float* out, GenSrc gen, float scale_log2) {
+    // metadata: tok[tau+1] + srcs[tau] (+ pids[tau] + ptok[tau+1]) + rowtab[per-CTA tokens]; the
+    // NEXT-2 local segment adds up to tau attended tokens
+    const size_t tiles = ((size_t)sel.tau * (gen.Kg ? 2 : 1) + kTile - 1) / kTile;
     const size_t rows = ((tiles + kMCL - 1) / kMCL) * kTile;
     const size_t meta = (size_t)(2 * sel.tau + 1) + (HOST ? (size_t)(2 * sel.tau + 1) : 0) + rows;
     const size_t smem = sizeof(MmaSmem<D>) + sizeof(int32_t) * meta;
     cudaError_t e = ensure_smem((const void*)attend_mma_kernel<D, GRP, HOST>, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(false, attend_mma_kernel<D, GRP, HOST>, grid, dim3(kMT), smem, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel,
-                      ledger, qs, out, scale_log2);
+                      ledger, qs, out, gen, scale_log2);
 }
 
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
-                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, cudaStream_t st) {
+                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, GenSrc gen,
+                              cudaStream_t st) {
     dim3 grid(kMCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
 #define SKV_MM(DV, GV)                                                                                          \
-    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, scale_log2) \
-                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, scale_log2)
+    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, scale_log2) \
+                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_MM(128, 1);

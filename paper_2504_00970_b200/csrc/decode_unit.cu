@@ -224,7 +224,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, float* __restrict__ out,
                  int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, const int32_t* __restrict__ sid, int sid_stride, int qmode,
-                 float scale_log2, int trace_idx) {
+                 GenSrc gen, float scale_log2, int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
     constexpr int GPW = 32 / TPS;               // sentences per warp step
@@ -867,10 +867,18 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
 
     // ---------------------------------------------------------------- 3. gather + attend (D3 + D4)
     const int count = ctl.count, ntok = ctl.ntok;
-    const int ntl = (ntok + kTile - 1) / kTile;
+    // NEXT-2 local segment: the tokens of the sentence being generated follow the selection in the
+    // attended range (always attended, not charged to tau; generated rows are L + position)
+    int hot0 = 0, nhot = 0;
+    if (gen.Kg) {
+        hot0 = gen.gstat[b * 4 + 1];
+        nhot = gen.gstat[b * 4 + 0] - hot0;
+    }
+    const int natt = ntok + nhot;
+    const int ntl = (natt + kTile - 1) / kTile;
     const int per = (ntl + kUC - 1) / kUC;
     const int tb = min(ntl, rank * per), te = min(ntl, tb + per);
-    const int T0 = tb * kTile, T1 = min(ntok, te * kTile);
+    const int T0 = tb * kTile, T1 = min(natt, te * kTile);
     // Host residency (D3 host): the HBM working set is a page cache (pages of kPage context
     // rows); a page-table entry holds the page's slot and the mask of its rows already in HBM.  A
     // selected row is read from its slot if the row is there, else from the mapped host store.  When
@@ -888,37 +896,42 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     auto cache_plan = [&]() {
         uint32_t* ownc = hist;  // slot -> page, copied (the histogram is idle now)
         static_assert(kUBins >= kMaxSlots, "slot table fits the histogram");
+        // the slot owners and the clock hand are loaded first and consumed late (their latency hides
+        // under the bitmap and the scan); the page-table entries of the selection are read in ONE
+        // round, once the pages are ranked
+        constexpr int kOwnPer = kMaxSlots / kUT;
+        int32_t own_r[kOwnPer];
+#pragma unroll
+        for (int k = 0; k < kOwnPer; ++k) {
+            const int j = tid + k * kUT;
+            own_r[k] = j < hc.slots ? hc.own[(size_t)unit * hc.slots + j] : -1;
+        }
+        const int hand = hc.hand[unit];
         const int nwords = (hc.pages + 31) >> 5;
         for (int w = tid; w < nwords; w += kUT) pbits[w] = 0u;
         for (int j = tid; j < kMaxSlots / 32; j += kUT) inuse[j] = 0u;
-        for (int j = tid; j < hc.slots; j += kUT) ownc[j] = (uint32_t)hc.own[(size_t)unit * hc.slots + j];
         __syncthreads();
         SKV_USTAMP(26);
-        // pages of the selection (bitmap) and the slots this step reads -- ALL pages of the selection,
-        // also those past the kNeedCap pages the plan tracks: such a slot must not be given away
-        for (int i = tid; i < count; i += kUT) {
+        for (int i = tid; i < count; i += kUT) {  // pages of the selection
             const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
-            for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
-                atomicOr(&pbits[p >> 5], 1u << (p & 31));
-                const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + p];
-                if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
-            }
+            for (int p = r0 / kPage; p <= r1 / kPage; ++p) atomicOr(&pbits[p >> 5], 1u << (p & 31));
         }
         __syncthreads();
         SKV_USTAMP(27);
-        {   // word bases: exclusive prefix of the popcounts (thread t owns words [4t, 4t + 4))
-            uint32_t c[4], sum = 0;
+        uint32_t total;
+        {   // word bases: exclusive prefix of the popcounts (thread t owns words [2t, 2t + 2))
+            static_assert(2 * kUT >= kMaxPageWords, "two bitmap words per thread");
+            uint32_t c[2], sum = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int w = 4 * tid + k;
+            for (int k = 0; k < 2; ++k) {
+                const int w = 2 * tid + k;
                 c[k] = w < nwords ? __popc(pbits[w]) : 0u;
                 sum += c[k];
             }
-            uint32_t total;
             uint32_t base = block_incl_sum<uint32_t>(sum, ws32, &total) - sum;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int w = 4 * tid + k;
+            for (int k = 0; k < 2; ++k) {
+                const int w = 2 * tid + k;
                 if (w < nwords) pbase[w] = base;
                 base += c[k];
             }
@@ -929,15 +942,33 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         for (int w = tid; w < nwords; w += kUT) {
             uint32_t m = pbits[w];
             int j = (int)pbase[w];
-            while (m && j < kNeedCap) {
+            while (m) {
                 const int bit = __ffs(m) - 1;
-                need[j] = (w << 5) + bit;
-                rowbits[j] = 0u;
+                const int p = (w << 5) + bit;
+                if (j < kNeedCap) {
+                    need[j] = p;
+                    rowbits[j] = 0u;
+                } else {  // past the tracked pages (rare): still mark its slot as read by this step
+                    const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + p];
+                    if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
+                }
                 ++j;
                 m &= m - 1u;
             }
         }
+#pragma unroll
+        for (int k = 0; k < kOwnPer; ++k) {
+            const int j = tid + k * kUT;
+            if (j < hc.slots) ownc[j] = (uint32_t)own_r[k];
+        }
         __syncthreads();
+        for (int j = tid; j < n_need; j += kUT) {
+            const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + need[j]];
+            pslot[j] = e;
+            slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
+            oldof[j] = -1;
+            if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
+        }
         for (int i = tid; i < count; i += kUT) {  // the selected rows of every page
             const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
             for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
@@ -946,17 +977,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 if (j < kNeedCap) atomicOr(&rowbits[j], ((2u << hi) - 1u) & ~((1u << lo) - 1u));
             }
         }
-        for (int j = tid; j < n_need; j += kUT) {
-            const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + need[j]];
-            pslot[j] = e;
-            slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
-            oldof[j] = -1;
-        }
         __syncthreads();
         SKV_USTAMP(28);
         // new pages (ascending) and free slots (clock order from the hand: empty, or holding a page
         // this selection does not use), both compacted by block scans (thread t owns 2 entries each)
-        const int hand = hc.hand[unit];
         uint32_t nn = 0, nf = 0;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -966,7 +990,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             sl = sl >= hc.slots ? sl - hc.slots : sl;
             nf += (2 * tid + k < hc.slots && ((int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u))) ? 1u : 0u;
         }
-        static_assert(2 * kUT >= kNeedCap && 2 * kUT >= kMaxSlots / 2, "two entries per thread cover the plan");
+        // (the clock scan looks at the first 2 * kUT = 512 slots from the hand; the new pages are at most kNeedCap)
+        static_assert(2 * kUT >= kNeedCap, "two entries per thread cover the new pages");
         uint32_t tot_new, tot_free;
         const uint32_t bn = block_incl_sum<uint32_t>(nn, ws32, &tot_new) - nn;
         const uint32_t bf = block_incl_sum<uint32_t>(nf, ws32, &tot_free) - nf;
@@ -998,7 +1023,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int my_miss = 0;
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
-        if (t < T1) {
+        if (t < T1 && t >= ntok) {
+            r.x = gen.L + hot0 + (t - ntok);  // local segment (device residency only)
+        } else if (t < T1) {
             int lo2 = 0, hi2 = count - 1;  // largest i with sel_tok[i] <= t
             while (lo2 < hi2) {
                 const int mid = (lo2 + hi2 + 1) >> 1;
@@ -1057,6 +1084,15 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         auto rowV = [&](int r) -> const __nv_bfloat16* {
             return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : Vd + (size_t)r * D;
         };
+        // device rows: context rows < L, generated rows (NEXT-2) >= L
+        const __nv_bfloat16* Kgu = gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr;
+        const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
+        auto devK = [&](int r) -> const __nv_bfloat16* {
+            return (!HOST && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
+        };
+        auto devV = [&](int r) -> const __nv_bfloat16* {
+            return (!HOST && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
+        };
         unsigned long long host_bytes = 0;
         uint4 qseg[D / 32];
         mma::load_q<D, GRP>(qseg, q + ((size_t)b * Hq + g * GRP) * D, lane);
@@ -1072,15 +1108,15 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
-                    pv[k] = rv[k].x != kInvalid ? (MISS ? rowV(rv[k].x) : Vd + (size_t)rv[k].x * D) : nullptr;
+                    pv[k] = rv[k].x != kInvalid ? (MISS ? rowV(rv[k].x) : devV(rv[k].x)) : nullptr;
                 }
                 mma::TileRegs<D> tr;
                 if constexpr (MISS)
                     mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr,
                                       rk1.x != kInvalid ? rowK(rk1.x) : nullptr, pv, lane);
                 else
-                    mma::load_tile<D>(tr, rk0.x != kInvalid ? Kd + (size_t)rk0.x * D : nullptr,
-                                      rk1.x != kInvalid ? Kd + (size_t)rk1.x * D : nullptr, pv, lane);
+                    mma::load_tile<D>(tr, rk0.x != kInvalid ? devK(rk0.x) : nullptr,
+                                      rk1.x != kInvalid ? devK(rk1.x) : nullptr, pv, lane);
                 mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
                 if constexpr (MISS) {
                     // write-through of the rows read from host into their working-set slot
@@ -1187,17 +1223,18 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     SKV_LSTAMP(2);
 }
 
-size_t unit_smem_bytes(int d, int tau) {
+size_t unit_smem_bytes(int d, int tau, int att) {
     (void)d;
-    const size_t rows = (((size_t)tau + kTile - 1) / kTile + kUC - 1) / kUC * kTile;
+    const size_t rows = (((size_t)att + kTile - 1) / kTile + kUC - 1) / kUC * kTile;  // attended tokens per CTA
     return (size_t)kUStages * kUTileBytes + sizeof(uint32_t) * kULocalCap + sizeof(int32_t) * (kULocalCap + 4) +
            sizeof(int4) * (kUOwnCap + kUBandCap) + sizeof(int32_t) * ((3 * (size_t)tau + 5) / 4 * 4) + sizeof(int2) * rows;
 }
 
 int unit_page_tokens() { return kPage; }
 
-bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages) {
-    return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap && unit_smem_bytes(d, tau) <= 200 * 1024 &&
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, bool local) {
+    return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap &&
+           unit_smem_bytes(d, tau, local ? 2 * tau : tau) <= 200 * 1024 &&
            slots <= kMaxSlots && pages <= kMaxPageWords * 32;
 }
 
@@ -1210,7 +1247,7 @@ static int trace_counter = 0;  // launch index for the trace build's per-launch 
 
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
-    const size_t smem = unit_smem_bytes(D, a.sel.tau);
+    const size_t smem = unit_smem_bytes(D, a.sel.tau, a.gen.Kg ? 2 * a.sel.tau : a.sel.tau);
     cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST>, smem);
     if (e != cudaSuccess) return e;
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
@@ -1218,7 +1255,7 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), a.out, a.out_ids,
-                      a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, scale_log2, trace_counter++);
+                      a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, a.gen, scale_log2, trace_counter++);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {

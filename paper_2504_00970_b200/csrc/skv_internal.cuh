@@ -46,6 +46,15 @@ struct QsState {
 // s * slot_stride + r) * d.  Device residency: the caller's K/V (unit_stride = L, slot_stride = 0,
 // rows = context tokens).  Host residency: the HBM working set (unit_stride = 2*tau,
 // slot_stride = tau, rows = gathered positions).
+// NEXT-2 local segment / generated rows (Kg == nullptr: off).  Rows >= L of a layer's buckets are
+// generated rows (row - L of the store); gstat[b] = {count, start of the current sentence, pending, overflow}.
+struct GenSrc {
+    const __nv_bfloat16* Kg;       // [B][G][stride][d]
+    const __nv_bfloat16* Vg;
+    const int32_t* gstat;          // [B][4]
+    int stride, L;
+};
+
 struct KvSrc {
     const __nv_bfloat16* K;
     const __nv_bfloat16* V;
@@ -92,6 +101,12 @@ struct LayerState {
     int32_t* rsid = nullptr;           // [B][m]   sentence id of each bucket
     int32_t* rS = nullptr;             // [B]      buckets (sentences with a retained token)
     size_t ret_bytes = 0;              // allocation key (B, G, m, L, N)
+    // NEXT-2 local segment and growth (cfg.max_generated > 0)
+    __nv_bfloat16* genK = nullptr;     // [B][G][max_gen][d] generated tokens' K / V
+    __nv_bfloat16* genV = nullptr;
+    int32_t* gstat = nullptr;          // [B][4]
+    int32_t* goff = nullptr;           // [B][Smax+1] the prompt's offsets followed by completed generated sentences
+    int32_t* gS = nullptr;             // [B] buckets
 };
 
 }  // namespace skv
@@ -195,7 +210,15 @@ cudaError_t launch_select(const float* scores, const int32_t* off, int off_strid
 // store (PCIe); every row is written through to the current slot; host bytes are added to *ledger.
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
-                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, cudaStream_t st);
+                              SelBufs sel, unsigned long long* ledger, QsState qs, float* out, GenSrc gen,
+                              cudaStream_t st);
+
+// NEXT-2 (local.cu): close the sentence that ended at the previous token into a bucket, append this
+// token's k, v ([B][G][d]) to the generated store, advance the per-sequence state
+cudaError_t launch_gen_append(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* Kg, __nv_bfloat16* Vg,
+                              int max_gen, int32_t* gstat, int32_t* goff, int off_stride, int32_t* gS, int Smax,
+                              __nv_bfloat16* E, const int32_t* input_token, const int32_t* bset, int nb, int B, int G,
+                              int L, int d, int tau, cudaStream_t st);
 
 // Opt-in dynamic shared memory of `func` on the current device (the attribute is per device
 // context; cached per (device, function), thread-safe).
@@ -242,10 +265,11 @@ struct UnitArgs {
     const int32_t* sid;            // optional [B][sid_stride]: output ids = sid[b][selected bucket] (retention)
     int sid_stride;
     int qmode;                     // 0 = Eq. 2 mean query, 1 = current token's query (NEXT-3)
+    GenSrc gen;                    // NEXT-2 local segment (gen.Kg == nullptr: off)
 };
-bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages);
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, bool local);
 int unit_page_tokens();
-size_t unit_smem_bytes(int d, int tau);
+size_t unit_smem_bytes(int d, int tau, int att);
 size_t unit_cand_entries(int units);
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st);
 

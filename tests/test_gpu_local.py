@@ -1,0 +1,104 @@
+"""GPU parity of SURVEY 8(f) NEXT-2 (local segment + context growth, reading A29) against the oracle,
+through the C ABI: each step appends the token's K/V (sentencekv_decode_append), completed generated
+sentences become buckets (their embeddings bit-exact), scores and selected ids (including generated
+sentences) bit-exact, O over selection + local segment within 2e-3."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.gpu_harness import ATOL, from_bits, to_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(mode, seed=0, B=2, M=1, Hq=8, G=2, d=64, L=3000, tau=128, steps=40, mean_sentence=6.0, max_generated=64,
+         graph=False):
+    import paper_2504_00970_b200 as skvlib
+
+    dev = torch.device("cuda:0")
+    toks, topics = synth.prompts(seed, B, L, median=20.0)
+    Ks, Vs = zip(*(synth.kv_layer(seed, l, topics, G, d) for l in range(M)))
+    skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
+                            max_generated=max_generated)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d, max_generated=max_generated)
+    Kd = [from_bits(K, dev) for K in Ks]
+    Vd = [from_bits(V, dev) for V in Vs]
+    tok_dev = torch.from_numpy(toks).to(dev)
+    for l in range(M):
+        skv.prefill_compress(l, Kd[l], Vd[l], token_ids=tok_dev if l == 0 else None,
+                             boundary_ids=synth.BOUNDARY_IDS if l == 0 else None)
+        orc.prefill_layer(l, Ks[l], Vs[l])
+    S0 = skv.sentence_counts()
+    script, target = synth.decode_script(seed, B, steps, mean_sentence=mean_sentence)
+    rng = np.random.default_rng(seed + 100)
+    ids = torch.empty((B, G, tau), dtype=torch.int32, device=dev)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+    worst, grown = 0.0, 0
+    for s in range(steps):
+        it = torch.from_numpy(script[s]).to(dev)
+        for l in range(M):
+            kg = synth.f32_to_bf16_bits(rng.standard_normal((B, G, d)).astype(np.float32) + 0.5)
+            vg = synth.f32_to_bf16_bits(rng.standard_normal((B, G, d)).astype(np.float32))
+            q = synth.queries(seed, l, s, target[s], Hq, G, d)
+            skv.decode_append(l, from_bits(kg, dev), from_bits(vg, dev), it)
+            orc.decode_append(l, kg, vg, script[s])
+            if mode == "split":
+                skv.decode_select(l, from_bits(q, dev), it, ids)
+                skv.decode_attend(l, from_bits(q, dev), out)
+            else:
+                skv.decode_step(l, from_bits(q, dev), it, out, ids)
+            sc_o, ids_o, _ = orc.decode_select(l, q, script[s])
+            O_o = orc.decode_attend(l, q, ids_o)
+            sc_g = skv.scores(l).cpu().numpy()
+            E = to_bits(skv.embeddings(l))
+            got, O_g = ids.cpu().numpy(), out.cpu().numpy()
+            for b in range(B):
+                nb = len(orc.offsets(l, b)) - 1
+                grown = max(grown, nb - S0[b])
+                for g in range(G):
+                    assert np.array_equal(E[b, g, S0[b]:nb], orc.E[l][b][g][S0[b]:nb]), f"generated E s={s} l={l}"
+                    assert np.array_equal(sc_g[b, g, :nb].view(np.uint32), sc_o[b][g].view(np.uint32)), \
+                        f"scores s={s} l={l} b={b} g={g}"
+                    n = len(ids_o[b][g])
+                    assert np.array_equal(got[b, g, :n], ids_o[b][g]) and np.all(got[b, g, n:] == -1), \
+                        f"ids s={s} l={l} b={b} g={g}"
+            err = float(np.abs(O_g - O_o).max())
+            assert err <= ATOL, f"O s={s} l={l}: {err}"
+            worst = max(worst, err)
+    skv.sync()
+    return worst, grown
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_local_segment_and_growth(cuda_device, mode):
+    worst, grown = _run(mode)
+    assert grown >= 3  # several generated sentences became buckets
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_local_d128_gqa4_two_layers_tau_cap(cuda_device, mode):
+    """d = 128, grp = 4, 2 layers; tau = 40 with long generated sentences (mean 30): the A5 cap closes them."""
+    _run(mode, seed=1, B=1, M=2, Hq=16, G=4, d=128, L=2500, tau=40, steps=50, mean_sentence=30.0)
+
+
+def test_local_overflow_is_a_state_error(cuda_device):
+    """More appends than max_generated: the token is dropped and sentencekv_sync reports STATE."""
+    import paper_2504_00970_b200 as skvlib
+
+    B, Hq, G, d, L = 1, 8, 2, 64, 1000
+    toks, topics = synth.prompts(2, B, L, median=20.0)
+    K, V = synth.kv_layer(2, 0, topics, G, d)
+    skv = skvlib.SentenceKV(batch=B, layers=1, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=64,
+                            max_generated=4)
+    Kd, Vd = from_bits(K, cuda_device), from_bits(V, cuda_device)
+    skv.prefill_compress(0, Kd, Vd, token_ids=torch.from_numpy(toks).to(cuda_device), boundary_ids=synth.BOUNDARY_IDS)
+    kv = torch.zeros((B, G, d), dtype=torch.bfloat16, device=cuda_device)
+    it = torch.full((B,), 9, dtype=torch.int32, device=cuda_device)
+    for _ in range(4):
+        skv.decode_append(0, kv, kv, it)
+    skv.sync()
+    skv.decode_append(0, kv, kv, it)
+    with pytest.raises(skvlib.SkvError, match="STATE"):
+        skv.sync()
