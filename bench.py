@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--outlier-n", type=float, default=0.0, help="NEXT-3 outlier split at mean + n*std (0 = off)")
     ap.add_argument("--query", choices=["mean", "current"], default="mean", help="NEXT-3 current-token query")
     ap.add_argument("--fill", choices=["prefix", "skip"], default="prefix", help="NEXT-3 skip-and-continue fill")
+    ap.add_argument("--local", action="store_true",
+                    help="NEXT-2: every step appends the token's K/V (local segment, context growth)")
     ap.add_argument("--residency", choices=["device", "host"], default=None,
                     help="K/V residency (default: host for 8b-128k, which configs[2] specifies, else device)")
     return ap.parse_args()
@@ -95,7 +97,8 @@ def config_dict(args, cfg, GB, extra=None):
                              getattr(args, "buckets", "sentence") != "sentence"),
                             (f"outlier{getattr(args, 'outlier_n', 0)}", getattr(args, "outlier_n", 0) > 0),
                             ("current-query", getattr(args, "query", "mean") == "current"),
-                            ("skip-fill", getattr(args, "fill", "prefix") == "skip")) if on]
+                            ("skip-fill", getattr(args, "fill", "prefix") == "skip"),
+                            ("local", getattr(args, "local", False))) if on]
     d = {"workload": "+".join([args.config] + tags), "global_batch": GB, "layers": cfg["M"], "q_heads": cfg["Hq"],
          "kv_heads": cfg["G"], "head_dim": cfg["d"], "context": cfg["L"], "token_budget": cfg["tau"],
          "median_sentence_tokens": cfg["median"]}
@@ -271,7 +274,7 @@ def main():
     Bl, Gl, Hl = plan.batch_count, plan.kv_head_count, plan.q_head_count
     b0, g0, h0 = plan.batch_begin, plan.kv_head_begin, plan.q_head_begin
     plain = (not args.retention and args.buckets == "sentence" and args.outlier_n == 0 and args.query == "mean"
-             and args.fill == "prefix")
+             and args.fill == "prefix" and not args.local)
     cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline and plain
     check = rank == 0 and world == 1 and not args.no_check and plain
     N = args.obs_window if args.retention else 0
@@ -283,7 +286,9 @@ def main():
     tok_dev = torch.from_numpy(toks).to(dev)
     top_dev = torch.from_numpy(topics).to(dev)
     host = residency == "host"
-    variant = dict(bucket_mode={"sentence": 0, "equal": 1, "quest": 2}[args.buckets],
+    n_cold_, n_split_ = (1 if residency == "host" else 0), (0 if args.no_split else 1 + max(2, args.warmup) + min(args.steps, 100))
+    max_gen = (n_cold_ + 2 + max(1, args.warmup) + args.steps + 1 + 4 + n_split_ + args.e2e_steps + 8) if args.local else 0
+    variant = dict(max_generated=max_gen, bucket_mode={"sentence": 0, "equal": 1, "quest": 2}[args.buckets],
                    chunk_size=args.page if args.buckets == "quest" else 0, outlier_n=args.outlier_n,
                    query_mode=1 if args.query == "current" else 0, fill_mode=1 if args.fill == "skip" else 0)
     skv = skvlib.SentenceKV(layers=M, head_dim=d, max_context=L, token_budget=tau, device=local,
@@ -353,6 +358,15 @@ def main():
         gen.manual_seed(1234 + 104729 * l + 7919 * rank)
         qall[:, l] = (cl + torch.randn(cl.shape, generator=gen, device=dev)).to(torch.bfloat16)
     tall = torch.from_numpy(script).to(dev)                     # [NQ][Bl]
+    kvall = None
+    if args.local:  # NEXT-2: this step's generated K/V per layer, drawn like the context's (topic + noise)
+        kvall = torch.empty((NQ, M, 2, Bl, Gl, d), dtype=torch.bfloat16, device=dev)
+        for l in range(M):
+            gen.manual_seed(777 + 104729 * l + 7919 * rank)
+            cl = Cs[l][g0:g0 + Gl][:, tgt.long(), :].permute(1, 2, 0, 3)  # [NQ][Bl][Gl][d]
+            kvall[:, l, 0] = (cl + torch.randn(cl.shape, generator=gen, device=dev)).to(torch.bfloat16)
+            kvall[:, l, 1] = torch.randn(cl.shape, generator=gen, device=dev).to(torch.bfloat16)
+    kvbuf = torch.empty((M, 2, Bl, Gl, d), dtype=torch.bfloat16, device=dev) if args.local else None
     qbuf = torch.empty((M, Bl, Hl, d), dtype=torch.bfloat16, device=dev)  # static inputs of the graph
     tbuf = torch.empty((Bl,), dtype=torch.int32, device=dev)
     outs = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
@@ -370,9 +384,13 @@ def main():
     def load(k):
         qbuf.copy_(qall[k], non_blocking=True)
         tbuf.copy_(tall[k], non_blocking=True)
+        if kvbuf is not None:
+            kvbuf.copy_(kvall[k], non_blocking=True)
 
     def body(with_tokens=False, split=False):
         for l in range(M):
+            if kvbuf is not None:  # NEXT-2: the token's K/V joins the local segment before its attention
+                skv.decode_append(l, kvbuf[l, 0], kvbuf[l, 1], tbuf)
             if split:
                 skv.decode_select(l, qbuf[l], tbuf, sel_tokens=sel_tok[l] if with_tokens else None)
                 skv.decode_attend(l, qbuf[l], outs[l])
@@ -584,6 +602,8 @@ def main():
         qdev.copy_(qhost[j], non_blocking=True)
         tdev.copy_(thost[j], non_blocking=True)
         for l in range(M):
+            if kvbuf is not None:  # NEXT-2 (the step's K/V from the device pool, not counted in h2d)
+                skvlib.sentencekv_decode_append(skv.ctx, l, kvall[k0 + j, l, 0], kvall[k0 + j, l, 1], tdev)
             skvlib.sentencekv_decode_step(skv.ctx, l, qdev[l], tdev, odev[l])
             if world > 1:
                 parallel.all_gather_outputs(odev[l], plan, gathered=gath[l])

@@ -334,7 +334,7 @@ struct LayerView {
     skv::GenSrc gen;       // NEXT-2 generated rows + local segment (gen.Kg == nullptr: off)
 };
 static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
-    const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0};
+    const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0x7fffffff};  // no generated rows
     if (ls.retained) return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false, none};
     if (ls.genK)
         return {ls.goff, c->Smax + 1, ls.gS, ls.K, ls.V, c->L, nullptr, 0, false,

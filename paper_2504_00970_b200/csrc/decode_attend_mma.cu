@@ -135,11 +135,11 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     const __nv_bfloat16* Kgu = gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr;
     const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
     auto rowK = [&](int r) -> const __nv_bfloat16* {
-        if (!HOST) return r >= gen.L ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
+        if (!HOST) return (gen.Kg && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
         return r >= 0 ? Kh + (size_t)r * D : Kp + (size_t)(-(r + 1)) * D;
     };
     auto rowV = [&](int r) -> const __nv_bfloat16* {
-        if (!HOST) return r >= gen.L ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
+        if (!HOST) return (gen.Kg && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
         return r >= 0 ? Vh + (size_t)r * D : Vp + (size_t)(-(r + 1)) * D;
     };
 

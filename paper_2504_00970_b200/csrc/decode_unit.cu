@@ -1088,10 +1088,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         const __nv_bfloat16* Kgu = gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr;
         const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
         auto devK = [&](int r) -> const __nv_bfloat16* {
-            return (!HOST && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
+            return (!HOST && gen.Kg && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
         };
         auto devV = [&](int r) -> const __nv_bfloat16* {
-            return (!HOST && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
+            return (!HOST && gen.Kg && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
         };
         unsigned long long host_bytes = 0;
         uint4 qseg[D / 32];
