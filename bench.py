@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-check", action="store_true", help="skip the end-of-run oracle check")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--shard", choices=["heads", "batch"], default="heads")
+    ap.add_argument("--gather", choices=["nccl", "fused"], default="nccl",
+                    help="N > 1: the per-layer output all-gather by NCCL (default) or fused into the attention "
+                         "epilogue (peer stores into torch symmetric memory + arrival counters, SURVEY 8(e))")
     ap.add_argument("--retention", action="store_true",
                     help="NEXT-1: importance-filtered retention at prefill (observation window of --obs-window "
                          "queries, top floor(r*tau) tokens kept in an HBM pool); decode ranks and attends the pool")
@@ -371,6 +374,23 @@ def main():
     tbuf = torch.empty((Bl,), dtype=torch.int32, device=dev)
     outs = torch.empty((M, Bl, Hl, d), dtype=torch.float32, device=dev)
     gath = [torch.empty((world, Bl, Hl, d), dtype=torch.float32, device=dev) for _ in range(M)] if world > 1 else None
+    fused = world > 1 and args.gather == "fused"
+    if fused:
+        # every rank's gather buffers and arrival counters in symmetric memory; the kernels store their
+        # outputs into every peer's buffer and count arrivals (sentencekv_set_output_peers)
+        import torch.distributed._symmetric_memory as symm_mem
+
+        gbuf = symm_mem.empty((M, world, Bl, Hl, d), dtype=torch.float32, device=dev)
+        fbuf = symm_mem.empty((M,), dtype=torch.int32, device=dev)
+        fbuf.zero_()
+        hb = symm_mem.rendezvous(gbuf, dist.group.WORLD)
+        hf = symm_mem.rendezvous(fbuf, dist.group.WORLD)
+        dist.barrier()
+        lay = world * Bl * Hl * d * 4
+        for l in range(M):
+            skv.set_output_peers(l, rank, [hb.buffer_ptrs[p] + l * lay for p in range(world)],
+                                 [hf.buffer_ptrs[p] + 4 * l for p in range(world)])
+        gath = [gbuf[l] for l in range(M)]
     sel_tok = torch.zeros((M, Bl, Gl), dtype=torch.int32, device=dev)
     history = []  # script index of every decode step executed on the context, in order
     nxt = [0]
@@ -396,7 +416,9 @@ def main():
                 skv.decode_attend(l, qbuf[l], outs[l])
             else:
                 skv.decode_step(l, qbuf[l], tbuf, outs[l], sel_tokens=sel_tok[l] if with_tokens else None)
-            if world > 1:  # the one exchange: all-gather of the per-head outputs of the layer
+            if fused:  # the exchange happened in the kernel's epilogue: wait for every rank's arrivals
+                skv.wait_outputs(l)
+            elif world > 1:  # the one exchange: all-gather of the per-head outputs of the layer
                 parallel.all_gather_outputs(outs[l], plan, gathered=gath[l])
 
     # cold step (host residency): the first decode step after the prefill finds the HBM page cache
@@ -605,7 +627,9 @@ def main():
             if kvbuf is not None:  # NEXT-2 (the step's K/V from the device pool, not counted in h2d)
                 skvlib.sentencekv_decode_append(skv.ctx, l, kvall[k0 + j, l, 0], kvall[k0 + j, l, 1], tdev)
             skvlib.sentencekv_decode_step(skv.ctx, l, qdev[l], tdev, odev[l])
-            if world > 1:
+            if fused:
+                skv.wait_outputs(l)
+            elif world > 1:
                 parallel.all_gather_outputs(odev[l], plan, gathered=gath[l])
             ev_o[l].record(c)
             with torch.cuda.stream(cstream):
@@ -658,7 +682,8 @@ def main():
                     "queries every step, topic switch after each boundary input)",
             "config": config_dict(args, cfg, GB),
             "run": {"sentences_rank0": S, "residency": "pinned host K/V + HBM working set" if host else "device (HBM)",
-                    "parallelism": f"{plan.batch_shards} batch x {plan.head_shards} KV-head shards",
+                    "parallelism": f"{plan.batch_shards} batch x {plan.head_shards} KV-head shards"
+                                   + (", fused gather epilogue" if fused else (", NCCL all-gather" if world > 1 else "")),
                     "l2": f"inputs > L2: {(e_bytes + kv_bytes) * M / 1e9:.2f} GB read per step per GPU (L2 126 MB), "
                           "no flush needed",
                     "cuda_graph": graph is not None},

@@ -255,6 +255,24 @@ skv_status sentencekv_decode_step(skv_ctx* ctx, int32_t layer, const void* q, co
 skv_status sentencekv_decode_append(skv_ctx* ctx, int32_t layer, const void* k, const void* v,
                                     const int32_t* input_token, skv_stream_t stream);
 
+/*
+ * Multi-GPU: the per-layer all-gather of the per-head outputs fused into the attention
+ * epilogue.  After this call, every decode_attend / decode_step of `layer` also stores its outputs
+ * into slot `rank` of every peer's gather buffer and, once the unit's outputs are in, adds 1 to every
+ * peer's arrival counter (release, system scope).
+ * peer_out   host array [world] of device pointers, peer-accessible from this device (e.g. torch
+ *            symmetric memory over NVLink): rank p's buffer fp32 [world][batch_count][kv_head_count*grp][d]
+ *            (the rank-major layout of an all-gather; all ranks hold equal shards)
+ * peer_flag  host array [world] of device pointers to uint32 arrival counters, zero at the first step
+ * world = 0 or peer_out == NULL turns it off (the caller's collective).  world <= 8.
+ */
+skv_status sentencekv_set_output_peers(skv_ctx* ctx, int32_t layer, int32_t world, int32_t rank, float* const* peer_out,
+                                       uint32_t* const* peer_flag);
+
+/* Enqueues on `stream` a wait until every rank's outputs of this step's `layer` are in this rank's buffer
+ * (world x units arrivals more than at the previous call; acquire, system scope).  CUDA-graph capturable. */
+skv_status sentencekv_wait_outputs(skv_ctx* ctx, int32_t layer, skv_stream_t stream);
+
 /* ---- introspection (tests, bench; not on the per-token path) ---- */
 
 /* Sentence counts of the current prompt: S_out host int32 [batch_count]. */

@@ -72,6 +72,8 @@ def _load():
         "sentencekv_decode_attend": (i32, [P, i32, P, P, P]),
         "sentencekv_decode_step": (i32, [P, i32, P, P, P, P, P, P, P]),
         "sentencekv_decode_append": (i32, [P, i32, P, P, P, P]),
+        "sentencekv_set_output_peers": (i32, [P, i32, i32, i32, P, P]),
+        "sentencekv_wait_outputs": (i32, [P, i32, P]),
         "sentencekv_sentence_counts": (i32, [P, P]),
         "sentencekv_sentence_capacity": (i32, [P]),
         "sentencekv_copy_offsets": (i32, [P, P, P]),
@@ -234,6 +236,16 @@ class SentenceKV:
     def decode_append(self, layer, k, v, input_token, stream=None):
         """NEXT-2: this step's key / value [B][G][d] into the local segment (before the step's decode)."""
         sentencekv_decode_append(self.ctx, layer, k, v, input_token, stream)
+
+    def set_output_peers(self, layer, rank, peer_out, peer_flag):
+        """8(e) fused gather: peer_out / peer_flag = lists of device pointers (ints or tensors) of every rank."""
+        world = len(peer_out)
+        arr = lambda xs: (ctypes.c_void_p * world)(*[x.data_ptr() if isinstance(x, torch.Tensor) else int(x) for x in xs])
+        _check(self.ctx, lib.sentencekv_set_output_peers(self.ctx, int(layer), world, int(rank), arr(peer_out),
+                                                         arr(peer_flag)))
+
+    def wait_outputs(self, layer, stream=None):
+        _check(self.ctx, lib.sentencekv_wait_outputs(self.ctx, int(layer), _stream(stream)))
 
     def decode_step(self, layer, q, input_token, out, sel_ids=None, sel_count=None, sel_tokens=None, stream=None):
         sentencekv_decode_step(self.ctx, layer, q, input_token, out, sel_ids, sel_count, sel_tokens, stream)

@@ -270,6 +270,7 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
         dfree(ls.Sq);
         dfree(ls.cnt);
         dfree(ls.ledger);
+        dfree(ls.peer_target);
         free_host_store(ls);
         free_retention(ls);
         if (ls.offload_done) cudaEventDestroy(ls.offload_done);
@@ -696,6 +697,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.sid_stride = v.sid_stride;
         a.qmode = c->cfg.query_mode;
         a.gen = v.gen;
+        a.peers = ls.peers;
         a.B = c->B;
         a.G = c->G;
         a.Smax = c->Smax;
@@ -749,6 +751,53 @@ SKV_API skv_status sentencekv_decode_append(skv_ctx* c, int32_t layer, const voi
     return SKV_OK;
 }
 
+SKV_API skv_status sentencekv_set_output_peers(skv_ctx* c, int32_t layer, int32_t world, int32_t rank,
+                                               float* const* peer_out, uint32_t* const* peer_flag) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (world == 0 || !peer_out) {  // back to the caller's collective
+        ls.peers = skv::OutPeers{};
+        ls.peer_local_flag = nullptr;
+        return SKV_OK;
+    }
+    if (world < 1 || world > skv::kMaxPeers || rank < 0 || rank >= world || !peer_flag)
+        return fail(c, SKV_ERR_INVALID_ARGUMENT, "world must be 1..%d with rank < world and both pointer arrays",
+                    skv::kMaxPeers);
+    for (int p = 0; p < world; ++p)
+        if (!peer_out[p] || !peer_flag[p] || !aligned16(peer_out[p]))
+            return fail(c, SKV_ERR_INVALID_ARGUMENT, "peer %d: NULL or unaligned pointer", p);
+    DeviceGuard dg(c->cfg.device);
+    if (!ls.peer_target) {
+        SKV_CUDA(c, dalloc(&ls.peer_target, 1));
+    }
+    SKV_CUDA(c, cudaMemset(ls.peer_target, 0, sizeof(unsigned int)));
+    skv::OutPeers pp{};
+    const size_t slot = (size_t)c->B * c->Hq * c->d;  // one rank's [B][Hq_loc][d] outputs
+    for (int p = 0; p < world; ++p) {
+        pp.out[p] = peer_out[p] + (size_t)rank * slot;
+        pp.flag[p] = reinterpret_cast<unsigned int*>(peer_flag[p]);
+    }
+    pp.n = world;
+    ls.peers = pp;
+    ls.peer_local_flag = reinterpret_cast<unsigned int*>(peer_flag[rank]);
+    ls.peer_per_step = (unsigned int)world * (unsigned int)(c->B * c->G);
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_wait_outputs(skv_ctx* c, int32_t layer, skv_stream_t stream_) {
+    if (!c) return SKV_ERR_INVALID_ARGUMENT;
+    if (c->sticky != SKV_OK) return c->sticky;
+    if (layer < 0 || layer >= c->cfg.layers) return fail(c, SKV_ERR_STATE, "layer %d out of range", layer);
+    skv::LayerState& ls = c->layer[layer];
+    if (!ls.peer_local_flag) return fail(c, SKV_ERR_STATE, "layer %d has no output peers", layer);
+    DeviceGuard dg(c->cfg.device);
+    SKV_CUDA(c, skv::launch_wait_peers(ls.peer_local_flag, ls.peer_target, ls.peer_per_step,
+                                       reinterpret_cast<cudaStream_t>(stream_)));
+    c->launches += 1;
+    return SKV_OK;
+}
+
 SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const void* q, float* out,
                                             skv_stream_t stream_) {
     if (!c) return SKV_ERR_INVALID_ARGUMENT;
@@ -771,12 +820,13 @@ SKV_API skv_status sentencekv_decode_attend(skv_ctx* c, int32_t layer, const voi
         }
         pa = prof_begin(c, st);
         SKV_CUDA(c, skv::launch_attend_mma(qb, skv::KvSrc{ls.wsK, ls.wsV, 0, 0}, ls.Kh, ls.Vh, c->L, ls.wsK, ls.wsV,
-                                           true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, v.gen, st));
+                                           true, c->B, c->G, c->grp, c->d, ls.sel, ls.ledger, qs, out, v.gen, ls.peers,
+                                           st));
     } else {
         pa = prof_begin(c, st);
         const skv::KvSrc kv{v.K, v.V, v.stride, 0};
         SKV_CUDA(c, skv::launch_attend_mma(qb, kv, nullptr, nullptr, (int)v.stride, nullptr, nullptr, false, c->B, c->G,
-                                           c->grp, c->d, ls.sel, nullptr, qs, out, v.gen, st));
+                                           c->grp, c->d, ls.sel, nullptr, qs, out, v.gen, ls.peers, st));
     }
     prof_end(c, SKV_K_ATTEND, pa, st);
     c->launches += 1;

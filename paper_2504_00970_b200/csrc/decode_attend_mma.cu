@@ -37,7 +37,7 @@ __global__ void __cluster_dims__(kMCL, 1, 1) __launch_bounds__(kMT, 2)
 attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bfloat16* Khost,
                   const __nv_bfloat16* Vhost, int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, int G, SelBufs sel,
                   unsigned long long* __restrict__ ledger, QsState qs, float* __restrict__ out, GenSrc gen,
-                  float scale_log2) {
+                  OutPeers peers, float scale_log2) {
     static_assert(GRP <= 8, "heads fill the N = 8 side");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MmaSmem<D>& sm = *reinterpret_cast<MmaSmem<D>*>(smem_raw);
@@ -202,18 +202,22 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     SKV_TRACE_POINT(9);
     cluster.sync();
     SKV_TRACE_POINT(10);
-    mma::merge_cluster<D, GRP, kMW, kMCL>(cluster, sm, rank, out + ((size_t)b * Hq + g * GRP) * D, kMT);
+    mma::merge_cluster<D, GRP, kMW, kMCL>(cluster, sm, rank, out + ((size_t)b * Hq + g * GRP) * D, kMT, &peers,
+                                          ((size_t)b * Hq + g * GRP) * D);
     SKV_TRACE_POINT(11);
     cluster.sync();
     SKV_TRACE_POINT(12);
-    if (rank == 0 && tid == 0) sel.parity[unit] = cur;
+    if (rank == 0 && tid == 0) {
+        sel.parity[unit] = cur;
+        if (peers.n) peers_arrive(peers);
+    }
 }
 
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16* q, KvSrc kv,
                                 const __nv_bfloat16* Kh, const __nv_bfloat16* Vh, int L, __nv_bfloat16* wsK,
                                 __nv_bfloat16* wsV, int G, SelBufs sel, unsigned long long* ledger, QsState qs,
-                                float* out, GenSrc gen, float scale_log2) {
+                                float* out, GenSrc gen, OutPeers peers, float scale_log2) {
     // metadata: tok[tau+1] + srcs[tau] (+ pids[tau] + ptok[tau+1]) + rowtab[per-CTA tokens]; the
     // NEXT-2 local segment adds up to tau attended tokens
     const size_t tiles = ((size_t)sel.tau * (gen.Kg ? 2 : 1) + kTile - 1) / kTile;
@@ -223,18 +227,18 @@ static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16*
     cudaError_t e = ensure_smem((const void*)attend_mma_kernel<D, GRP, HOST>, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(false, attend_mma_kernel<D, GRP, HOST>, grid, dim3(kMT), smem, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel,
-                      ledger, qs, out, gen, scale_log2);
+                      ledger, qs, out, gen, peers, scale_log2);
 }
 
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
                               SelBufs sel, unsigned long long* ledger, QsState qs, float* out, GenSrc gen,
-                              cudaStream_t st) {
+                              OutPeers peers, cudaStream_t st) {
     dim3 grid(kMCL, G, B);
     const float scale_log2 = (float)(1.0 / sqrt((double)d) * 1.4426950408889634);
 #define SKV_MM(DV, GV)                                                                                          \
-    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, scale_log2) \
-                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, scale_log2)
+    return host ? launch_mma_t<DV, GV, true>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, peers, scale_log2) \
+                : launch_mma_t<DV, GV, false>(grid, st, q, kv, Kh, Vh, L, wsK, wsV, G, sel, ledger, qs, out, gen, peers, scale_log2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_MM(128, 1);

@@ -224,7 +224,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                  int4* __restrict__ cand_g, uint2* __restrict__ hint, int band_w, float* __restrict__ out,
                  int32_t* __restrict__ out_ids, int32_t* __restrict__ out_count,
                  int32_t* __restrict__ out_tokens, const int32_t* __restrict__ sid, int sid_stride, int qmode,
-                 GenSrc gen, float scale_log2, int trace_idx) {
+                 GenSrc gen, OutPeers peers, float scale_log2, int trace_idx) {
     constexpr int TPS = 4;                      // threads per sentence (scoring)
     constexpr int NPT = D / 8 / TPS;            // canonical 8-dim partials per thread (4 or 2)
     constexpr int GPW = 32 / TPS;               // sentences per warp step
@@ -1199,7 +1199,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     }
     cluster.sync();  // #2: CTA partials ready
     SKV_USTAMP(8);
-    mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT);
+    mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT, &peers,
+                                         ((size_t)b * Hq + g * GRP) * D);
     if (HOST && rank == 0 && ctl.any_miss) {
         // page-table update of this step's plan (every CTA has done its lookups: after barrier #2);
         // all selected rows of a page with a slot are in it now
@@ -1218,7 +1219,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
     }
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
-    if (rank == 0 && tid == 0) sel.parity[unit] = cur;
+    if (rank == 0 && tid == 0) {
+        sel.parity[unit] = cur;
+        if (peers.n) peers_arrive(peers);  // every CTA's slice is in every peer's buffer (8(e) fused gather)
+    }
     SKV_USTAMP(9);
     SKV_LSTAMP(2);
 }
@@ -1255,7 +1259,8 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), a.out, a.out_ids,
-                      a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, a.gen, scale_log2, trace_counter++);
+                      a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, a.gen, a.peers, scale_log2,
+                      trace_counter++);
 }
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {

@@ -84,7 +84,27 @@ __global__ void gen_state_kernel(int B, int L, int max_gen, int tau, int32_t* __
     }
 }
 
+// SURVEY 8(e) fused gather: one thread advances the expected arrival count of this step and spins
+// (acquire, system scope) until every rank's units have counted their arrival in this rank's buffer.
+__global__ void wait_peers_kernel(const unsigned int* __restrict__ flag, unsigned int* __restrict__ target,
+                                  unsigned int per_step) {
+    if (threadIdx.x != 0) return;
+    const unsigned int want = *target + per_step;
+    *target = want;
+    unsigned int v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((int)(v - want) >= 0) break;
+        __nanosleep(64);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_wait_peers(const unsigned int* flag, unsigned int* target, unsigned int per_step, cudaStream_t st) {
+    wait_peers_kernel<<<1, 32, 0, st>>>(flag, target, per_step);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_gen_append(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* Kg, __nv_bfloat16* Vg,
                               int max_gen, int32_t* gstat, int32_t* goff, int off_stride, int32_t* gS, int Smax,

@@ -18,6 +18,23 @@
 #include "device_util.cuh"
 
 namespace skv {
+
+// SURVEY 8(e), the per-layer all-gather fused into the attention epilogue: device pointers (UVA,
+// peer-accessible: torch symmetric memory on NVLink) to every rank's gather buffer, already offset to
+// THIS rank's slot, and to every rank's arrival counter for the layer.
+constexpr int kMaxPeers = 8;
+struct OutPeers {
+    float* out[kMaxPeers];
+    unsigned int* flag[kMaxPeers];
+    int n;
+};
+
+// The unit's outputs are in every peer's buffer: count the arrival at every peer (release, system scope).
+__device__ __forceinline__ void peers_arrive(const OutPeers& p) {
+    for (int i = 0; i < p.n; ++i)
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.flag[i]) : "memory");
+}
+
 namespace mma {
 
 constexpr int kTile = 16;  // tokens per MMA tile
@@ -245,7 +262,8 @@ __device__ __forceinline__ void merge_warps(MergeSmem<D, NW>& sm, const WarpAcc<
 // merge_warps in every CTA; CTA `rank` writes its 1/NC share of the GRP x D outputs to `out`.
 template <int D, int GRP, int NW, int NC>
 __device__ __forceinline__ void merge_cluster(cooperative_groups::cluster_group& cluster, MergeSmem<D, NW>& sm,
-                                              int rank, float* __restrict__ out, int nthreads) {
+                                              int rank, float* __restrict__ out, int nthreads,
+                                              const OutPeers* peers = nullptr, size_t peer_off = 0) {
     constexpr int E = (GRP * D + NC - 1) / NC;
     const int e0 = rank * E;
     for (int idx = e0 + (int)threadIdx.x; idx < min(GRP * D, e0 + E); idx += nthreads) {
@@ -268,8 +286,12 @@ __device__ __forceinline__ void merge_cluster(cooperative_groups::cluster_group&
             den = fmaf(w, lr[r], den);
             num = fmaf(w, orr[r], num);
         }
-        out[idx] = num / den;
+        const float o = num / den;
+        out[idx] = o;
+        if (peers)  // multi-GPU: the same value straight into this rank's slot of every peer's gather buffer
+            for (int p = 0; p < peers->n; ++p) peers->out[p][peer_off + idx] = o;
     }
+    if (peers && peers->n) asm volatile("fence.acq_rel.sys;" ::: "memory");  // before the flag release
 }
 
 }  // namespace mma

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/sentencekv.h"
+#include "mma_attend.cuh"
 
 namespace skv {
 
@@ -107,6 +108,11 @@ struct LayerState {
     int32_t* gstat = nullptr;          // [B][4]
     int32_t* goff = nullptr;           // [B][Smax+1] the prompt's offsets followed by completed generated sentences
     int32_t* gS = nullptr;             // [B] buckets
+    // SURVEY 8(e) fused all-gather epilogue (sentencekv_set_output_peers)
+    OutPeers peers{};
+    unsigned int* peer_local_flag = nullptr;  // this rank's arrival counter for the layer (peer memory)
+    unsigned int* peer_target = nullptr;      // device: arrivals expected so far
+    unsigned int peer_per_step = 0;           // world * units per rank
 };
 
 }  // namespace skv
@@ -211,7 +217,11 @@ cudaError_t launch_select(const float* scores, const int32_t* off, int off_strid
 cudaError_t launch_attend_mma(const __nv_bfloat16* q, KvSrc kv, const __nv_bfloat16* Kh, const __nv_bfloat16* Vh,
                               int L, __nv_bfloat16* wsK, __nv_bfloat16* wsV, bool host, int B, int G, int grp, int d,
                               SelBufs sel, unsigned long long* ledger, QsState qs, float* out, GenSrc gen,
-                              cudaStream_t st);
+                              OutPeers peers, cudaStream_t st);
+
+// SURVEY 8(e) fused gather: wait until `target` (advanced by `per_step` on the device each call)
+// arrivals have been counted in *flag (acquire, system scope).
+cudaError_t launch_wait_peers(const unsigned int* flag, unsigned int* target, unsigned int per_step, cudaStream_t st);
 
 // NEXT-2 (local.cu): close the sentence that ended at the previous token into a bucket, append this
 // token's k, v ([B][G][d]) to the generated store, advance the per-sequence state
@@ -266,6 +276,7 @@ struct UnitArgs {
     int sid_stride;
     int qmode;                     // 0 = Eq. 2 mean query, 1 = current token's query (NEXT-3)
     GenSrc gen;                    // NEXT-2 local segment (gen.Kg == nullptr: off)
+    OutPeers peers;                // 8(e) fused gather (peers.n == 0: off)
 };
 bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, bool local);
 int unit_page_tokens();

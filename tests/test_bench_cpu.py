@@ -55,5 +55,5 @@ def test_bench_two_ranks_same_gpu():
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     (line,) = _lines(r.stdout)
-    assert line["n_gpus"] == 2 and line["run"]["parallelism"] == "1 batch x 2 KV-head shards"
+    assert line["n_gpus"] == 2 and line["run"]["parallelism"].startswith("1 batch x 2 KV-head shards")
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] == 32 * 4
