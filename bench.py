@@ -503,6 +503,20 @@ def main():
     ms_step = ms_total / args.steps
     value = GB / (ms_step / 1e3)
     host_step_bytes = (sum(skv.host_fetch_bytes(l) for l in range(M)) - ledger0) / args.steps if host else 0
+    link_gbs = None
+    if host:  # the host link's copy rate on this box (pinned -> HBM, 256 MB, CUDA events): the link roofline
+        hsrc = torch.empty(1 << 28, dtype=torch.uint8).pin_memory()
+        hdst = torch.empty(1 << 28, dtype=torch.uint8, device=dev)
+        lk = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record()
+            hdst.copy_(hsrc, non_blocking=True)
+            b_.record()
+            torch.cuda.synchronize()
+            lk.append(a_.elapsed_time(b_))
+        link_gbs = (1 << 28) / (min(lk) / 1e3) / 1e9
+        del hsrc, hdst
 
     # ---------------- end-of-run check: one more step, eager, with its selections; sampled units
     # against the CPU oracle replaying this context's whole decode history (Eq. 2 state included)
@@ -709,7 +723,15 @@ def main():
                                if prof_prefill["offload"][1] else None,
                                "offload_wall_s_incl_pinning": round(offload_s, 2) if offload_s else None,
                                "page_cache_tokens_per_unit": int(2.0 * tau), "cold_first_step": cold,
-                               "paper_onload": "PAPER.md P:740: onload 1024 tokens 0.0038 s (H100 NVL, per step)"}
+                               "paper_onload": "PAPER.md P:740: onload 1024 tokens 0.0038 s (H100 NVL, per step)",
+                               # host residency is bound by HBM AND the host link, one after the other
+                               # (the rows to fetch are known only after the selection): the step's
+                               # lower bound is HBM bytes / HBM peak + host bytes / link copy rate
+                               "link_roofline": {
+                                   "bound": "hbm + host link (serial)", "link_gbs_measured": round(link_gbs, 2),
+                                   "hbm_bytes_per_step": int(unit_bytes * M), "host_bytes_per_step": int(host_step_bytes),
+                                   "t_min_ms": round((unit_bytes * M / (hbm_peak * 1e9) + host_step_bytes / (link_gbs * 1e9)) * 1e3, 4),
+                                   "frac": round((unit_bytes * M / (hbm_peak * 1e9) + host_step_bytes / (link_gbs * 1e9)) * 1e3 / ms_step, 4)}}
             if host else None,
             "end_check": chk,
             "retention": ret,
