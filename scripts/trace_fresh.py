@@ -56,7 +56,15 @@ for step in range(STEPS):
         reason = T[::8, 10].astype(int) & 15
         for u in np.nonzero(gen_path[::8])[0]:
             why.append((step, l, int(u), int(reason[u]), int(T[u * 8, 13])))
-        rows.append(dict(step=step, layer=l, span=t(9).max(), scored=t(1).max(), selected=t(5).max(),
+        bandp = ~gen_path
+        sub = {}
+        if bandp.any():
+            for nm, (x0, x1) in (("b_decide", (2, 16)), ("b_gather", (16, 17)), ("b_rank", (17, 18)), ("b_compact", (18, 3))):
+                sub[nm] = float(np.max(t(x1)[bandp] - t(x0)[bandp]))
+        if gen_path.any():
+            for nm, (x0, x1) in (("g_local", (3, 4)), ("g_gather", (4, 19)), ("g_minmax", (19, 20)), ("g_levels", (20, 21)), ("g_compact", (21, 5))):
+                sub[nm] = float(np.max(t(x1)[gen_path] - t(x0)[gen_path]))
+        rows.append(dict(step=step, layer=l, span=t(9).max(), **sub, scored=t(1).max(), selected=t(5).max(),
                          rowtab=t(25).max(), planned=t(6).max(), attended=t(7).max(), csync2=t(8).max(),
                          miss_ctas=int(miss.sum()), gen_ctas=int(gen_path.sum()), host_mb=hb / 1e6,
                          att_miss=np.median(t(7)[miss] - t(6)[miss]) if miss.any() else 0.0,
@@ -65,13 +73,15 @@ for step in range(STEPS):
                          **({f"p{k}": float(np.median(t(k)[miss] - t(k - 1 if k > 26 else 25)[miss])) for k in (26, 27, 28, 29, 30)}
                             if miss.any() else {f"p{k}": 0.0 for k in (26, 27, 28, 29, 30)})))
 import statistics as st
-keys = ["span", "scored", "selected", "rowtab", "planned", "attended", "csync2", "miss_ctas", "gen_ctas", "host_mb", "plan_miss", "att_miss", "att_hit", "p26", "p27", "p28", "p29", "p30"]
+keys = ["span", "scored", "selected", "rowtab", "planned", "attended", "csync2", "miss_ctas", "gen_ctas", "host_mb", "plan_miss", "att_miss", "att_hit", "p26", "p27", "p28", "p29", "p30",
+        "b_decide", "b_gather", "b_rank", "b_compact", "g_local", "g_gather", "g_minmax", "g_levels", "g_compact"]
 print(f"residency={'host' if HOST else 'device'}{' +retention' if RET else ''} layers={M} steps={STEPS}: per launch (max over CTAs of phase end, us since first CTA start)")
-print("  all  : " + " ".join(f"{k}={st.median([r[k] for r in rows]):.2f}" for k in keys))
+med = lambda rs, k: st.median([r[k] for r in rs if k in r]) if any(k in r for r in rs) else float("nan")
+print("  all  : " + " ".join(f"{k}={med(rows, k):.2f}" for k in keys))
 for sel, name in ((lambda r: r["miss_ctas"] == 0, "nomiss"), (lambda r: 0 < r["miss_ctas"] and r["host_mb"] < 1, "fewmiss"), (lambda r: r["host_mb"] >= 1, "bigmiss")):
     rs = [r for r in rows if sel(r)]
     if rs:
-        print(f"  {name:6s} n={len(rs):4d}: " + " ".join(f"{k}={st.median([r[k] for r in rs]):.2f}" for k in keys))
+        print(f"  {name:6s} n={len(rs):4d}: " + " ".join(f"{k}={med(rs, k):.2f}" for k in keys))
 from collections import Counter
 late = [w for w in why if w[0] > 0]
 print("general-path units after step 0:", len(late), "of", (STEPS - 1) * M * B * G, "unit-launches; reasons (1 ovf, 2 above>tau, 4 below band):",

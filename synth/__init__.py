@@ -11,7 +11,8 @@ bytes it produces.
 - K/V: each sentence draws one of T = 64 topics; K_t = bf16(c[layer, g, topic] + N(0, 1)),
   V_t = bf16(N(0, 1)); c ~ N(0, I_d).  (Topic structure as in SPEC.md S:58.)
 - Queries: q_t = bf16(c[layer, g(h), target] + N(0, 1)); the target topic changes whenever
-  the step's input token is a boundary (about every 25 steps).
+  the step's input token is a boundary: generated sentences follow the prompt's length
+  distribution (median 25), staggered across sequences.
 """
 from __future__ import annotations
 
@@ -93,11 +94,20 @@ def kv_layer(seed: int, layer: int, topics: np.ndarray, G: int, d: int):
 
 
 def decode_script(seed: int, B: int, steps: int, boundary_ids=BOUNDARY_IDS, mean_sentence: float = 25.0):
-    """Per step: input token ids [steps][B] (a boundary about every 25 steps) and the
-    target topic of each step [steps][B] (changes after each boundary)."""
+    """Per step: input token ids [steps][B] and the target topic of each step [steps][B].
+
+    The generated text of each sequence is a run of sentences whose lengths follow the prompt's
+    distribution (lognormal, median `mean_sentence`, clamp [2, 256]); the last token of each sentence
+    is a boundary id, after which the target topic changes.  The first sentence of each sequence
+    starts at a random phase, so the sequences' boundaries are staggered."""
     rng = _rng(seed, 0xDEC0)
     bset = np.asarray(boundary_ids, dtype=np.int32)
-    is_b = rng.random((steps, B)) < 1.0 / mean_sentence
+    is_b = np.zeros((steps, B), dtype=bool)
+    for b in range(B):
+        n = np.clip(np.rint(np.exp(rng.normal(np.log(mean_sentence), 0.5, size=steps + 2))), 2, 256).astype(np.int64)
+        ends = np.cumsum(n) - 1 - int(rng.integers(0, n[0]))
+        ends = ends[(ends >= 0) & (ends < steps)]
+        is_b[ends, b] = True
     tok = rng.integers(VOCAB_LO, VOCAB_HI, size=(steps, B)).astype(np.int32)
     tok = np.where(np.isin(tok, bset), VOCAB_LO, tok).astype(np.int32)
     tok[is_b] = bset[rng.integers(0, len(bset), size=int(is_b.sum()))]
