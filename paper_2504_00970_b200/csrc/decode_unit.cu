@@ -124,6 +124,7 @@ constexpr int kUExact = kUT;             // crossing-bin candidates ranked exact
 constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
 constexpr int kUBandCap = 256;           // band-path list entries per CTA
 constexpr int kBentCap = 2 * 4 * kULocalCap / 16;  // packed band entries in the (idle) keys + offsets area
+constexpr int kBandQuad = 384;           // band entries ranked by the quadratic loop (more: histogram ranking)
 static_assert(kUC * kUBandCap * (16 + 4 + 4) <= kUStages * kUTileBytes, "band lists fit the ring");
 using mma::kInvalid;
 using mma::kTile;
@@ -547,10 +548,117 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         __syncthreads();
         SKV_USTAMP(17);
-        {
-            // a band entry is selected iff (weight above the band) + (weight of band entries ranked
-            // above it) + its length fits tau; the one that first does not fit is the crossing point
-            const int nbd = ctl.nband;
+        // a band entry is selected iff (weight above the band) + (weight of band entries ranked above
+        // it) + its length fits tau; the one that first does not fit is the crossing point.  Small
+        // bands: every entry counts the weight above it (quadratic, no barrier).  Large bands (many
+        // short buckets, e.g. after NEXT-1 retention: measured 24.6 us for the quadratic loop): the
+        // range-refining length histogram of the general path over the band entries, O(n) per level.
+        const int nbd = ctl.nband;
+        bool quad = nbd <= kBandQuad;
+        if (!quad) {
+            const int per_b = (nbd + kUT - 1) / kUT;
+            const int x0 = min(nbd, tid * per_b), x1 = min(nbd, x0 + per_b);
+            if (tid == 0) {
+                ctl.lo = 0xffffffffu;
+                ctl.hi = 0u;
+            }
+            __syncthreads();
+            {
+                uint32_t mn = 0xffffffffu, mx = 0u;
+                for (int x = x0; x < x1; ++x) {
+                    const uint32_t k = (uint32_t)gath[bidx[x]].x;
+                    mn = min(mn, k);
+                    mx = max(mx, k);
+                }
+                mn = __reduce_min_sync(0xffffffffu, mn);
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                if (lane == 0) {
+                    atomicMin(&ctl.lo, mn);
+                    atomicMax(&ctl.hi, mx);
+                }
+            }
+            __syncthreads();
+            uint32_t lo = ctl.lo, hi = ctl.hi, rem = (uint32_t)tau - W0;
+            bool all_fit = false, done = false;
+            unsigned long long thr = 0ull;
+            for (int level = 0; level < 4 && !done; ++level) {
+                for (int i = tid; i < kUBins; i += kUT) hist[i] = 0u;
+                __syncthreads();
+                const Binner bin(lo, hi);
+                for (int x = x0; x < x1; ++x) {
+                    const int4 e = gath[bidx[x]];
+                    const uint32_t k = (uint32_t)e.x;
+                    if (k >= lo && k <= hi) atomicAdd(&hist[bin(k)], (uint32_t)e.w);
+                }
+                __syncthreads();
+                uint32_t cb, rem_in;
+                if (!crossing_bin(hist, rem, ws32, ctl, &cb, &rem_in)) {  // (level 0 only) every entry fits
+                    all_fit = true;
+                    break;
+                }
+                if (tid == 0) {
+                    ctl.lo = 0xffffffffu;
+                    ctl.hi = 0u;
+                    ctl.ncand = 0u;
+                }
+                __syncthreads();
+                {
+                    uint32_t mn = 0xffffffffu, mx = 0u;
+                    for (int x = x0; x < x1; ++x) {
+                        const int4 e = gath[bidx[x]];
+                        const uint32_t k = (uint32_t)e.x;
+                        if (k < lo || k > hi || bin(k) != cb) continue;
+                        mn = min(mn, k);
+                        mx = max(mx, k);
+                        const uint32_t p = atomicAdd(&ctl.ncand, 1u);
+                        if (p < (uint32_t)kUExact) {
+                            ckey[p] = ukey64(k, e.y);
+                            clen[p] = (uint32_t)e.w;
+                        }
+                    }
+                    mn = __reduce_min_sync(0xffffffffu, mn);
+                    mx = __reduce_max_sync(0xffffffffu, mx);
+                    if (lane == 0) {
+                        atomicMin(&ctl.lo, mn);
+                        atomicMax(&ctl.hi, mx);
+                    }
+                }
+                __syncthreads();
+                const int nc = (int)ctl.ncand;
+                if (nc <= kUExact) {  // rank the crossing bin's entries exactly (unique key64s)
+                    if (tid < nc) {
+                        const unsigned long long mk = ckey[tid];
+                        uint32_t wab = 0;
+                        for (int c = 0; c < nc; ++c)
+                            if (ckey[c] > mk) wab += clen[c];
+                        if (wab <= rem_in && wab + clen[tid] > rem_in) ctl.thr = mk;
+                    }
+                    __syncthreads();
+                    thr = ctl.thr;
+                    done = true;
+                    break;
+                }
+                rem = rem_in;
+                lo = ctl.lo;
+                hi = ctl.hi;
+                __syncthreads();
+                if (lo == hi) break;  // > kUExact entries tie on one score: the quadratic rank below
+            }
+            if (all_fit || done) {
+                for (int x = x0; x < x1; ++x) {
+                    const int i = bidx[x];
+                    const int4 e = gath[i];
+                    if (all_fit || ukey64((uint32_t)e.x, e.y) > thr) flag[i] = 1;
+                }
+                if (tid == 0 && !all_fit) {
+                    ctl.kc = (uint32_t)(thr >> 32);  // the crossing sentence
+                    ctl.kc_set = 1;
+                }
+            } else {
+                quad = true;
+            }
+        }
+        if (quad) {
             const uint32_t WHI = W0;
             // band entries packed as (key, ~id, length) in the idle keys/offsets area, so the
             // quadratic rank loop reads one broadcast 16-byte word per entry, no indirection
