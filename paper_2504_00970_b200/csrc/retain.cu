@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "device_util.cuh"
 #include "skv_internal.cuh"
@@ -314,6 +315,158 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 }
 
 // ---------------------------------------------------------------------------- top-k + buckets
+// Multi-CTA top-m of ordered(alpha) per sequence (r02: the one-CTA-per-sequence version took 258 us
+// per layer): 3 radix levels of 11 / 11 / 10 bits, each a histogram over all CTAs (shared-memory
+// histogram, then global atomics) and one digit search per sequence; then per-CTA counts of the keys
+// above / at the threshold, one scan per sequence, and the ordered keep writes.  Ties at the
+// threshold key -> lowest index (A21): the first (m - #greater) equal keys in index order.
+constexpr int kTkThreads = 256;
+constexpr int kTkChunk = 2048;   // candidates per CTA
+constexpr int kTkBins = 2048;
+
+__device__ __forceinline__ int tk_shift(int level) { return level == 0 ? 21 : level == 1 ? 10 : 0; }
+__device__ __forceinline__ uint32_t tk_bins(int level) { return level == 2 ? 1024u : 2048u; }
+
+// tstate[b] = {prefix, need, -, -}; hist [B][kTkBins] zero on entry
+__global__ void __launch_bounds__(kTkThreads) topk_hist_kernel(const float* __restrict__ alpha, int Lc, int level,
+                                                              const uint32_t* __restrict__ tstate,
+                                                              uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kTkBins];
+    const int b = blockIdx.y;
+    const int shift = tk_shift(level);
+    const uint32_t hmask = level == 0 ? 0u : (0xffffffffu << (tk_shift(level - 1)));
+    const uint32_t prefix = tstate[b * 4];
+    for (int i = threadIdx.x; i < kTkBins; i += kTkThreads) h[i] = 0u;
+    __syncthreads();
+    const float* a = alpha + (size_t)b * Lc;
+    const int j0 = blockIdx.x * kTkChunk, j1 = min(Lc, j0 + kTkChunk);
+    const uint32_t dmask = tk_bins(level) - 1u;
+#pragma unroll 4
+    for (int j = j0 + threadIdx.x; j < j1; j += kTkThreads) {
+        const uint32_t k = ordered_key(a[j]);
+        if ((k & hmask) == prefix) atomicAdd(&h[(k >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (int)tk_bins(level); i += kTkThreads)
+        if (h[i]) atomicAdd(&hist[(size_t)b * kTkBins + i], h[i]);
+}
+
+// digit d with (count above d) < need <= (count above d) + hist[d]; prefix |= d << shift; zero hist
+__global__ void __launch_bounds__(1024) topk_digit_kernel(int level, uint32_t* __restrict__ tstate,
+                                                         uint32_t* __restrict__ hist) {
+    __shared__ uint32_t ws32[32];
+    __shared__ uint32_t s_d, s_need;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const uint32_t nb = tk_bins(level);
+    uint32_t* hb = hist + (size_t)b * kTkBins;
+    // thread t owns the 2 bins nb-1-2t, nb-2-2t (descending digits in thread order)
+    uint32_t c[2], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int bin = (int)nb - 1 - (2 * tid + k);
+        c[k] = bin >= 0 ? hb[bin] : 0u;
+        sum += c[k];
+    }
+    uint32_t tot;
+    uint32_t above = block_incl_sum<uint32_t>(sum, ws32, &tot) - sum;
+    const uint32_t need = tstate[b * 4 + 1];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int bin = (int)nb - 1 - (2 * tid + k);
+        if (bin >= 0 && above < need && above + c[k] >= need) {
+            s_d = (uint32_t)bin;
+            s_need = need - above;
+        }
+        above += c[k];
+    }
+    __syncthreads();
+    for (int i = tid; i < kTkBins; i += 1024) hb[i] = 0u;
+    if (tid == 0) {
+        tstate[b * 4] |= s_d << tk_shift(level);
+        tstate[b * 4 + 1] = s_need;
+    }
+}
+
+// per CTA: keys above / equal to the threshold T = tstate[b].prefix
+__global__ void __launch_bounds__(kTkThreads) topk_count_kernel(const float* __restrict__ alpha, int Lc,
+                                                               const uint32_t* __restrict__ tstate,
+                                                               uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t ws32[32];
+    const int b = blockIdx.y;
+    const uint32_t T = tstate[b * 4];
+    const float* a = alpha + (size_t)b * Lc;
+    const int j0 = blockIdx.x * kTkChunk, j1 = min(Lc, j0 + kTkChunk);
+    uint32_t v = 0;
+#pragma unroll 4
+    for (int j = j0 + threadIdx.x; j < j1; j += kTkThreads) {
+        const uint32_t k = ordered_key(a[j]);
+        v += k > T ? (1u << 16) : (k == T ? 1u : 0u);  // (gt << 16) | eq, both <= kTkChunk
+    }
+    uint32_t tot;
+    block_incl_sum<uint32_t>(v, ws32, &tot);
+    if (threadIdx.x == 0) cnt[(size_t)b * gridDim.x + blockIdx.x] = tot;
+}
+
+// ordered keep writes: the CTA's first output slot and equal-key rank from the counts of the CTAs before
+__global__ void __launch_bounds__(kTkThreads) topk_write_kernel(const float* __restrict__ alpha, int Lc, int m,
+                                                               const uint32_t* __restrict__ tstate,
+                                                               const uint32_t* __restrict__ cnt,
+                                                               int32_t* __restrict__ keep) {
+    __shared__ uint32_t ws32[32];
+    __shared__ uint32_t s_gt, s_eq;
+    const int b = blockIdx.y, tid = threadIdx.x;
+    const uint32_t T = tstate[b * 4], need = tstate[b * 4 + 1];
+    if (tid < 32) {  // counts of the CTAs before this one
+        uint32_t g = 0, e = 0;
+        for (int x = tid; x < (int)blockIdx.x; x += 32) {
+            const uint32_t c = cnt[(size_t)b * gridDim.x + x];
+            g += c >> 16;
+            e += c & 0xffffu;
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+            e += __shfl_xor_sync(0xffffffffu, e, o);
+        }
+        if (tid == 0) {
+            s_gt = g;
+            s_eq = e;
+        }
+    }
+    __syncthreads();
+    const float* a = alpha + (size_t)b * Lc;
+    int32_t* kp = keep + (size_t)b * m;
+    // thread t owns the contiguous elements [j0 + 8t, j0 + 8t + 8)
+    const int j0 = blockIdx.x * kTkChunk + tid * (kTkChunk / kTkThreads);
+    uint32_t k8[kTkChunk / kTkThreads];
+    uint32_t eq = 0;
+#pragma unroll
+    for (int u = 0; u < kTkChunk / kTkThreads; ++u) {
+        const int j = j0 + u;
+        k8[u] = j < Lc ? ordered_key(a[j]) : 0u;
+        eq += (j < Lc && k8[u] == T) ? 1u : 0u;
+    }
+    uint32_t tot;
+    uint32_t e = s_eq + block_incl_sum<uint32_t>(eq, ws32, &tot) - eq;  // equal keys before this thread's
+    uint32_t mine = 0;
+    {
+        uint32_t ee = e;
+#pragma unroll
+        for (int u = 0; u < kTkChunk / kTkThreads; ++u) {
+            const int j = j0 + u;
+            if (j < Lc && (k8[u] > T || (k8[u] == T && ee++ < need))) ++mine;
+        }
+    }
+    // kept before this CTA = its gt count + min(its equal count, need)
+    uint32_t pos = s_gt + min(s_eq, need) + block_incl_sum<uint32_t>(mine, ws32, &tot) - mine;
+#pragma unroll
+    for (int u = 0; u < kTkChunk / kTkThreads; ++u) {
+        const int j = j0 + u;
+        if (j < Lc && (k8[u] > T || (k8[u] == T && e++ < need))) kp[pos++] = j;
+    }
+}
+
+
 // One CTA per sequence.  Keys: ordered(alpha) (NaN ranks last, reading A14's rule); the m-th largest
 // key T by a 4-pass 8-bit radix select; kept = key > T, or key == T among the first (m - #greater)
 // in index order (ties -> lowest index, A21).  Then the retained buckets: kept token i lies in
@@ -322,122 +475,16 @@ alpha_colsum_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 constexpr int kTopThreads = 1024;
 constexpr int kTopWarps = kTopThreads / 32;
 
-__global__ void __launch_bounds__(kTopThreads) retain_topk_kernel(const float* __restrict__ alpha, int Lc, int m,
-                                                                 const int32_t* __restrict__ off, int off_stride,
-                                                                 const int32_t* __restrict__ S, int32_t* __restrict__ keep,
-                                                                 int32_t* __restrict__ roff, int32_t* __restrict__ rsid,
-                                                                 int32_t* __restrict__ rS, int off_cap) {
-    __shared__ uint32_t hist[256];
-    __shared__ uint32_t ws32[32];
-    __shared__ uint32_t s_need, s_digit;
-    __shared__ uint32_t wgt[kTopWarps], weq[kTopWarps];
+__global__ void __launch_bounds__(kTopThreads) retain_buckets_kernel(int m, const int32_t* __restrict__ off,
+                                                                     int off_stride, const int32_t* __restrict__ S,
+                                                                     const int32_t* __restrict__ keep,
+                                                                     int32_t* __restrict__ roff,
+                                                                     int32_t* __restrict__ rsid,
+                                                                     int32_t* __restrict__ rS, int off_cap) {
+    __shared__ uint32_t wgt[kTopWarps];
     __shared__ int32_t s_last[kTopWarps];
     const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const float* a = alpha + (size_t)b * Lc;
-    int32_t* kp = keep + (size_t)b * m;
-    const int C = (Lc + kTopWarps - 1) / kTopWarps;  // elements per warp
-    const int w0 = min(Lc, warp * C), w1 = min(Lc, w0 + C);
-    uint32_t prefix = 0, need = (uint32_t)m;  // keys >= T must number m
-    for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
-        const uint32_t hmask = pass == 0 ? 0u : (0xffffffffu << (shift + 8));
-        for (int i = tid; i < 256; i += kTopThreads) hist[i] = 0u;
-        __syncthreads();
-        for (int j0 = w0; j0 < w1; j0 += 32 * 8) {
-            uint32_t k[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = j0 + u * 32 + lane;
-                k[u] = j < w1 ? ordered_key(a[j]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (j0 + u * 32 + lane < w1 && (k[u] & hmask) == prefix) atomicAdd(&hist[(k[u] >> shift) & 255u], 1u);
-        }
-        __syncthreads();
-        if (tid < 32) {
-            // digit d with (count above d) < need <= (count above d) + hist[d], scanning from 255 down
-            uint32_t cnt[8], tot = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                cnt[i] = hist[255 - (tid * 8 + i)];
-                tot += cnt[i];
-            }
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += n;
-            }
-            uint32_t above = incl - tot;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (above < need && above + cnt[i] >= need) {
-                    s_digit = 255u - (uint32_t)(tid * 8 + i);
-                    s_need = need - above;
-                }
-                above += cnt[i];
-            }
-        }
-        __syncthreads();
-        prefix |= s_digit << shift;
-        need = s_need;
-        __syncthreads();
-    }
-    const uint32_t T = prefix;  // the m-th largest key; `need` of the keys equal to T are kept
-    // counts per warp, then each warp's first output position in closed form
-    {
-        uint32_t gt = 0, eq = 0;
-        for (int j0 = w0; j0 < w1; j0 += 32 * 8) {
-            uint32_t k[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = j0 + u * 32 + lane;
-                k[u] = j < w1 ? ordered_key(a[j]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const bool in = j0 + u * 32 + lane < w1;
-                gt += __popc(__ballot_sync(0xffffffffu, in && k[u] > T));
-                eq += __popc(__ballot_sync(0xffffffffu, in && k[u] == T));
-            }
-        }
-        if (lane == 0) {
-            wgt[warp] = gt;
-            weq[warp] = eq;
-        }
-    }
-    __syncthreads();
-    uint32_t gt_before = 0, eq_before = 0;
-    for (int w = 0; w < warp; ++w) {
-        gt_before += wgt[w];
-        eq_before += weq[w];
-    }
-    uint32_t pos = gt_before + min(eq_before, need);
-    {
-        const unsigned lt = (1u << lane) - 1u;
-        uint32_t e = eq_before;
-        for (int j00 = w0; j00 < w1; j00 += 32 * 8) {
-            uint32_t kk[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = j00 + u * 32 + lane;
-                kk[u] = j < w1 ? ordered_key(a[j]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = j00 + u * 32 + lane;
-                const uint32_t k = kk[u];
-                const unsigned em = __ballot_sync(0xffffffffu, j < w1 && k == T);
-                const bool kept = j < w1 && (k > T || (k == T && e + __popc(em & lt) < need));
-                const unsigned km = __ballot_sync(0xffffffffu, kept);
-                if (kept) kp[pos + __popc(km & lt)] = j;
-                pos += __popc(km);
-                e += __popc(em);
-            }
-        }
-    }
-    __syncthreads();
+    const int32_t* kp = keep + (size_t)b * m;
     // buckets: sentence of every kept token (binary search in the prompt offsets), starts where it changes
     const int Sb = S[b];
     const int32_t* o = off + (size_t)b * off_stride;
@@ -571,7 +618,8 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims
 size_t retain_scratch_floats(int B, int G, int L, int N, int grp) {
     const int R = N * grp, nrb = (R + 127) / 128;
     const int nchunk = (L + kKT - 1) / kKT;  // upper bound (chunk_tiles >= 1)
-    return (size_t)B * G * nrb * nchunk * 128 * 2 + (size_t)B * G * R * 2;
+    const size_t topk = 4 * (size_t)B + (size_t)B * kTkBins + (size_t)B * ((L + kTkChunk - 1) / kTkChunk);
+    return (size_t)B * G * nrb * nchunk * 128 * 2 + (size_t)B * G * R * 2 + topk;
 }
 
 bool retain_supported(int d, int N, int grp) {
@@ -639,11 +687,30 @@ cudaError_t launch_retain(const RetainArgs& a, cudaStream_t st) {
                                                                           tiles_per_cta, qhalf, scale_log2, stats, a.alpha);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    // the prompt's sentence offsets go to shared memory when they fit in 96 KB
+    // top-m: 3 radix levels over all CTAs, then counts, then the ordered keep writes
+    {
+        const int nblk = (Lc + kTkChunk - 1) / kTkChunk;
+        uint32_t* ts = reinterpret_cast<uint32_t*>(stats + (size_t)a.B * a.G * R);  // [B][4]
+        uint32_t* th = ts + 4 * a.B;                                                // [B][kTkBins]
+        uint32_t* tc = th + (size_t)a.B * kTkBins;                                  // [B][nblk]
+        std::vector<uint32_t> init(4 * a.B, 0u);
+        for (int b = 0; b < a.B; ++b) init[4 * b + 1] = (uint32_t)a.m;
+        if ((e = cudaMemcpyAsync(ts, init.data(), sizeof(uint32_t) * 4 * a.B, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+            return e;
+        if ((e = cudaMemsetAsync(th, 0, sizeof(uint32_t) * a.B * kTkBins, st)) != cudaSuccess) return e;
+        for (int level = 0; level < 3; ++level) {
+            topk_hist_kernel<<<dim3(nblk, a.B), kTkThreads, 0, st>>>(a.alpha, Lc, level, ts, th);
+            topk_digit_kernel<<<a.B, 1024, 0, st>>>(level, ts, th);
+        }
+        topk_count_kernel<<<dim3(nblk, a.B), kTkThreads, 0, st>>>(a.alpha, Lc, ts, tc);
+        topk_write_kernel<<<dim3(nblk, a.B), kTkThreads, 0, st>>>(a.alpha, Lc, a.m, ts, tc, a.keep);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    // buckets (the prompt's sentence offsets in shared memory when they fit in 96 KB)
     const int off_cap = std::min(a.off_stride, 96 * 1024 / 4);
-    if ((e = ensure_smem((const void*)retain_topk_kernel, (size_t)off_cap * 4)) != cudaSuccess) return e;
-    retain_topk_kernel<<<a.B, kTopThreads, (size_t)off_cap * 4, st>>>(a.alpha, Lc, a.m, a.off, a.off_stride, a.S, a.keep,
-                                                                     a.roff, a.rsid, a.rS, off_cap);
+    if ((e = ensure_smem((const void*)retain_buckets_kernel, (size_t)off_cap * 4)) != cudaSuccess) return e;
+    retain_buckets_kernel<<<a.B, kTopThreads, (size_t)off_cap * 4, st>>>(a.m, a.off, a.off_stride, a.S, a.keep, a.roff,
+                                                                        a.rsid, a.rS, off_cap);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int blocks = std::max(1, std::min(64, (a.m * a.d / 8 + 255) / 256));
     retain_gather_kernel<<<dim3(blocks, a.G, a.B), 256, 0, st>>>(a.K, a.V, a.G, a.L, a.d, a.m, a.keep, a.PK, a.PV);
