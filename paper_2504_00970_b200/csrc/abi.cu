@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <new>
 
@@ -280,6 +281,7 @@ SKV_API skv_status sentencekv_destroy(skv_ctx* c) {
     dfree(c->unit_cand);
     dfree(c->ret_scratch);
     dfree(c->cap_dev);
+    dfree(c->seg_scratch);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -452,7 +454,11 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             c->off_stride = L + 1;
         }
         if (boundary_ids && n_boundary > 0) {
-            SKV_CUDA(c, cudaMemcpyAsync(c->bset, boundary_ids, sizeof(int32_t) * n_boundary, cudaMemcpyHostToDevice, st));
+            // sorted (the segmentation kernels test membership by binary search); pageable source: the
+            // copy is staged before the call returns
+            std::vector<int32_t> sorted(boundary_ids, boundary_ids + n_boundary);
+            std::sort(sorted.begin(), sorted.end());
+            SKV_CUDA(c, cudaMemcpyAsync(c->bset, sorted.data(), sizeof(int32_t) * n_boundary, cudaMemcpyHostToDevice, st));
             c->n_bset = n_boundary;
         } else {  // Quest without a boundary set: no input token resets Q_s (Quest does not use it)
             c->n_bset = 0;
@@ -462,16 +468,23 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             SKV_CUDA(c, skv::launch_chunks(c->B, L, c->tau, c->cfg.chunk_size, c->off, c->off_stride, c->S_dev, st));
             c->launches += 1;
         } else {
+            const size_t need = skv::segment_scratch_ints(c->B, L);
+            if (c->seg_scratch_n < need) {
+                dfree(c->seg_scratch);
+                c->seg_scratch_n = 0;
+                SKV_CUDA(c, dalloc(&c->seg_scratch, need));
+                c->seg_scratch_n = need;
+            }
             SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off, c->off_stride,
-                                            c->S_dev, nullptr, st));
-            c->launches += 1;
+                                            c->S_dev, nullptr, c->seg_scratch, st));
+            c->launches += 3;
             if (c->cfg.outlier_n > 0.0f) {  // NEXT-3 outlier split: re-segment under the per-prompt cap T
                 if (!c->cap_dev) SKV_CUDA(c, dalloc(&c->cap_dev, (size_t)c->B));
                 SKV_CUDA(c, skv::launch_outlier_cap(c->off, c->off_stride, c->S_dev, c->B, (double)c->cfg.outlier_n,
                                                     c->cap_dev, st));
                 SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off,
-                                                c->off_stride, c->S_dev, c->cap_dev, st));
-                c->launches += 2;
+                                                c->off_stride, c->S_dev, c->cap_dev, c->seg_scratch, st));
+                c->launches += 4;
             } else if (c->cfg.bucket_mode == SKV_BUCKETS_EQUAL) {  // NEXT-3 equal chunks, as many as sentences
                 SKV_CUDA(c, skv::launch_chunks(c->B, L, c->tau, 0, c->off, c->off_stride, c->S_dev, st));
                 c->launches += 1;
@@ -535,6 +548,7 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         if (c->ret_scratch_n < need) {
             dfree(c->ret_scratch);
     dfree(c->cap_dev);
+    dfree(c->seg_scratch);
             c->ret_scratch_n = 0;
             SKV_CUDA(c, dalloc(&c->ret_scratch, need));
             c->ret_scratch_n = need;

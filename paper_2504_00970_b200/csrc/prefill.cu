@@ -8,59 +8,159 @@
 
 namespace skv {
 
-// One CTA per prompt.  Each thread owns a contiguous run of tokens.  Sentence ends are the
-// boundary tokens (A1, A2), the last token (A4), and every tau-th token of a boundary-free run
-// (A5 tau-cap).  Pass 1 finds the last boundary before each thread's run (block max-scan), pass
-// 2 counts ends (block sum-scan -> sentence index base), pass 3 writes off[s+1] = end + 1.
-__global__ void __launch_bounds__(1024) segment_kernel(const int32_t* __restrict__ tokens, int L,
-                                                       const int32_t* __restrict__ bset, int nb, int tau,
-                                                       int32_t* __restrict__ off, int off_stride,
-                                                       int32_t* __restrict__ S_out, const int32_t* __restrict__ cap_b) {
+// P1 segmentation, multi-CTA (r02; the r01 kernel used one CTA per prompt and ran at 6.6 GB/s,
+// 0.32 ms for 4 x 131072 tokens).  Chunks of kSegChunk tokens, one CTA each, thread = 8 consecutive tokens;
+// the boundary set is sorted on the host, membership by binary search.  Same rules and output as
+// segment_kernel: a sentence ends at a boundary token, at L-1, or every tau-th token of a
+// boundary-free run (the tau-cap counts from the last boundary, so only the last boundary before
+// each token is carried across chunks):
+//   seg_lastb_kernel: last boundary of every chunk;
+//   seg_count_kernel: ends per chunk (last boundary before the chunk = max over the chunks before);
+//   seg_write_kernel: offsets (base = ends of the chunks before + a block scan).
+constexpr int kSegThreads = 256, kSegPer = 8, kSegChunk = kSegThreads * kSegPer;
+
+__device__ __forceinline__ bool in_sorted(int32_t tok, const int32_t* set, int n) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (set[mid] < tok) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && set[lo] == tok;
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_lastb_kernel(const int32_t* __restrict__ tokens, int L,
+                                                               const int32_t* __restrict__ bset, int nb,
+                                                               int32_t* __restrict__ lastb) {
     __shared__ int32_t sb[kMaxBoundary];
-    __shared__ int32_t ws[32];
-    const int b = blockIdx.x;
-    // NEXT-3 outlier split: a per-prompt cap T below tau (reading A27); else the tau-cap (A5)
-    if (cap_b) tau = min(tau, max(1, cap_b[b]));
-    const int32_t* tok = tokens + (size_t)b * L;
-    int32_t* o = off + (size_t)b * off_stride;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) sb[i] = bset[i];
+    __shared__ int ws[32];
+    const int b = blockIdx.y, c = blockIdx.x;
+    for (int i = threadIdx.x; i < nb; i += kSegThreads) sb[i] = bset[i];
     __syncthreads();
-
-    const int per = (L + blockDim.x - 1) / blockDim.x;
-    const int lo = min(L, (int)threadIdx.x * per), hi = min(L, lo + per);
-
-    int lastb = -1;
-    for (int i = lo; i < hi; ++i)
-        if (in_set(tok[i], sb, nb)) lastb = i;
-    const int before = block_excl_max(lastb, -1, ws);
-
-    int last = before, nend = 0;
-    for (int i = lo; i < hi; ++i) {
-        const bool bnd = in_set(tok[i], sb, nb);
-        nend += (bnd || i == L - 1 || (i - last) % tau == 0) ? 1 : 0;
-        if (bnd) last = i;
-    }
-    int total;
-    const int base = block_incl_sum(nend, ws, &total) - nend;
-
-    last = before;
-    int k = base;
-    for (int i = lo; i < hi; ++i) {
-        const bool bnd = in_set(tok[i], sb, nb);
-        if (bnd || i == L - 1 || (i - last) % tau == 0) o[++k] = i + 1;
-        if (bnd) last = i;
-    }
+    const int32_t* tok = tokens + (size_t)b * L;
+    int lb = -1;
+    for (int i = c * kSegChunk + threadIdx.x; i < min(L, (c + 1) * kSegChunk); i += kSegThreads)
+        if (in_sorted(tok[i], sb, nb)) lb = max(lb, i);
+    lb = __reduce_max_sync(0xffffffffu, lb);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = lb;
+    __syncthreads();
     if (threadIdx.x == 0) {
+        int m = -1;
+        for (int w = 0; w < kSegThreads / 32; ++w) m = max(m, ws[w]);
+        lastb[(size_t)b * gridDim.x + c] = m;
+    }
+}
+
+// per thread: its 8 tokens' boundary flags and the last boundary before them; returns the ends
+template <bool WRITE>
+__device__ __forceinline__ int seg_chunk(const int32_t* tok, int L, const int32_t* sb, int nb, int tau, int c,
+                                         int lastb_in, int* ws, int32_t* o, int base) {
+    const int i0 = c * kSegChunk + threadIdx.x * kSegPer;
+    bool bnd[kSegPer];
+    int lb = -1;
+#pragma unroll
+    for (int u = 0; u < kSegPer; ++u) {
+        const int i = i0 + u;
+        bnd[u] = i < L && in_sorted(tok[i], sb, nb);
+        if (bnd[u]) lb = i;
+    }
+    int before = block_excl_max(lb, -1, ws);
+    before = max(before, lastb_in);
+    int last = before, n = 0;
+#pragma unroll
+    for (int u = 0; u < kSegPer; ++u) {
+        const int i = i0 + u;
+        if (i < L && (bnd[u] || i == L - 1 || (i - last) % tau == 0)) ++n;
+        if (bnd[u]) last = i;
+    }
+    if constexpr (WRITE) {
+        int total;
+        int k = base + block_incl_sum(n, ws, &total) - n;
+        last = before;
+#pragma unroll
+        for (int u = 0; u < kSegPer; ++u) {
+            const int i = i0 + u;
+            if (i < L && (bnd[u] || i == L - 1 || (i - last) % tau == 0)) o[++k] = i + 1;
+            if (bnd[u]) last = i;
+        }
+        return total;
+    } else {
+        int total;
+        block_incl_sum(n, ws, &total);
+        return total;
+    }
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_count_kernel(const int32_t* __restrict__ tokens, int L,
+                                                               const int32_t* __restrict__ bset, int nb, int tau,
+                                                               const int32_t* __restrict__ cap_b,
+                                                               const int32_t* __restrict__ lastb,
+                                                               int32_t* __restrict__ ends) {
+    __shared__ int32_t sb[kMaxBoundary];
+    __shared__ int ws[32];
+    __shared__ int s_in;
+    const int b = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+    if (cap_b) tau = min(tau, max(1, cap_b[b]));
+    for (int i = threadIdx.x; i < nb; i += kSegThreads) sb[i] = bset[i];
+    if (threadIdx.x < 32) {
+        int m = -1;
+        for (int x = threadIdx.x; x < c; x += 32) m = max(m, lastb[(size_t)b * nch + x]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (threadIdx.x == 0) s_in = m;
+    }
+    __syncthreads();
+    const int total = seg_chunk<false>(tokens + (size_t)b * L, L, sb, nb, tau, c, s_in, ws, nullptr, 0);
+    if (threadIdx.x == 0) ends[(size_t)b * nch + c] = total;
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_write_kernel(const int32_t* __restrict__ tokens, int L,
+                                                               const int32_t* __restrict__ bset, int nb, int tau,
+                                                               const int32_t* __restrict__ cap_b,
+                                                               const int32_t* __restrict__ lastb,
+                                                               const int32_t* __restrict__ ends,
+                                                               int32_t* __restrict__ off, int off_stride,
+                                                               int32_t* __restrict__ S_out) {
+    __shared__ int32_t sb[kMaxBoundary];
+    __shared__ int ws[32];
+    __shared__ int s_in, s_base;
+    const int b = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+    if (cap_b) tau = min(tau, max(1, cap_b[b]));
+    for (int i = threadIdx.x; i < nb; i += kSegThreads) sb[i] = bset[i];
+    if (threadIdx.x < 32) {
+        int m = -1, e = 0;
+        for (int x = threadIdx.x; x < c; x += 32) {
+            m = max(m, lastb[(size_t)b * nch + x]);
+            e += ends[(size_t)b * nch + x];
+        }
+        m = __reduce_max_sync(0xffffffffu, m);
+        e = __reduce_add_sync(0xffffffffu, e);
+        if (threadIdx.x == 0) {
+            s_in = m;
+            s_base = e;
+        }
+    }
+    __syncthreads();
+    int32_t* o = off + (size_t)b * off_stride;
+    const int total = seg_chunk<true>(tokens + (size_t)b * L, L, sb, nb, tau, c, s_in, ws, o, s_base);
+    if (threadIdx.x == 0 && c == nch - 1) {
         o[0] = 0;
-        S_out[b] = total;
+        S_out[b] = s_base + total;
     }
 }
 
 cudaError_t launch_segment(const int32_t* tokens, int B, int L, const int32_t* bset, int nb, int tau,
-                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, cudaStream_t st) {
-    segment_kernel<<<B, 1024, 0, st>>>(tokens, L, bset, nb, tau, off, off_stride, S, cap_b);
+                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, int32_t* scratch,
+                           cudaStream_t st) {
+    const int nch = (L + kSegChunk - 1) / kSegChunk;
+    int32_t* lastb = scratch;             // [B][nch]
+    int32_t* ends = scratch + (size_t)B * nch;  // [B][nch]
+    seg_lastb_kernel<<<dim3(nch, B), kSegThreads, 0, st>>>(tokens, L, bset, nb, lastb);
+    seg_count_kernel<<<dim3(nch, B), kSegThreads, 0, st>>>(tokens, L, bset, nb, tau, cap_b, lastb, ends);
+    seg_write_kernel<<<dim3(nch, B), kSegThreads, 0, st>>>(tokens, L, bset, nb, tau, cap_b, lastb, ends, off,
+                                                          off_stride, S);
     return cudaGetLastError();
 }
+
+size_t segment_scratch_ints(int B, int L) { return 2 * (size_t)B * ((L + kSegChunk - 1) / kSegChunk); }
 
 // One thread per (sentence, 8 dims): D/8 threads cover a sentence's key row (one 16-byte load
 // per token), so a warp streams 2 (D=128) or 4 (D=64) sentences' contiguous K runs.  The sum is

@@ -137,6 +137,8 @@ struct skv_ctx {
     std::vector<skv::LayerState> layer;
     int4* unit_cand = nullptr;         // overflow scratch of the per-unit step kernel's candidate lists
     int32_t* cap_dev = nullptr;        // NEXT-3 outlier split: per-prompt length cap [B]
+    int32_t* seg_scratch = nullptr;    // P1: per-chunk last boundary and ends
+    size_t seg_scratch_n = 0;
     float* ret_scratch = nullptr;      // NEXT-1 pass A partials + row stats
     size_t ret_scratch_n = 0;
 
@@ -176,7 +178,9 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 bl
 // P1: sentence offsets for B prompts.  tokens [B][L]; off [B][Smax_cap+1]; S [B]; cap_b [B] or
 // nullptr: a per-prompt length cap below tau (NEXT-3 outlier split).
 cudaError_t launch_segment(const int32_t* tokens, int B, int L, const int32_t* bset, int nb, int tau,
-                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, cudaStream_t st);
+                           int32_t* off, int off_stride, int32_t* S, const int32_t* cap_b, int32_t* scratch,
+                           cudaStream_t st);
+size_t segment_scratch_ints(int B, int L);  // scratch of launch_segment; bset must be sorted ascending
 
 // ---- NEXT-3 / NEXT-4 bucket and ranking variants (variants.cu) ----
 // outlier split threshold T = floor((L + n * sqrt(S * sum len^2 - L^2)) / S) per prompt (reading A27)
