@@ -463,23 +463,23 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         } else {  // Quest without a boundary set: no input token resets Q_s (Quest does not use it)
             c->n_bset = 0;
         }
+        const size_t need = skv::segment_scratch_ints(c->B, L);
+        if (c->seg_scratch_n < need) {  // (allocated outside the profiled region)
+            dfree(c->seg_scratch);
+            c->seg_scratch_n = 0;
+            SKV_CUDA(c, dalloc(&c->seg_scratch, need));
+            c->seg_scratch_n = need;
+        }
+        if (c->cfg.outlier_n > 0.0f && !c->cap_dev) SKV_CUDA(c, dalloc(&c->cap_dev, (size_t)c->B));
         cudaEvent_t pa = prof_begin(c, st);
         if (quest) {  // NEXT-4: fixed pages of chunk_size tokens
             SKV_CUDA(c, skv::launch_chunks(c->B, L, c->tau, c->cfg.chunk_size, c->off, c->off_stride, c->S_dev, st));
             c->launches += 1;
         } else {
-            const size_t need = skv::segment_scratch_ints(c->B, L);
-            if (c->seg_scratch_n < need) {
-                dfree(c->seg_scratch);
-                c->seg_scratch_n = 0;
-                SKV_CUDA(c, dalloc(&c->seg_scratch, need));
-                c->seg_scratch_n = need;
-            }
             SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off, c->off_stride,
                                             c->S_dev, nullptr, c->seg_scratch, st));
             c->launches += 3;
             if (c->cfg.outlier_n > 0.0f) {  // NEXT-3 outlier split: re-segment under the per-prompt cap T
-                if (!c->cap_dev) SKV_CUDA(c, dalloc(&c->cap_dev, (size_t)c->B));
                 SKV_CUDA(c, skv::launch_outlier_cap(c->off, c->off_stride, c->S_dev, c->B, (double)c->cfg.outlier_n,
                                                     c->cap_dev, st));
                 SKV_CUDA(c, skv::launch_segment(token_ids, c->B, L, c->bset, n_boundary, c->tau, c->off,
