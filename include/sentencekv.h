@@ -172,8 +172,9 @@ skv_status sentencekv_sync(skv_ctx* ctx);
  *                   reading A25); Eq. 1 runs over the retained tokens only;
  *                 the retained K/V form a ctx-owned pool in HBM ([B][G][m][d], token order) that every
  *                 decode call of the layer ranks and attends (the HBM working set of floor(r*tau)
- *                 tokens holds all of it), and K/V are not borrowed: the caller may free them after
- *                 sentencekv_sync.  SKV_KV_HOST: P3 offloads the pool, not the full K/V (Alg. 1 l.7,
+ *                 tokens holds all of it); the N window tokens' K/V are kept too and attended by every
+ *                 decode step besides the selection, uncharged (reading A25); K/V are not borrowed:
+ *                 the caller may free them after sentencekv_sync.  SKV_KV_HOST: P3 offloads the pool, not the full K/V (Alg. 1 l.7,
  *                 P:580 "Offload a small subset (r*tau) of tokens to CPU").
  *               Decode outputs (sel_ids) stay the prompt's sentence ids; sel_tokens count retained
  *               tokens.  Introspection: sentencekv_copy_importance / sentencekv_copy_retained.

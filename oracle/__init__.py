@@ -322,7 +322,7 @@ class Oracle:
         self.V = {}
         # NEXT-1 retention (obs_window > 0): per layer, per b: alpha, retained token ids, bucket
         # offsets over the pool and the sentence id of each bucket; K/V above are then the pools
-        self.alpha, self.keep, self.loff, self.sid = {}, {}, {}, {}
+        self.alpha, self.keep, self.loff, self.sid, self.win = {}, {}, {}, {}, {}
         # NEXT-2 local segment and growth (max_generated > 0; reading A29): per layer, per b: the
         # generated tokens' K/V, the start of the current (unfinished) generated sentence, whether the
         # sentence ended at the last appended token, and the bucket offsets extended by the completed
@@ -392,6 +392,10 @@ class Oracle:
             Kp.append(np.ascontiguousarray(K_bits[b][:, keep]))
             Vp.append(np.ascontiguousarray(V_bits[b][:, keep]))
         self.alpha[layer], self.keep[layer], self.loff[layer], self.sid[layer] = al, kp, lo, sd
+        # the observation window itself (positions >= L - N): not a candidate, attended every step (A25)
+        L = K_bits.shape[2]
+        self.win[layer] = [(np.ascontiguousarray(K_bits[b][:, L - self.N:]), np.ascontiguousarray(V_bits[b][:, L - self.N:]))
+                           for b in range(self.B)]
         self.K[layer], self.V[layer] = Kp, Vp  # [b] -> [G][m][d]
         self.E[layer] = [[embed(Kp[b][g], lo[b]) for g in range(self.G)] for b in range(self.B)]
 
@@ -430,12 +434,19 @@ class Oracle:
     def decode_attend(self, layer: int, q_bits, ids):
         """Alg. 1 line 19 / Eq. 3 over the selection of this layer: O fp64 [B][Hq][d].  NEXT-2: the
         selected buckets (prompt rows, then generated rows) plus the local segment -- the tokens of the
-        unfinished generated sentence, attended uncharged (reading A29)."""
+        unfinished generated sentence, attended uncharged (reading A29).  NEXT-1: the selected buckets
+        of the retained pool plus the observation window (reading A25)."""
         O = np.zeros((self.B, self.Hq, self.d), dtype=np.float64)
         for b in range(self.B):
             for g in range(self.G):
                 h0 = g * self.grp
                 K, V, off, sel = self.K[layer][b][g], self.V[layer][b][g], self.offsets(layer, b), list(ids[b][g])
+                if layer in self.win:  # NEXT-1: the observation window, attended every step (A25)
+                    wk, wv = self.win[layer][b]
+                    K = np.concatenate([K, wk[g]])
+                    V = np.concatenate([V, wv[g]])
+                    off = np.append(off, np.int32(K.shape[0]))
+                    sel = sel + [len(off) - 2]
                 if layer in self.gK:
                     n = self.gK[layer][b].shape[1]
                     K = np.concatenate([K, self.gK[layer][b][g]])

@@ -103,6 +103,9 @@ void free_layer_prompt(skv::LayerState& ls) {
 }
 
 void free_retention(skv::LayerState& ls) {
+    dfree(ls.winK);
+    dfree(ls.winV);
+    dfree(ls.wstat);
     dfree(ls.PK);
     dfree(ls.PV);
     dfree(ls.alpha);
@@ -337,11 +340,14 @@ struct LayerView {
     skv::GenSrc gen;       // NEXT-2 generated rows + local segment (gen.Kg == nullptr: off)
 };
 static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
-    const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0x7fffffff};  // no generated rows
-    if (ls.retained) return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false, none};
+    const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0x7fffffff, 0, 0};  // no generated rows
+    if (ls.retained)  // the pool; rows >= m are the observation window's, always attended (A25)
+        return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false,
+                skv::GenSrc{ls.winK, ls.winV, ls.wstat, c->cfg.obs_window, ls.ret_m, c->cfg.obs_window,
+                            c->cfg.obs_window}};
     if (ls.genK)
         return {ls.goff, c->Smax + 1, ls.gS, ls.K, ls.V, c->L, nullptr, 0, false,
-                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated, c->L}};
+                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated, c->L, 0, c->tau}};
     return {c->off, c->off_stride, c->S_dev, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST, none};
 }
 
@@ -542,6 +548,14 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
             SKV_CUDA(c, dalloc(&ls.roff, (size_t)c->B * (m + 1)));
             SKV_CUDA(c, dalloc(&ls.rsid, (size_t)c->B * m));
             SKV_CUDA(c, dalloc(&ls.rS, (size_t)c->B));
+            SKV_CUDA(c, dalloc(&ls.winK, U * N * c->d));
+            SKV_CUDA(c, dalloc(&ls.winV, U * N * c->d));
+            SKV_CUDA(c, dalloc(&ls.wstat, (size_t)c->B * 4));
+            {
+                std::vector<int32_t> ws(4 * c->B, 0);
+                for (int b = 0; b < c->B; ++b) ws[4 * b] = ws[4 * b + 1] = N;
+                SKV_CUDA(c, cudaMemcpy(ls.wstat, ws.data(), sizeof(int32_t) * 4 * c->B, cudaMemcpyHostToDevice));
+            }
             ls.ret_bytes = key;
         }
         const size_t need = skv::retain_scratch_floats(c->B, c->G, L, N, c->grp);
@@ -556,6 +570,13 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         skv::RetainArgs ra{static_cast<const __nv_bfloat16*>(q_window), Kb, Vb, c->B, c->G, c->grp, c->d, L, N, m,
                            c->off, c->off_stride, c->S_dev, ls.alpha, c->ret_scratch, ls.keep, ls.roff, ls.rsid, ls.rS,
                            ls.PK, ls.PV};
+        // the observation window's K/V rows [L-N, L): attended by every decode step (reading A25)
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.winK, sizeof(__nv_bfloat16) * N * c->d, Kb + (size_t)(L - N) * c->d,
+                                      sizeof(__nv_bfloat16) * L * c->d, sizeof(__nv_bfloat16) * N * c->d,
+                                      (size_t)c->B * c->G, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.winV, sizeof(__nv_bfloat16) * N * c->d, Vb + (size_t)(L - N) * c->d,
+                                      sizeof(__nv_bfloat16) * L * c->d, sizeof(__nv_bfloat16) * N * c->d,
+                                      (size_t)c->B * c->G, cudaMemcpyDeviceToDevice, st));
         cudaEvent_t pr = prof_begin(c, st);
         SKV_CUDA(c, skv::launch_retain(ra, st));
         prof_end(c, SKV_K_RETAIN, pr, st);
@@ -684,7 +705,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
     const bool host = v.host;
     const bool unit_path = c->cfg.bucket_mode != SKV_BUCKETS_QUEST && c->cfg.fill_mode == SKV_FILL_PREFIX;
     if (unit_path && skv::unit_supported(c->d, c->grp, c->Smax, c->tau, host ? cache_slots(c) : 0,
-                                         host ? ls.pc_pages : 0, v.gen.Kg != nullptr)) {
+                                         host ? ls.pc_pages : 0, v.gen.Kg ? v.gen.max_att : 0)) {
         // default: one launch per layer, one thread-block cluster per (b, g) unit (decode_unit.cu)
         skv::UnitArgs a{};
         if (host) {
@@ -938,6 +959,14 @@ SKV_API skv_status sentencekv_host_fetch_bytes(skv_ctx* c, int32_t layer, uint64
 SKV_API skv_status sentencekv_set_profiling(skv_ctx* c, int32_t on) {
     if (!c) return SKV_ERR_INVALID_ARGUMENT;
     c->profiling = on != 0;
+    if (c->profiling) {  // events created up front: creating one between two records would be timed
+        DeviceGuard dg(c->cfg.device);
+        while (c->ev_pool.size() < 256) {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreate(&e) != cudaSuccess) break;
+            c->ev_pool.push_back(e);
+        }
+    }
     return SKV_OK;
 }
 

@@ -97,7 +97,7 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     int hot0 = 0, nhot = 0;
     if (gen.Kg) {
         hot0 = gen.gstat[b * 4 + 1];
-        nhot = gen.gstat[b * 4 + 0] - hot0;
+        nhot = gen.fixed + gen.gstat[b * 4 + 0] - hot0;  // the always-attended rows, then the hot sentence
     }
     const int natt = ntok + nhot;
     const int ntiles = (natt + kTile - 1) / kTile;
@@ -108,7 +108,8 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     for (int t = T0 + tid; t < te * kTile; t += kMT) {
         int r = kInvalid;
         if (t < T1 && t >= ntok) {
-            r = gen.L + hot0 + (t - ntok);
+            const int x = t - ntok;
+            r = gen.L + (x < gen.fixed ? x : hot0 + (x - gen.fixed));
         } else if (t < T1) {
             int lo = 0, hi = count - 1;  // largest i with tok[i] <= t
             while (lo < hi) {
@@ -220,7 +221,7 @@ static cudaError_t launch_mma_t(dim3 grid, cudaStream_t st, const __nv_bfloat16*
                                 float* out, GenSrc gen, OutPeers peers, float scale_log2) {
     // metadata: tok[tau+1] + srcs[tau] (+ pids[tau] + ptok[tau+1]) + rowtab[per-CTA tokens]; the
     // NEXT-2 local segment adds up to tau attended tokens
-    const size_t tiles = ((size_t)sel.tau * (gen.Kg ? 2 : 1) + kTile - 1) / kTile;
+    const size_t tiles = ((size_t)sel.tau + (gen.Kg ? gen.max_att : 0) + kTile - 1) / kTile;
     const size_t rows = ((tiles + kMCL - 1) / kMCL) * kTile;
     const size_t meta = (size_t)(2 * sel.tau + 1) + (HOST ? (size_t)(2 * sel.tau + 1) : 0) + rows;
     const size_t smem = sizeof(MmaSmem<D>) + sizeof(int32_t) * meta;

@@ -980,7 +980,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int hot0 = 0, nhot = 0;
     if (gen.Kg) {
         hot0 = gen.gstat[b * 4 + 1];
-        nhot = gen.gstat[b * 4 + 0] - hot0;
+        nhot = gen.fixed + gen.gstat[b * 4 + 0] - hot0;  // the always-attended rows, then the hot sentence
     }
     const int natt = ntok + nhot;
     const int ntl = (natt + kTile - 1) / kTile;
@@ -1132,7 +1132,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
         if (t < T1 && t >= ntok) {
-            r.x = gen.L + hot0 + (t - ntok);  // local segment (device residency only)
+            const int x = t - ntok;  // local segment (device residency only)
+            r.x = gen.L + (x < gen.fixed ? x : hot0 + (x - gen.fixed));
         } else if (t < T1) {
             int lo2 = 0, hi2 = count - 1;  // largest i with sel_tok[i] <= t
             while (lo2 < hi2) {
@@ -1344,9 +1345,9 @@ size_t unit_smem_bytes(int d, int tau, int att) {
 
 int unit_page_tokens() { return kPage; }
 
-bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, bool local) {
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, int local_att) {
     return (d == 64 || d == 128) && grp <= 8 && Smax <= kUC * kULocalCap &&
-           unit_smem_bytes(d, tau, local ? 2 * tau : tau) <= 200 * 1024 &&
+           unit_smem_bytes(d, tau, tau + local_att) <= 200 * 1024 &&
            slots <= kMaxSlots && pages <= kMaxPageWords * 32;
 }
 
@@ -1359,7 +1360,7 @@ static int trace_counter = 0;  // launch index for the trace build's per-launch 
 
 template <int D, int GRP, bool HOST>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
-    const size_t smem = unit_smem_bytes(D, a.sel.tau, a.gen.Kg ? 2 * a.sel.tau : a.sel.tau);
+    const size_t smem = unit_smem_bytes(D, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0));
     cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST>, smem);
     if (e != cudaSuccess) return e;
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);

@@ -49,11 +49,15 @@ struct QsState {
 // slot_stride = tau, rows = gathered positions).
 // NEXT-2 local segment / generated rows (Kg == nullptr: off).  Rows >= L of a layer's buckets are
 // generated rows (row - L of the store); gstat[b] = {count, start of the current sentence, pending, overflow}.
+// Also the NEXT-1 observation window (retention): its N rows are the `fixed` always-attended rows.
+// Attended beyond the selection: store rows [0, fixed) and [gstat.start, gstat.count).
 struct GenSrc {
     const __nv_bfloat16* Kg;       // [B][G][stride][d]
     const __nv_bfloat16* Vg;
     const int32_t* gstat;          // [B][4]
     int stride, L;
+    int fixed;                     // always-attended rows at the start of the store
+    int max_att;                   // upper bound of the attended rows beyond the selection (smem sizing)
 };
 
 struct KvSrc {
@@ -108,6 +112,10 @@ struct LayerState {
     int32_t* gstat = nullptr;          // [B][4]
     int32_t* goff = nullptr;           // [B][Smax+1] the prompt's offsets followed by completed generated sentences
     int32_t* gS = nullptr;             // [B] buckets
+    // NEXT-1 observation window, always attended with retention (reading A25)
+    __nv_bfloat16* winK = nullptr;     // [B][G][N][d]
+    __nv_bfloat16* winV = nullptr;
+    int32_t* wstat = nullptr;          // [B][4] = {N, N, 0, 0}: no generated sentence in progress
     // SURVEY 8(e) fused all-gather epilogue (sentencekv_set_output_peers)
     OutPeers peers{};
     unsigned int* peer_local_flag = nullptr;  // this rank's arrival counter for the layer (peer memory)
@@ -282,7 +290,7 @@ struct UnitArgs {
     GenSrc gen;                    // NEXT-2 local segment (gen.Kg == nullptr: off)
     OutPeers peers;                // 8(e) fused gather (peers.n == 0: off)
 };
-bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, bool local);
+bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, int local_att);
 int unit_page_tokens();
 size_t unit_smem_bytes(int d, int tau, int att);
 size_t unit_cand_entries(int units);

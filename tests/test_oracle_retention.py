@@ -133,13 +133,14 @@ def test_retained_buckets_worked():
 
 
 def test_driver_retention_equals_full_when_everything_is_kept():
-    """floor(r*tau) >= L - N keeps every candidate: the buckets are the prompt's sentences cut at
-    the window (E, selection and attention as over the truncated prompt)."""
-    B, M, Hq, G, d, L, tau, N = 1, 1, 4, 2, 64, 300, 160, 8
+    """floor(r*tau) >= L - N keeps every candidate: the buckets are the prompt's sentences cut at the
+    window; with a budget that fits them all, the decode attends every bucket plus the observation
+    window (A25) -- i.e. full attention over the whole prompt (fp64 SDPA, a library routine)."""
+    B, M, Hq, G, d, L, tau, N = 1, 1, 4, 2, 64, 300, 300, 8
     toks, topics = synth.prompts(5, B, L, median=20.0)
     K, V = synth.kv_layer(5, 0, topics, G, d)
     qw = synth.f32_to_bf16_bits(np.random.default_rng(1).standard_normal((B, N, Hq, d)).astype(np.float32))
-    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d, obs_window=N, semantic_factor=2.0)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d, obs_window=N, semantic_factor=1.0)
     orc.prefill_layer(0, K, V, q_window=qw)
     assert orc.keep[0][0].tolist() == list(range(L - N))
     off = orc.off[0]
@@ -147,13 +148,14 @@ def test_driver_retention_equals_full_when_everything_is_kept():
     want = np.concatenate([cut, [L - N]]) if cut[-1] != L - N else cut
     assert orc.loff[0][0].tolist() == want.tolist()
     q = synth.queries(5, 0, 0, np.zeros(B, np.int32), Hq, G, d)
-    _, ids, _ = orc.decode_select(0, q, np.array([300], np.int32))
+    _, ids, ntok = orc.decode_select(0, q, np.array([300], np.int32))
+    assert all(n == L - N for n in ntok[0])  # every retained token selected (r * tau = 300 >= L - N)
     O = orc.decode_attend(0, q, ids)
-    for g in range(G):
-        idx = np.concatenate([np.arange(orc.loff[0][0][s], orc.loff[0][0][s + 1]) for s in ids[0][g]])
-        ref = oracle.attend(q[0, g * 2:(g + 1) * 2], K[0, g, idx], V[0, g, idx],
-                            np.array([0, len(idx)], np.int32), np.array([0], np.int32))
-        np.testing.assert_allclose(O[0, g * 2:(g + 1) * 2], ref, rtol=0, atol=1e-12)
+    qf = torch.from_numpy(synth.bf16_bits_to_f32(q[0]).astype(np.float64)).view(G, Hq // G, 1, d)
+    kf = torch.from_numpy(synth.bf16_bits_to_f32(K[0]).astype(np.float64)).unsqueeze(1).expand(-1, Hq // G, -1, -1)
+    vf = torch.from_numpy(synth.bf16_bits_to_f32(V[0]).astype(np.float64)).unsqueeze(1).expand(-1, Hq // G, -1, -1)
+    ref = torch.nn.functional.scaled_dot_product_attention(qf, kf, vf).reshape(Hq, d).numpy()
+    np.testing.assert_allclose(O[0], ref, rtol=0, atol=1e-10)
 
 
 def test_driver_retention_budget():
