@@ -302,3 +302,59 @@ def test_host_residency_large_selections(cuda_device, mode, L, tau, median):
     orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d)
     st = run_parity(skv, orc, toks, Ks, Vs, qs, script, synth.BOUNDARY_IDS, cuda_device, mode=mode)
     assert st["max_abs"] <= ATOL
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_nan_inf_and_signed_zero_keys(cuda_device, mode):
+    """The key rule on the GPU (reading A14: NaN scores rank last, -0 == +0, +-Inf order as numbers):
+    sentences whose keys hold NaN, +Inf or -Inf give NaN / infinite embeddings and scores; the scores
+    (bit patterns) and the selected ids must equal the oracle's, and O where both sides are finite."""
+    import paper_2504_00970_b200 as skvlib
+
+    B, Hq, G, d, L, tau, steps = 1, 4, 1, 64, 3000, 120, 6
+    toks, topics = synth.prompts(31, B, L, median=20.0)
+    K, V = synth.kv_layer(31, 0, topics, G, d)
+    off = oracle.segment(toks[0], synth.BOUNDARY_IDS, tau)
+    Kf = synth.bf16_bits_to_f32(K).copy()
+    for s, val in ((5, np.nan), (9, np.inf), (14, -np.inf), (20, np.nan), (33, np.inf)):
+        Kf[0, 0, off[s], s % d] = val                       # one poisoned coordinate
+    Kf[0, 0, off[40]:off[41]] = -0.0                         # a sentence of negative zeros
+    Kf[0, 0, off[41]:off[42]] = 0.0                          # ... and one of positive zeros
+    K = synth.f32_to_bf16_bits(Kf)
+    dev = cuda_device
+    skv = _skv(B, 1, Hq, G, d, L, tau)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, 1, Hq, G, d)
+    Kd, Vd = from_bits(K, dev), from_bits(V, dev)
+    skv.prefill_compress(0, Kd, Vd, token_ids=torch.from_numpy(toks).to(dev), boundary_ids=synth.BOUNDARY_IDS)
+    orc.prefill_layer(0, K, V)
+    E = to_bits(skv.embeddings(0))
+    S = skv.sentence_counts()[0]
+    assert np.array_equal(E[0, 0, :S], orc.E[0][0][0])
+    ids = torch.empty((B, G, tau), dtype=torch.int32, device=dev)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+    rng = np.random.default_rng(5)
+    seen_nonfinite = False
+    for s in range(steps):
+        qf = rng.standard_normal((B, Hq, d)).astype(np.float32)
+        if s == 2:
+            qf[:] = 0.0  # q = 0: Inf * 0 = NaN scores for the infinite sentences
+        q = synth.f32_to_bf16_bits(qf)
+        it = torch.full((B,), 500, dtype=torch.int32, device=dev)
+        if mode == "split":
+            skv.decode_select(0, from_bits(q, dev), it, ids)
+            skv.decode_attend(0, from_bits(q, dev), out)
+        else:
+            skv.decode_step(0, from_bits(q, dev), it, out, ids)
+        sc_o, ids_o, _ = orc.decode_select(0, q, np.array([500]))
+        O_o = orc.decode_attend(0, q, ids_o)
+        sc_g = skv.scores(0).cpu().numpy()
+        assert np.array_equal(sc_g[0, 0, :S].view(np.uint32), sc_o[0][0].view(np.uint32)), f"scores s={s}"
+        seen_nonfinite |= not np.all(np.isfinite(sc_o[0][0]))
+        n = len(ids_o[0][0])
+        got = ids.cpu().numpy()
+        assert np.array_equal(got[0, 0, :n], ids_o[0][0]) and np.all(got[0, 0, n:] == -1), f"ids s={s}"
+        O_g = out.cpu().numpy()
+        fin = np.isfinite(O_o) & np.isfinite(O_g)
+        assert np.array_equal(np.isfinite(O_o), np.isfinite(O_g))
+        assert np.all(np.abs(O_g[fin] - O_o[fin]) <= ATOL)
+    assert seen_nonfinite
