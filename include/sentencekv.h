@@ -112,8 +112,9 @@ typedef struct {
     int32_t fill_mode;       /* skv_fill_mode (default SKV_FILL_PREFIX) */
     int32_t max_generated;   /* NEXT-2 (reading A29): > 0 keeps a local segment and grows the context -- up to
                                 this many generated tokens per (sequence, layer) appended with
-                                sentencekv_decode_append; 0 = off.  Device residency, without retention or
-                                Quest pages (else UNSUPPORTED). */
+                                sentencekv_decode_append; 0 = off.  Device residency, without Quest pages
+                                (else UNSUPPORTED).  With retention (obs_window > 0) the buckets start as
+                                the retained buckets and the observation window stays attended. */
 } skv_config;
 
 /* Fills cfg with defaults (shard = everything, device residency, r = 2, obs_window = 0). */
@@ -245,7 +246,8 @@ skv_status sentencekv_decode_step(skv_ctx* ctx, int32_t layer, const void* q, co
  *   - if the sentence being generated ended at the previous step's token (a boundary input, A11, or
  *     tau tokens long, A5), it becomes a retrievable bucket of the layer: Eq. 1 mean of its keys
  *     appended to the layer's embeddings, its rows appended to the layer's bucket offsets (rows
- *     >= L are generated rows; sel_ids >= the prompt's sentence count name generated sentences);
+ *     >= L are generated rows; sel_ids >= the prompt's sentence count name generated sentences --
+ *     the k-th one is sel_id S + k, S the prompt's sentence count, with or without retention);
  *   - this step's k, v are appended to the generated store; the tokens of the sentence being
  *     generated (this one included) form the local segment, which decode_attend / decode_step attend
  *     in addition to the selection, not charged to tau.

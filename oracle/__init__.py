@@ -350,7 +350,12 @@ class Oracle:
             self.gV[layer] = [np.zeros((self.G, 0, self.d), np.uint16) for _ in range(self.B)]
             self.ghot[layer] = [0] * self.B
             self.gpend[layer] = [False] * self.B
-            self.goff[layer] = [self.off[b].copy() for b in range(self.B)]
+            self.goff[layer] = [self.offsets(layer, b).copy() for b in range(self.B)]
+            if layer in self.loff:  # retention: bucket ids -> sentence ids, extended by the generated ones
+                self.gsid0 = getattr(self, "gsid0", {})
+                self.gsid0[layer] = [len(self.sid[layer][b]) for b in range(self.B)]
+        # rows of generated token i: L + i, or (retention) m + N + i behind the pool and the window
+        base = [(L if layer not in self.loff else self.loff[layer][b][-1] + self.N) for b in range(self.B)]
         for b in range(self.B):
             n = self.gK[layer][b].shape[1]
             if self.gpend[layer][b]:
@@ -358,7 +363,10 @@ class Oracle:
                 for g in range(self.G):
                     e = embed(self.gK[layer][b][g, h:n], np.array([0, n - h], np.int32))
                     self.E[layer][b][g] = np.concatenate([self.E[layer][b][g], e])
-                self.goff[layer][b] = np.append(self.goff[layer][b], np.int32(L + n))
+                self.goff[layer][b] = np.append(self.goff[layer][b], np.int32(base[b] + n))
+                if layer in self.loff:  # generated sentence k of sequence b is sentence S_b + k
+                    k = len(self.goff[layer][b]) - 2 - self.gsid0[layer][b]
+                    self.sid[layer][b] = np.append(self.sid[layer][b], np.int32(len(self.off[b]) - 1 + k))
                 self.ghot[layer][b] = n
                 self.gpend[layer][b] = False
             self.gK[layer][b] = np.concatenate([self.gK[layer][b], k_bits[b][:, None, :]], axis=1)
@@ -440,20 +448,24 @@ class Oracle:
         for b in range(self.B):
             for g in range(self.G):
                 h0 = g * self.grp
-                K, V, off, sel = self.K[layer][b][g], self.V[layer][b][g], self.offsets(layer, b), list(ids[b][g])
-                if layer in self.win:  # NEXT-1: the observation window, attended every step (A25)
+                # the attended rows, written out: selected buckets, the observation window (retention),
+                # the sentence being generated (NEXT-2); rows index the concatenation of the context (or
+                # the retained pool), the window and the generated tokens
+                K, V = self.K[layer][b][g], self.V[layer][b][g]
+                off = self.offsets(layer, b)
+                rows = [np.arange(off[s], off[s + 1]) for s in ids[b][g]]
+                if layer in self.win:
                     wk, wv = self.win[layer][b]
+                    rows.append(np.arange(K.shape[0], K.shape[0] + self.N))
                     K = np.concatenate([K, wk[g]])
                     V = np.concatenate([V, wv[g]])
-                    off = np.append(off, np.int32(K.shape[0]))
-                    sel = sel + [len(off) - 2]
                 if layer in self.gK:
-                    n = self.gK[layer][b].shape[1]
+                    n, h = self.gK[layer][b].shape[1], self.ghot[layer][b]
+                    rows.append(np.arange(K.shape[0] + h, K.shape[0] + n))
                     K = np.concatenate([K, self.gK[layer][b][g]])
                     V = np.concatenate([V, self.gV[layer][b][g]])
-                    if n > self.ghot[layer][b]:  # the local segment as one extra, always-attended range
-                        off = np.append(off, np.int32(K.shape[0]))
-                        sel = sel + [len(off) - 2]
-                O[b, h0 : h0 + self.grp] = attend(
-                    q_bits[b, h0 : h0 + self.grp], K, V, off, np.asarray(sel, np.int32))
+                idx = np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64)
+                Ka, Va = np.ascontiguousarray(K[idx]), np.ascontiguousarray(V[idx])
+                O[b, h0 : h0 + self.grp] = attend(q_bits[b, h0 : h0 + self.grp], Ka, Va,
+                                                  np.array([0, len(idx)], np.int32), np.array([0], np.int32))
         return O

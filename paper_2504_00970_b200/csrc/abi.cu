@@ -82,6 +82,8 @@ void free_sel(skv::SelBufs& s) {
 }
 
 void free_local(skv::LayerState& ls) {
+    dfree(ls.gsid);
+    dfree(ls.gS0);
     dfree(ls.genK);
     dfree(ls.genV);
     dfree(ls.gstat);
@@ -217,8 +219,7 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
     if (cfg.obs_window > 0 && cfg.bucket_mode == SKV_BUCKETS_QUEST) return SKV_ERR_UNSUPPORTED;
     if (cfg.max_generated < 0) return SKV_ERR_INVALID_ARGUMENT;
     // NEXT-2 local segment: device residency, sentence / equal buckets, no retention (this build)
-    if (cfg.max_generated > 0 && (cfg.residency != SKV_KV_DEVICE || cfg.obs_window > 0 ||
-                                  cfg.bucket_mode == SKV_BUCKETS_QUEST))
+    if (cfg.max_generated > 0 && (cfg.residency != SKV_KV_DEVICE || cfg.bucket_mode == SKV_BUCKETS_QUEST))
         return SKV_ERR_UNSUPPORTED;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
         (cfg.obs_window > 0 && !skv::retain_supported(cfg.head_dim, cfg.obs_window, grp)))
@@ -341,6 +342,10 @@ struct LayerView {
 };
 static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
     const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0x7fffffff, 0, 0};  // no generated rows
+    if (ls.retained && ls.genK)  // + NEXT-2: the store = the window (always attended), then generated rows
+        return {ls.goff, c->Smax + 1, ls.gS, ls.PK, ls.PV, ls.ret_m, ls.gsid, c->Smax, false,
+                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated + c->cfg.obs_window, ls.ret_m,
+                            c->cfg.obs_window, c->cfg.obs_window + c->tau}};
     if (ls.retained)  // the pool; rows >= m are the observation window's, always attended (A25)
         return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false,
                 skv::GenSrc{ls.winK, ls.winV, ls.wstat, c->cfg.obs_window, ls.ret_m, c->cfg.obs_window,
@@ -408,12 +413,17 @@ static skv_status alloc_prompt_buffers(skv_ctx* c, int Smax) {
         }
         SKV_CUDA(c, dalloc(&ls.unit_hint, U));
         if (c->cfg.max_generated > 0) {
-            const size_t mg = (size_t)c->cfg.max_generated;
+            // the store holds the observation window first when retention is on (always attended)
+            const size_t mg = (size_t)c->cfg.max_generated + (size_t)c->cfg.obs_window;
             SKV_CUDA(c, dalloc(&ls.genK, U * mg * d));
             SKV_CUDA(c, dalloc(&ls.genV, U * mg * d));
             SKV_CUDA(c, dalloc(&ls.gstat, B * 4));
             SKV_CUDA(c, dalloc(&ls.goff, B * (size_t)(Smax + 1)));
             SKV_CUDA(c, dalloc(&ls.gS, B));
+            if (c->cfg.obs_window > 0) {
+                SKV_CUDA(c, dalloc(&ls.gsid, B * (size_t)Smax));
+                SKV_CUDA(c, dalloc(&ls.gS0, B));
+            }
         }
     }
     dfree(c->unit_cand);
@@ -636,7 +646,25 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         ls.K = Kb;  // device residency: borrowed until the next prefill or destroy
         ls.V = Vb;
     }
-    if (c->cfg.max_generated > 0) {
+    if (c->cfg.max_generated > 0 && ls.retained) {
+        // NEXT-1 + NEXT-2: the buckets start as the retained buckets (and their sentence ids); the store
+        // starts with the observation window's rows, always attended; no generated token yet
+        const int m = ls.ret_m;
+        const size_t cap = (size_t)c->cfg.max_generated + N;
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.goff, sizeof(int32_t) * (c->Smax + 1), ls.roff, sizeof(int32_t) * (m + 1),
+                                      sizeof(int32_t) * std::min(m + 1, c->Smax + 1), c->B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.gsid, sizeof(int32_t) * c->Smax, ls.rsid, sizeof(int32_t) * m,
+                                      sizeof(int32_t) * std::min(m, c->Smax), c->B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.gS, ls.rS, sizeof(int32_t) * c->B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.gS0, ls.rS, sizeof(int32_t) * c->B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.genK, sizeof(__nv_bfloat16) * cap * c->d, ls.winK,
+                                      sizeof(__nv_bfloat16) * N * c->d, sizeof(__nv_bfloat16) * N * c->d,
+                                      (size_t)c->B * c->G, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpy2DAsync(ls.genV, sizeof(__nv_bfloat16) * cap * c->d, ls.winV,
+                                      sizeof(__nv_bfloat16) * N * c->d, sizeof(__nv_bfloat16) * N * c->d,
+                                      (size_t)c->B * c->G, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(c, cudaMemcpyAsync(ls.gstat, ls.wstat, sizeof(int32_t) * 4 * c->B, cudaMemcpyDeviceToDevice, st));
+    } else if (c->cfg.max_generated > 0) {
         // NEXT-2: the layer's buckets start as the prompt's sentences; no generated token yet
         SKV_CUDA(c, cudaMemcpy2DAsync(ls.goff, sizeof(int32_t) * (c->Smax + 1), c->off, sizeof(int32_t) * c->off_stride,
                                       sizeof(int32_t) * (std::min(c->off_stride, c->Smax + 1)), c->B,
@@ -777,10 +805,12 @@ SKV_API skv_status sentencekv_decode_append(skv_ctx* c, int32_t layer, const voi
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_);
     DeviceGuard dg(c->cfg.device);
     cudaEvent_t pa = prof_begin(c, st);
+    const bool ret = ls.retained;
     SKV_CUDA(c, skv::launch_gen_append(static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v),
-                                       ls.genK, ls.genV, c->cfg.max_generated, ls.gstat, ls.goff, c->Smax + 1, ls.gS,
-                                       c->Smax, ls.E, input_token, c->bset, c->n_bset, c->B, c->G, c->L, c->d, c->tau,
-                                       st));
+                                       ls.genK, ls.genV, c->cfg.max_generated + (ret ? c->cfg.obs_window : 0), ls.gstat,
+                                       ls.goff, c->Smax + 1, ls.gS, c->Smax, ls.E, input_token, c->bset, c->n_bset, c->B,
+                                       c->G, ret ? ls.ret_m : c->L, c->d, c->tau, ret ? ls.gsid : nullptr,
+                                       ret ? c->S_dev : nullptr, ret ? ls.gS0 : nullptr, st));
     prof_end(c, SKV_K_APPEND, pa, st);
     c->launches += 2;
     return SKV_OK;

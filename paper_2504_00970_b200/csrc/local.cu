@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(128) gen_close_append_kernel(const __nv_bfloat
 // One thread per sequence: bucket offsets / count of a closed sentence, then the counters.
 __global__ void gen_state_kernel(int B, int L, int max_gen, int tau, int32_t* __restrict__ gstat, int32_t* __restrict__ goff,
                                  int off_stride, int32_t* __restrict__ gS, const int32_t* __restrict__ input_token,
-                                 const int32_t* __restrict__ bset, int nb) {
+                                 const int32_t* __restrict__ bset, int nb, int32_t* __restrict__ gsid, int sid_stride,
+                                 const int32_t* __restrict__ S_prompt, const int32_t* __restrict__ gS0) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     int32_t* st = gstat + b * 4;
@@ -71,6 +72,8 @@ __global__ void gen_state_kernel(int B, int L, int max_gen, int tau, int32_t* __
         const int s = gS[b];
         goff[(size_t)b * off_stride + s + 1] = L + n;
         gS[b] = s + 1;
+        // retention: bucket ids map to sentence ids; a generated sentence is sentence S + k of the text
+        if (gsid) gsid[(size_t)b * sid_stride + s] = S_prompt[b] + (s - gS0[b]);
         st[1] = n;
         st[2] = 0;
     }
@@ -109,7 +112,8 @@ cudaError_t launch_wait_peers(const unsigned int* flag, unsigned int* target, un
 cudaError_t launch_gen_append(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* Kg, __nv_bfloat16* Vg,
                               int max_gen, int32_t* gstat, int32_t* goff, int off_stride, int32_t* gS, int Smax,
                               __nv_bfloat16* E, const int32_t* input_token, const int32_t* bset, int nb, int B, int G,
-                              int L, int d, int tau, cudaStream_t st) {
+                              int L, int d, int tau, int32_t* gsid, const int32_t* S_prompt, const int32_t* gS0,
+                              cudaStream_t st) {
     if (d == 128)
         gen_close_append_kernel<128><<<dim3(G, B), 128, 0, st>>>(k, v, Kg, Vg, max_gen, gstat, gS, Smax, E);
     else
@@ -117,7 +121,7 @@ cudaError_t launch_gen_append(const __nv_bfloat16* k, const __nv_bfloat16* v, __
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     gen_state_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, L, max_gen, tau, gstat, goff, off_stride, gS, input_token, bset,
-                                                     nb);
+                                                     nb, gsid, Smax, S_prompt, gS0);
     return cudaGetLastError();
 }
 

@@ -112,6 +112,8 @@ struct LayerState {
     int32_t* gstat = nullptr;          // [B][4]
     int32_t* goff = nullptr;           // [B][Smax+1] the prompt's offsets followed by completed generated sentences
     int32_t* gS = nullptr;             // [B] buckets
+    int32_t* gsid = nullptr;           // retention + NEXT-2: [B][Smax] bucket -> sentence id (generated: S + k)
+    int32_t* gS0 = nullptr;            // retention + NEXT-2: [B] retained buckets at prefill
     // NEXT-1 observation window, always attended with retention (reading A25)
     __nv_bfloat16* winK = nullptr;     // [B][G][N][d]
     __nv_bfloat16* winV = nullptr;
@@ -240,7 +242,8 @@ cudaError_t launch_wait_peers(const unsigned int* flag, unsigned int* target, un
 cudaError_t launch_gen_append(const __nv_bfloat16* k, const __nv_bfloat16* v, __nv_bfloat16* Kg, __nv_bfloat16* Vg,
                               int max_gen, int32_t* gstat, int32_t* goff, int off_stride, int32_t* gS, int Smax,
                               __nv_bfloat16* E, const int32_t* input_token, const int32_t* bset, int nb, int B, int G,
-                              int L, int d, int tau, cudaStream_t st);
+                              int L, int d, int tau, int32_t* gsid, const int32_t* S_prompt, const int32_t* gS0,
+                              cudaStream_t st);
 
 // Opt-in dynamic shared memory of `func` on the current device (the attribute is per device
 // context; cached per (device, function), thread-safe).

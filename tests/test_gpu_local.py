@@ -102,3 +102,68 @@ def test_local_overflow_is_a_state_error(cuda_device):
     skv.decode_append(0, kv, kv, it)
     with pytest.raises(skvlib.SkvError, match="STATE"):
         skv.sync()
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_local_with_retention(cuda_device, mode):
+    """NEXT-1 + NEXT-2 together (a serving loop with retention): the retained pool's buckets, the
+    observation window (always attended), the sentence being generated (always attended) and the
+    completed generated sentences (buckets; sel_ids = the prompt's sentence count + k)."""
+    import paper_2504_00970_b200 as skvlib
+
+    dev = cuda_device
+    B, M, Hq, G, d, L, N, steps, seed = 1, 1, 32, 8, 128, 3000, 32, 30, 3
+    toks, topics = synth.prompts(seed, B, L, median=20.0)
+    Ks, Vs = zip(*(synth.kv_layer(seed, l, topics, G, d) for l in range(M)))
+    # the window asks about 3 topics (as in test_gpu_retention): the retained set is unambiguous
+    for k in range(100):
+        pick = np.random.default_rng(seed * 1000 + k).choice(synth.N_TOPICS, 3, replace=False)
+        count = int(np.isin(topics[0, :L - N], pick).sum())
+        if count % 2 == 0:
+            break
+    tau = count // 2
+    qw = [synth.window_queries(seed, l, pick[np.arange(N) % 3][None, :], Hq, G, d, scale=3.0) for l in range(M)]
+    skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
+                            semantic_factor=2.0, obs_window=N, max_generated=64)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d, obs_window=N, semantic_factor=2.0,
+                        max_generated=64)
+    tok_dev = torch.from_numpy(toks).to(dev)
+    for l in range(M):
+        skv.prefill_compress(l, from_bits(Ks[l], dev), from_bits(Vs[l], dev), token_ids=tok_dev if l == 0 else None,
+                             boundary_ids=synth.BOUNDARY_IDS if l == 0 else None, q_window=from_bits(qw[l], dev))
+        orc.prefill_layer(l, Ks[l], Vs[l], q_window=qw[l])
+    skv.sync()
+    assert np.array_equal(skv.retained(0)[0].cpu().numpy()[0], orc.keep[0][0])
+    script, target = synth.decode_script(seed, B, steps, mean_sentence=5.0)
+    rng = np.random.default_rng(seed + 7)
+    ids = torch.empty((B, G, tau), dtype=torch.int32, device=dev)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+    S_prompt = len(orc.off[0]) - 1
+    n_pool = len(orc.sid[0][0])
+    grown = False
+    for s in range(steps):
+        it = torch.from_numpy(script[s]).to(dev)
+        for l in range(M):
+            kg = synth.f32_to_bf16_bits(rng.standard_normal((B, G, d)).astype(np.float32) + 0.5)
+            vg = synth.f32_to_bf16_bits(rng.standard_normal((B, G, d)).astype(np.float32))
+            q = synth.queries(seed, l, s, target[s], Hq, G, d)
+            skv.decode_append(l, from_bits(kg, dev), from_bits(vg, dev), it)
+            orc.decode_append(l, kg, vg, script[s])
+            if mode == "split":
+                skv.decode_select(l, from_bits(q, dev), it, ids)
+                skv.decode_attend(l, from_bits(q, dev), out)
+            else:
+                skv.decode_step(l, from_bits(q, dev), it, out, ids)
+            _, ids_o, _ = orc.decode_select(l, q, script[s])
+            O_o = orc.decode_attend(l, q, ids_o)
+            got = ids.cpu().numpy()
+            for g in range(G):
+                want = orc.sid[l][0][ids_o[0][g]]
+                grown |= bool(np.any(want >= S_prompt))
+                n = len(want)
+                assert np.array_equal(got[0, g, :n], want) and np.all(got[0, g, n:] == -1), f"ids s={s} g={g}"
+            err = float(np.abs(out.cpu().numpy() - O_o).max())
+            assert err <= ATOL, f"O s={s}: {err}"
+    skv.sync()
+    gen = orc.sid[0][0][n_pool:]
+    assert len(gen) >= 3 and np.array_equal(gen, S_prompt + np.arange(len(gen)))  # generated buckets appeared

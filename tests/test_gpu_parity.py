@@ -329,7 +329,11 @@ def test_nan_inf_and_signed_zero_keys(cuda_device, mode):
     orc.prefill_layer(0, K, V)
     E = to_bits(skv.embeddings(0))
     S = skv.sentence_counts()[0]
-    assert np.array_equal(E[0, 0, :S], orc.E[0][0][0])
+    # bit-exact, except that a NaN's payload is not part of the canonical arithmetic (A7: NaN stays NaN)
+    Eg, Eo = E[0, 0, :S], orc.E[0][0][0]
+    nan_g, nan_o = np.isnan(synth.bf16_bits_to_f32(Eg)), np.isnan(synth.bf16_bits_to_f32(Eo))
+    assert np.array_equal(nan_g, nan_o) and nan_o.any()
+    assert np.array_equal(Eg[~nan_o], Eo[~nan_o])
     ids = torch.empty((B, G, tau), dtype=torch.int32, device=dev)
     out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
     rng = np.random.default_rng(5)
@@ -347,8 +351,10 @@ def test_nan_inf_and_signed_zero_keys(cuda_device, mode):
             skv.decode_step(0, from_bits(q, dev), it, out, ids)
         sc_o, ids_o, _ = orc.decode_select(0, q, np.array([500]))
         O_o = orc.decode_attend(0, q, ids_o)
-        sc_g = skv.scores(0).cpu().numpy()
-        assert np.array_equal(sc_g[0, 0, :S].view(np.uint32), sc_o[0][0].view(np.uint32)), f"scores s={s}"
+        sc_g = skv.scores(0).cpu().numpy()[0, 0, :S]
+        so = sc_o[0][0]
+        assert np.array_equal(np.isnan(sc_g), np.isnan(so)), f"NaN scores s={s}"
+        assert np.array_equal(sc_g[~np.isnan(so)].view(np.uint32), so[~np.isnan(so)].view(np.uint32)), f"scores s={s}"
         seen_nonfinite |= not np.all(np.isfinite(sc_o[0][0]))
         n = len(ids_o[0][0])
         got = ids.cpu().numpy()
