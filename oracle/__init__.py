@@ -354,8 +354,13 @@ class Oracle:
             if layer in self.loff:  # retention: bucket ids -> sentence ids, extended by the generated ones
                 self.gsid0 = getattr(self, "gsid0", {})
                 self.gsid0[layer] = [len(self.sid[layer][b]) for b in range(self.B)]
-        # rows of generated token i: L + i, or (retention) m + N + i behind the pool and the window
-        base = [(L if layer not in self.loff else self.loff[layer][b][-1] + self.N) for b in range(self.B)]
+                # the observation window's rows are the local segment when decoding starts (A29): the
+                # store begins with them, and they close with the first generated sentence
+                self.gK[layer] = [self.win[layer][b][0].copy() for b in range(self.B)]
+                self.gV[layer] = [self.win[layer][b][1].copy() for b in range(self.B)]
+        # store row i (generated token i, or with retention the window's rows first) is row L + i, or
+        # (retention) m + i behind the retained pool
+        base = [(L if layer not in self.loff else self.loff[layer][b][-1]) for b in range(self.B)]
         for b in range(self.B):
             n = self.gK[layer][b].shape[1]
             if self.gpend[layer][b]:
@@ -454,7 +459,7 @@ class Oracle:
                 K, V = self.K[layer][b][g], self.V[layer][b][g]
                 off = self.offsets(layer, b)
                 rows = [np.arange(off[s], off[s + 1]) for s in ids[b][g]]
-                if layer in self.win:
+                if layer in self.win and layer not in self.gK:  # (with NEXT-2 the window is in the store)
                     wk, wv = self.win[layer][b]
                     rows.append(np.arange(K.shape[0], K.shape[0] + self.N))
                     K = np.concatenate([K, wk[g]])

@@ -342,10 +342,10 @@ struct LayerView {
 };
 static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
     const skv::GenSrc none{nullptr, nullptr, nullptr, 0, 0x7fffffff, 0, 0};  // no generated rows
-    if (ls.retained && ls.genK)  // + NEXT-2: the store = the window (always attended), then generated rows
+    if (ls.retained && ls.genK)  // + NEXT-2: the store = the window, then the generated rows (A29)
         return {ls.goff, c->Smax + 1, ls.gS, ls.PK, ls.PV, ls.ret_m, ls.gsid, c->Smax, false,
-                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated + c->cfg.obs_window, ls.ret_m,
-                            c->cfg.obs_window, c->cfg.obs_window + c->tau}};
+                skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated + c->cfg.obs_window, ls.ret_m, 0,
+                            c->cfg.obs_window + c->tau}};
     if (ls.retained)  // the pool; rows >= m are the observation window's, always attended (A25)
         return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false,
                 skv::GenSrc{ls.winK, ls.winV, ls.wstat, c->cfg.obs_window, ls.ret_m, c->cfg.obs_window,
@@ -647,8 +647,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         ls.V = Vb;
     }
     if (c->cfg.max_generated > 0 && ls.retained) {
-        // NEXT-1 + NEXT-2: the buckets start as the retained buckets (and their sentence ids); the store
-        // starts with the observation window's rows, always attended; no generated token yet
+        // NEXT-1 + NEXT-2 (reading A29): the buckets start as the retained buckets (and their sentence
+        // ids); the store starts with the observation window's rows, which are the local segment when
+        // decoding starts (attended every step, and part of the first generated bucket once the first
+        // generated sentence ends); no generated token yet
         const int m = ls.ret_m;
         const size_t cap = (size_t)c->cfg.max_generated + N;
         SKV_CUDA(c, cudaMemcpy2DAsync(ls.goff, sizeof(int32_t) * (c->Smax + 1), ls.roff, sizeof(int32_t) * (m + 1),
@@ -663,7 +665,10 @@ SKV_API skv_status sentencekv_prefill_compress(skv_ctx* c, int32_t layer, const 
         SKV_CUDA(c, cudaMemcpy2DAsync(ls.genV, sizeof(__nv_bfloat16) * cap * c->d, ls.winV,
                                       sizeof(__nv_bfloat16) * N * c->d, sizeof(__nv_bfloat16) * N * c->d,
                                       (size_t)c->B * c->G, cudaMemcpyDeviceToDevice, st));
-        SKV_CUDA(c, cudaMemcpyAsync(ls.gstat, ls.wstat, sizeof(int32_t) * 4 * c->B, cudaMemcpyDeviceToDevice, st));
+        // the window rows are the local segment when decoding starts: {count N, sentence start 0}
+        std::vector<int32_t> gs(4 * (size_t)c->B, 0);
+        for (int b = 0; b < c->B; ++b) gs[4 * (size_t)b] = N;
+        SKV_CUDA(c, cudaMemcpyAsync(ls.gstat, gs.data(), sizeof(int32_t) * gs.size(), cudaMemcpyHostToDevice, st));
     } else if (c->cfg.max_generated > 0) {
         // NEXT-2: the layer's buckets start as the prompt's sentences; no generated token yet
         SKV_CUDA(c, cudaMemcpy2DAsync(ls.goff, sizeof(int32_t) * (c->Smax + 1), c->off, sizeof(int32_t) * c->off_stride,

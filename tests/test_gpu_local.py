@@ -106,9 +106,10 @@ def test_local_overflow_is_a_state_error(cuda_device):
 
 @pytest.mark.parametrize("mode", ["split", "step"])
 def test_local_with_retention(cuda_device, mode):
-    """NEXT-1 + NEXT-2 together (a serving loop with retention): the retained pool's buckets, the
-    observation window (always attended), the sentence being generated (always attended) and the
-    completed generated sentences (buckets; sel_ids = the prompt's sentence count + k)."""
+    """NEXT-1 + NEXT-2 together (a serving loop with retention): the retained pool's buckets, the local
+    segment -- the observation window, then the sentence being generated (always attended) -- and the
+    completed generated sentences (buckets; sel_ids = the prompt's sentence count + k; the first one
+    holds the window's rows too, reading A29)."""
     import paper_2504_00970_b200 as skvlib
 
     dev = cuda_device
@@ -164,6 +165,10 @@ def test_local_with_retention(cuda_device, mode):
                 assert np.array_equal(got[0, g, :n], want) and np.all(got[0, g, n:] == -1), f"ids s={s} g={g}"
             err = float(np.abs(out.cpu().numpy() - O_o).max())
             assert err <= ATOL, f"O s={s}: {err}"
+            nb = len(orc.sid[l][0])  # generated buckets' E (the first includes the window's keys): bit-exact
+            E = to_bits(skv.embeddings(l))
+            for g in range(G):
+                assert np.array_equal(E[0, g, n_pool:nb], orc.E[l][0][g][n_pool:nb]), f"generated E s={s} g={g}"
     skv.sync()
     gen = orc.sid[0][0][n_pool:]
     assert len(gen) >= 3 and np.array_equal(gen, S_prompt + np.arange(len(gen)))  # generated buckets appeared

@@ -96,3 +96,54 @@ def test_no_append_is_the_plain_path():
     rb = b.decode_select(0, q, np.array([9, 9]))
     assert all(np.array_equal(x, y) for x, y in zip(ra[1][0] + ra[1][1], rb[1][0] + rb[1][1]))
     np.testing.assert_array_equal(a.decode_attend(0, q, ra[1]), b.decode_attend(0, q, rb[1]))
+
+
+def test_with_retention_full_budget_equals_full_attention():
+    """NEXT-1 + NEXT-2 (reading A29 with retention): floor(r*tau) >= L - N keeps every prompt token, and a
+    budget above everything selects every bucket, so the decode -- retained buckets, the always-attended
+    observation window, the completed generated sentences and the sentence being generated -- is full
+    attention over the prompt and every generated token (fp64 SDPA, a library routine); the generated
+    buckets are named S + k (S = the prompt's sentence count) and their E is the mean of their keys --
+    the first one's includes the window's N keys (the local segment when decoding starts, A29)."""
+    B, Hq, G, d, L, N, tau = 1, 4, 2, 64, 300, 8, 400
+    toks, topics = synth.prompts(5, B, L, median=20.0)
+    K, V = synth.kv_layer(5, 0, topics, G, d)
+    qw = synth.f32_to_bf16_bits(np.random.default_rng(6).standard_normal((B, N, Hq, d)).astype(np.float32))
+    o = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, 1, Hq, G, d, obs_window=N, semantic_factor=1.0,
+                      max_generated=64)
+    o.prefill_layer(0, K, V, q_window=qw)
+    assert o.keep[0][0].tolist() == list(range(L - N))
+    S = len(o.off[0]) - 1
+    n_pool = len(o.sid[0][0])
+    rng = np.random.default_rng(7)
+    script, target = synth.decode_script(5, B, 25, mean_sentence=5.0)
+    gk, gv = [], []
+    for s in range(25):
+        k, v = _gen_kv(rng, B, G, d)
+        gk.append(k)
+        gv.append(v)
+        o.decode_append(0, k, v, script[s])
+        q = synth.queries(5, 0, s, target[s], Hq, G, d)
+        _, ids, _ = o.decode_select(0, q, script[s])
+        O = o.decode_attend(0, q, ids)
+        Kall = np.concatenate([K[0], np.stack([x[0] for x in gk], axis=1)], axis=1)  # [G][L+s+1][d]
+        Vall = np.concatenate([V[0], np.stack([x[0] for x in gv], axis=1)], axis=1)
+        qf = torch.from_numpy(synth.bf16_bits_to_f32(q[0]).astype(np.float64)).view(G, Hq // G, 1, d)
+        kf = torch.from_numpy(synth.bf16_bits_to_f32(Kall).astype(np.float64)).unsqueeze(1)
+        vf = torch.from_numpy(synth.bf16_bits_to_f32(Vall).astype(np.float64)).unsqueeze(1)
+        ref = torch.nn.functional.scaled_dot_product_attention(qf, kf.expand(-1, Hq // G, -1, -1),
+                                                               vf.expand(-1, Hq // G, -1, -1))
+        np.testing.assert_allclose(O[0], ref.reshape(Hq, d).numpy(), rtol=0, atol=1e-10)
+    gen = o.sid[0][0][n_pool:]
+    assert len(gen) >= 3 and gen.tolist() == list(range(S, S + len(gen)))
+    starts = np.flatnonzero(np.isin(np.concatenate(script[:, 0:1]), synth.BOUNDARY_IDS)) + 1  # sentence ends
+    first = np.concatenate([[0], starts[:len(gen) - 1]])
+    for i in range(len(gen)):  # bucket n_pool + i = generated tokens [first_i, first_{i+1})
+        a, e = int(first[i]), int(starts[i])
+        for g in range(G):
+            rows = [gk[t][0][g] for t in range(a, e)]
+            if i == 0:
+                rows = list(K[0][g][L - N:]) + rows
+            m = synth.bf16_bits_to_f32(np.stack(rows)).astype(np.float64).mean(axis=0)
+            got = synth.bf16_bits_to_f32(o.E[0][0][g][n_pool + i]).astype(np.float64)
+            assert np.max(np.abs(got - m)) <= np.abs(m).max() * 2 ** -8 + 1e-7
