@@ -140,7 +140,8 @@ struct Ctl {
     int bn;             // band path: entries of this CTA at or above the band's lower edge
     uint32_t whi, wband;  // band path: weight above the band / inside it (this CTA)
     int base[kUC + 1];  // exclusive prefix of the cluster's list sizes
-    int ok, nsel, nband, count, ntok, reset, cnt0, kc_set, any_miss;
+    int ok, nsel, nband, count, ntok, reset, cnt0, kc_set;
+    int miss_rank;      // host residency (rank 0's copy): lowest rank of the cluster that met a miss
     int mode;           // band-list ranking mode (see step 2), -1 = general path
     uint32_t WHI, WB, ks, kc;
     uint32_t lo, hi, cb, rem, ncand;
@@ -294,7 +295,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         ctl.nsel = 0;
         ctl.nband = 0;
         ctl.ntok = 0;
-        ctl.any_miss = 0;
+        ctl.miss_rank = kUC;
     }
     // The prompt's sentence counts and embeddings are written only by the prefill, never by the
     // decode kernel this one may overlap (programmatic launch), so the first E tiles are requested
@@ -446,6 +447,21 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             atomicAdd(&ctl.wband, wband);
         }
         if (tid == 0) ctl.bn = (int)total;
+#ifdef SKV_PF_ABOVE
+        // device residency: the K/V runs of this CTA's sentences above the previous step's band are
+        // (almost always) selected -- ask L2 for them now, while the cluster selects (HBM idle)
+        if constexpr (!HOST) {
+            const char* Kb = reinterpret_cast<const char*>(kv.K + (size_t)unit * kv.unit_stride * D);
+            const char* Vb = reinterpret_cast<const char*>(kv.V + (size_t)unit * kv.unit_stride * D);
+            for (int i = i0; i < i1; ++i)
+                if (keys[i] > khi && (!gen.Kg || offs[i + 1] <= gen.L)) {  // context rows only
+                    const size_t o0 = (size_t)offs[i] * D * 2;
+                    const uint32_t nb2 = (uint32_t)(offs[i + 1] - offs[i]) * D * 2;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Kb + o0), "r"(nb2) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Vb + o0), "r"(nb2) : "memory");
+                }
+        }
+#endif
     }
     __syncthreads();
     SKV_USTAMP(1);
@@ -1175,7 +1191,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
         }
         SKV_USTAMP(30);
-        if (tid == 0) atomicOr(cluster.map_shared_rank(&ctl.any_miss, 0), 1);  // rank 0 updates the table
+        if (tid == 0) atomicMin(cluster.map_shared_rank(&ctl.miss_rank, 0), rank);  // lowest such rank updates the table
         __syncthreads();
     }
     SKV_USTAMP(6);
@@ -1306,14 +1322,22 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         pdl_trigger();
         mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
     }
-    cluster.sync();  // #2: CTA partials ready
+    cluster.sync();  // #2: CTA partials ready; every CTA has done its page-table lookups
     SKV_USTAMP(8);
+    // host residency: the lowest rank that met a miss applies its plan (the same in every CTA that
+    // computed one) after barrier #3 -- no other CTA recomputes it, and nobody waits for the update
+    bool upd = false;
+    if constexpr (HOST) upd = any_miss && *cluster.map_shared_rank(&ctl.miss_rank, 0) == rank;
     mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT, &peers,
                                          ((size_t)b * Hq + g * GRP) * D);
-    if (HOST && rank == 0 && ctl.any_miss) {
-        // page-table update of this step's plan (every CTA has done its lookups: after barrier #2);
-        // all selected rows of a page with a slot are in it now
-        if (!any_miss) cache_plan();  // the misses were in other CTAs: same plan, from the same table
+    cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
+    if (rank == 0 && tid == 0) {
+        sel.parity[unit] = cur;
+        if (peers.n) peers_arrive(peers);  // every CTA's slice is in every peer's buffer (8(e) fused gather)
+    }
+    if (HOST && upd) {
+        // page-table update of this step's plan; all selected rows of a page with a slot are in it now.
+        // (The next step reads the table after its programmatic-launch wait, i.e. after this grid.)
         const int n_need = n_need_s;
         int32_t* pt = hc.pt + (size_t)unit * hc.pages;
         for (int j = tid; j < n_need; j += kUT) {
@@ -1326,11 +1350,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (oldof[j] >= 0) pt[oldof[j]] = (int32_t)kEmpty;
         }
         if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
-    }
-    cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
-    if (rank == 0 && tid == 0) {
-        sel.parity[unit] = cur;
-        if (peers.n) peers_arrive(peers);  // every CTA's slice is in every peer's buffer (8(e) fused gather)
     }
     SKV_USTAMP(9);
     SKV_LSTAMP(2);
