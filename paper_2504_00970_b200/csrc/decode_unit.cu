@@ -139,11 +139,12 @@ struct Ctl {
     int own_global;     // general path: list stored in global scratch (overflow)
     int bn;             // band path: entries of this CTA at or above the band's lower edge
     uint32_t whi, wband;  // band path: weight above the band / inside it (this CTA)
+    uint32_t wnar;        // band path: weight of the band's upper part [klo_n, khi] (this CTA)
     int base[kUC + 1];  // exclusive prefix of the cluster's list sizes
     int ok, nsel, nband, count, ntok, reset, cnt0, kc_set;
     int miss_rank;      // host residency (rank 0's copy): lowest rank of the cluster that met a miss
     int mode;           // band-list ranking mode (see step 2), -1 = general path
-    uint32_t WHI, WB, ks, kc;
+    uint32_t WHI, WB, WN, ks, kc;
     uint32_t lo, hi, cb, rem, ncand;
     unsigned long long thr;
 };
@@ -213,6 +214,91 @@ __device__ __forceinline__ bool crossing_bin(const uint32_t* hist, uint32_t rem,
     *cb_out = ctl.cb;
     *rem_out = ctl.rem;
     return true;
+}
+
+// D3 + D4 of one CTA (step 3 of unit_step_kernel): its 16-token tiles of the gathered rows ->
+// mma.sync fragments -> per-warp online softmax -> CTA partial in `msm`.  Not inlined: the caller's
+// state lives across this phase, and inlined it pushed the tile registers into local memory (spills
+// in the tile loop, measured slower); across a call it is saved once.
+//   Kd / Vd: device residency: the unit's context rows (generated rows >= genL in Kgu / Vgu);
+//            host residency: the unit's working-set rows (r >= 0), host row -(r+1) in Khu / Vhu
+//   MISS:    some rows of this CTA come from host (they are written through into the working set)
+template <int D, int GRP, bool HOST, bool MISS>
+__device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int tb, int te, int T0, int T1,
+                                          const __nv_bfloat16* __restrict__ qg, const __nv_bfloat16* Kd,
+                                          const __nv_bfloat16* Vd, const __nv_bfloat16* Khu, const __nv_bfloat16* Vhu,
+                                          const __nv_bfloat16* Kgu, const __nv_bfloat16* Vgu, int genL,
+                                          unsigned long long* ledger, float scale_log2,
+                                          USmemMerge<D>& msm) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gq = lane >> 2, cq = lane & 3;
+    auto rowK = [&](int r) -> const __nv_bfloat16* {
+        return (HOST && r < 0) ? Khu + (size_t)(-(r + 1)) * D : Kd + (size_t)r * D;
+    };
+    auto rowV = [&](int r) -> const __nv_bfloat16* {
+        return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : Vd + (size_t)r * D;
+    };
+    // device rows: context rows < L, generated rows (NEXT-2) >= L
+    auto devK = [&](int r) -> const __nv_bfloat16* {
+        return (!HOST && Kgu && r >= genL) ? Kgu + (size_t)(r - genL) * D : Kd + (size_t)r * D;
+    };
+    auto devV = [&](int r) -> const __nv_bfloat16* {
+        return (!HOST && Vgu && r >= genL) ? Vgu + (size_t)(r - genL) * D : Vd + (size_t)r * D;
+    };
+    unsigned long long host_bytes = 0;
+    uint4 qseg[D / 32];
+    mma::load_q<D, GRP>(qseg, qg, lane);
+    mma::WarpAcc<D> wacc;
+    wacc.init();
+    {
+        for (int tile = tb + warp; tile < te; tile += kUW) {
+            const int t0 = tile * kTile;
+            const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+            int2 rv[4];
+            const __nv_bfloat16* pv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+                pv[k] = rv[k].x != kInvalid ? (MISS ? rowV(rv[k].x) : devV(rv[k].x)) : nullptr;
+            }
+            mma::TileRegs<D> tr;
+            if constexpr (MISS)
+                mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr,
+                                  rk1.x != kInvalid ? rowK(rk1.x) : nullptr, pv, lane);
+            else
+                mma::load_tile<D>(tr, rk0.x != kInvalid ? devK(rk0.x) : nullptr,
+                                  rk1.x != kInvalid ? devK(rk1.x) : nullptr, pv, lane);
+            mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
+            if constexpr (MISS) {
+                // write-through of the rows read from host into their working-set slot
+                constexpr int NU = D / 32, NVP = D / 64;
+                __nv_bfloat16* Kw = const_cast<__nv_bfloat16*>(Kd);  // (host residency: the working set)
+                __nv_bfloat16* Vw = const_cast<__nv_bfloat16*>(Vd);
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + mma::kseg(cq, u)) = tr.kA[u];
+                    if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + mma::kseg(cq, u)) = tr.kB[u];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int pp = 0; pp < NVP; ++pp)
+                        if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
+                // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
+                if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
+                if (gq == 0)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
+            }
+        }
+    }
+    if constexpr (HOST) {
+        // transfer ledger: host rows read by this CTA
+#pragma unroll
+        for (int o2 = 16; o2 >= 1; o2 >>= 1) host_bytes += __shfl_xor_sync(0xffffffffu, host_bytes, o2);
+        if (lane == 0 && host_bytes) atomicAdd(ledger, host_bytes);
+    }
+    mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
 }
 
 }  // namespace
@@ -290,6 +376,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         ctl.bn = 0;
         ctl.whi = 0u;
         ctl.wband = 0u;
+        ctl.wnar = 0u;
         ctl.ks = 0xffffffffu;
         ctl.kc_set = 0;
         ctl.nsel = 0;
@@ -324,6 +411,11 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int prev = sel.parity[unit], cur = prev ^ 1;
     const uint2 band = hint[unit];  // [klo, khi]: where the crossing point was at the previous step
     const uint32_t klo = band.x, khi = band.y;
+    // the band's upper part [klo_n, khi], klo_n = crossing point - w: the crossing point usually stays
+    // there, and then only that part is ranked (the quadratic rank is ~9x cheaper than over the band)
+    auto klo_narrow = [&]() -> uint32_t {
+        return klo ? klo + (((uint32_t)band_w << kBandLoShift) - (uint32_t)band_w) : 0u;
+    };
     if (warp == kUW - 2) {
         // does this step's input token end a sentence (Q_s reset after this step, A11)?
         const int it = input_token[b];
@@ -427,13 +519,18 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int per_t = (n + kUT - 1) / kUT;
     const int i0 = min(n, tid * per_t), i1 = min(n, i0 + per_t);
     {
-        uint32_t mine = 0, whi = 0, wband = 0;
+        uint32_t mine = 0, whi = 0, wband = 0, wnar = 0;
+        const uint32_t klo_n = klo_narrow();
         for (int i = i0; i < i1; ++i) {
             const uint32_t k = keys[i];
             if (k >= klo) {
                 ++mine;
                 const uint32_t len = (uint32_t)(offs[i + 1] - offs[i]);
-                if (k > khi) whi += len; else wband += len;
+                if (k > khi) whi += len;
+                else {
+                    wband += len;
+                    if (k >= klo_n) wnar += len;
+                }
             }
         }
         uint32_t total;
@@ -442,9 +539,11 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (keys[i] >= klo) blist[pos++] = make_int4((int)keys[i], s0 + i, offs[i], offs[i + 1] - offs[i]);
         whi = __reduce_add_sync(0xffffffffu, whi);
         wband = __reduce_add_sync(0xffffffffu, wband);
+        wnar = __reduce_add_sync(0xffffffffu, wnar);
         if (lane == 0) {
             atomicAdd(&ctl.whi, whi);
             atomicAdd(&ctl.wband, wband);
+            atomicAdd(&ctl.wnar, wnar);
         }
         if (tid == 0) ctl.bn = (int)total;
 #ifdef SKV_PF_ABOVE
@@ -473,19 +572,21 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     // ranking changes little from token to token): everything above khi is selected and only the
     // band is ranked.  Exact whenever its conditions hold; otherwise the general path below.
     if (warp == 0) {
-        uint32_t whi = 0, wband = 0;
+        uint32_t whi = 0, wband = 0, wnar = 0;
         int bn = 0;
         const int4* lp = nullptr;
         if (lane < kUC) {
             Ctl* rc = cluster.map_shared_rank(&ctl, lane);
             whi = rc->whi;
             wband = rc->wband;
+            wnar = rc->wnar;
             bn = rc->bn;
             lp = cluster.map_shared_rank(blist, lane);
         }
         const bool ovf = __any_sync(0xffffffffu, bn > kUBandCap);
         const int incl = warp_incl_sum<int>(bn);
         const uint32_t WHI = __reduce_add_sync(0xffffffffu, whi), WB = __reduce_add_sync(0xffffffffu, wband);
+        const uint32_t WN = __reduce_add_sync(0xffffffffu, wnar);
         if (lane < kUC) {
             ctl.base[lane + 1] = incl;
             lists[lane] = lp;
@@ -494,6 +595,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             ctl.base[0] = 0;
             ctl.WHI = WHI;
             ctl.WB = WB;
+            ctl.WN = WN;
             // 0: the crossing point is in the band; 2: above it (only entries above khi can be
             // selected, and all of them are listed); -1: a list overflowed, or the crossing point is
             // below the band -> general path.  (Rebuilding the lists below the band instead was
@@ -526,6 +628,14 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         auto_gt = 0xffffffffu;
         rank_ge = khi + 1u;  // khi < 0xffffffff here (else WHI = 0)
         W0 = 0u;
+    } else if (mode == 0 && klo_narrow() > klo) {
+        const uint32_t klo_n = klo_narrow();
+        if (ctl.WHI + ctl.WN > (uint32_t)tau) {
+            rank_ge = klo_n;  // the crossing point is in the upper part: the lower part is not selected
+        } else {
+            auto_gt = klo_n - 1u;  // the upper part is selected too; the crossing point is below it
+            W0 = ctl.WHI + ctl.WN;
+        }
     }
     bool ok = mode >= 0;
     if (ok) {
@@ -1195,133 +1305,63 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         __syncthreads();
     }
     SKV_USTAMP(6);
+    // ---- stores of this step's state, spread over the CTAs (nothing waits on them) ----
     {
-        const int gq = lane >> 2, cq = lane & 3;
-        // device residency: rows of the context K/V; host residency: r >= 0 working-set row, r < 0 host
-        // row -(r+1) of the mapped pinned store
-        const __nv_bfloat16* Kd = HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D;
-        const __nv_bfloat16* Vd = HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D;
-        const __nv_bfloat16* Khu = HOST ? hc.Kh + (size_t)unit * hc.L * D : nullptr;
-        const __nv_bfloat16* Vhu = HOST ? hc.Vh + (size_t)unit * hc.L * D : nullptr;
-        auto rowK = [&](int r) -> const __nv_bfloat16* {
-            return (HOST && r < 0) ? Khu + (size_t)(-(r + 1)) * D : Kd + (size_t)r * D;
-        };
-        auto rowV = [&](int r) -> const __nv_bfloat16* {
-            return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : Vd + (size_t)r * D;
-        };
-        // device rows: context rows < L, generated rows (NEXT-2) >= L
-        const __nv_bfloat16* Kgu = gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr;
-        const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
-        auto devK = [&](int r) -> const __nv_bfloat16* {
-            return (!HOST && gen.Kg && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
-        };
-        auto devV = [&](int r) -> const __nv_bfloat16* {
-            return (!HOST && gen.Kg && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
-        };
-        unsigned long long host_bytes = 0;
-        uint4 qseg[D / 32];
-        mma::load_q<D, GRP>(qseg, q + ((size_t)b * Hq + g * GRP) * D, lane);
-        mma::WarpAcc<D> wacc;
-        wacc.init();
-        auto tiles = [&](auto miss_tag) {  // miss_tag: some rows of this CTA come from host
-            constexpr bool MISS = decltype(miss_tag)::value;
-        for (int tile = tb + warp; tile < te; tile += kUW) {
-                const int t0 = tile * kTile;
-                const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
-                int2 rv[4];
-                const __nv_bfloat16* pv[4];
-    #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
-                    pv[k] = rv[k].x != kInvalid ? (MISS ? rowV(rv[k].x) : devV(rv[k].x)) : nullptr;
-                }
-                mma::TileRegs<D> tr;
-                if constexpr (MISS)
-                    mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr,
-                                      rk1.x != kInvalid ? rowK(rk1.x) : nullptr, pv, lane);
-                else
-                    mma::load_tile<D>(tr, rk0.x != kInvalid ? devK(rk0.x) : nullptr,
-                                      rk1.x != kInvalid ? devK(rk1.x) : nullptr, pv, lane);
-                mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
-                if constexpr (MISS) {
-                    // write-through of the rows read from host into their working-set slot
-                    constexpr int NU = D / 32, NVP = D / 64;
-                    __nv_bfloat16* Kw = hc.wsK + (size_t)unit * hc.slots * kPage * D;
-                    __nv_bfloat16* Vw = hc.wsV + (size_t)unit * hc.slots * kPage * D;
-    #pragma unroll
-                    for (int u = 0; u < NU; ++u) {
-                        if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + mma::kseg(cq, u)) = tr.kA[u];
-                        if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + mma::kseg(cq, u)) = tr.kB[u];
-                    }
-    #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-    #pragma unroll
-                        for (int pp = 0; pp < NVP; ++pp)
-                            if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
-                    // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
-                    if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
-                    if (gq == 0)
-    #pragma unroll
-                        for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
-                }
-            }
-        };
-        if (HOST && any_miss) tiles(std::true_type{});
-        else tiles(std::false_type{});
-        SKV_USTAMP(7);
-        if constexpr (HOST) {
-            // transfer ledger: host rows read by this CTA
-#pragma unroll
-            for (int o2 = 16; o2 >= 1; o2 >>= 1) host_bytes += __shfl_xor_sync(0xffffffffu, host_bytes, o2);
-            if (lane == 0 && host_bytes) atomicAdd(hc.ledger, host_bytes);
+        const int sh = (count + kUC - 1) / kUC;  // selection entries written by this CTA
+        int32_t* gids = sel.ids_of(cur, unit);
+        int32_t* gtok = sel.tok_of(cur, unit);
+        int32_t* gsrc = sel.src_of(cur, unit);
+        for (int i = rank * sh + tid; i < min(count, (rank + 1) * sh); i += kUT) {
+            gids[i] = sel_id[i];
+            gtok[i] = sel_tok[i];
+            gsrc[i] = sel_src[i];
+            if (out_ids) out_ids[(size_t)unit * tau + i] = sid ? sid[(size_t)b * sid_stride + sel_id[i]] : sel_id[i];
         }
-        // ---- stores of this step's state, spread over the CTAs (nothing waits on them) ----
-        {
-            const int sh = (count + kUC - 1) / kUC;  // selection entries written by this CTA
-            int32_t* gids = sel.ids_of(cur, unit);
-            int32_t* gtok = sel.tok_of(cur, unit);
-            int32_t* gsrc = sel.src_of(cur, unit);
-            for (int i = rank * sh + tid; i < min(count, (rank + 1) * sh); i += kUT) {
-                gids[i] = sel_id[i];
-                gtok[i] = sel_tok[i];
-                gsrc[i] = sel_src[i];
-                if (out_ids) out_ids[(size_t)unit * tau + i] = sid ? sid[(size_t)b * sid_stride + sel_id[i]] : sel_id[i];
-            }
-            if (out_ids) {
-                const int pad = (tau - count + kUC - 1) / kUC;
-                for (int i = count + rank * pad + tid; i < min(tau, count + (rank + 1) * pad); i += kUT)
-                    out_ids[(size_t)unit * tau + i] = -1;
-            }
-            if (rank == 0) {
-                // deferred Eq. 2 state update: Sq += q_t, or reset after a boundary input (A11)
-                const bool reset = ctl.reset != 0;
-                for (int i = tid; i < GRP * D; i += kUT)
-                    Sq[((size_t)b * Hq + g * GRP) * D + i] = reset ? 0.0f : sqsum[i];
-                if (tid == 0) {
-                    cnt[unit] = reset ? 0 : ctl.cnt0 + 1;
-                    gtok[count] = ntok;
-                    *sel.count_of(cur, unit) = count;
-                    if (out_count) out_count[unit] = count;
-                    if (out_tokens) out_tokens[unit] = ntok;
-                }
-            }
-            if (rank == kUC - 1 && tid == 0) {
-                // the next step's band: the crossing point and the lowest selected key, widened
-                uint2 h = make_uint2(0u, 0xffffffffu);  // everything fits: the band is everything
-                if (ctl.kc_set) {
-                    const uint32_t kc = ctl.kc, ks = ctl.ks, w = (uint32_t)band_w;
-                    const uint32_t wl = w << kBandLoShift;
-                    h.x = kc > wl ? kc - wl : 0u;
-                    h.y = ks < 0xffffffffu - w ? ks + w : 0xffffffffu;
-                }
-                hint[unit] = h;
+        if (out_ids) {
+            const int pad = (tau - count + kUC - 1) / kUC;
+            for (int i = count + rank * pad + tid; i < min(tau, count + (rank + 1) * pad); i += kUT)
+                out_ids[(size_t)unit * tau + i] = -1;
+        }
+        if (rank == 0) {
+            // deferred Eq. 2 state update: Sq += q_t, or reset after a boundary input (A11)
+            const bool reset = ctl.reset != 0;
+            for (int i = tid; i < GRP * D; i += kUT)
+                Sq[((size_t)b * Hq + g * GRP) * D + i] = reset ? 0.0f : sqsum[i];
+            if (tid == 0) {
+                cnt[unit] = reset ? 0 : ctl.cnt0 + 1;
+                gtok[count] = ntok;
+                *sel.count_of(cur, unit) = count;
+                if (out_count) out_count[unit] = count;
+                if (out_tokens) out_tokens[unit] = ntok;
             }
         }
-        // the next kernel of the stream may start launching (it reads this step's state only after
-        // its pdl_wait, i.e. after this grid has completed)
-        pdl_trigger();
-        mma::merge_warps<D, GRP, kUW>(msm, wacc, kUT);  // the ring / gathered area is idle now
+        if (rank == kUC - 1 && tid == 0) {
+            // the next step's band: the crossing point and the lowest selected key, widened
+            uint2 h = make_uint2(0u, 0xffffffffu);  // everything fits: the band is everything
+            if (ctl.kc_set) {
+                const uint32_t kc = ctl.kc, ks = ctl.ks, w = (uint32_t)band_w;
+                const uint32_t wl = w << kBandLoShift;
+                h.x = kc > wl ? kc - wl : 0u;
+                h.y = ks < 0xffffffffu - w ? ks + w : 0xffffffffu;
+            }
+            hint[unit] = h;
+        }
     }
+    // the next kernel of the stream may start launching (it reads this step's state only after its
+    // pdl_wait, i.e. after this grid has completed)
+    pdl_trigger();
+    auto attend = [&](auto miss_tag) {
+        attend_phase<D, GRP, HOST, decltype(miss_tag)::value>(
+        rowtab, tb, te, T0, T1, q + ((size_t)b * Hq + g * GRP) * D,
+        HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D,
+        HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D,
+        HOST ? hc.Kh + (size_t)unit * hc.L * D : nullptr, HOST ? hc.Vh + (size_t)unit * hc.L * D : nullptr,
+        gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr, gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr,
+        gen.L, hc.ledger, scale_log2, msm);
+    };
+    if (HOST && any_miss) attend(std::true_type{});
+    else attend(std::false_type{});
+    SKV_USTAMP(7);
     cluster.sync();  // #2: CTA partials ready; every CTA has done its page-table lookups
     SKV_USTAMP(8);
     // host residency: the lowest rank that met a miss applies its plan (the same in every CTA that
