@@ -112,8 +112,9 @@ typedef struct {
     int32_t fill_mode;       /* skv_fill_mode (default SKV_FILL_PREFIX) */
     int32_t max_generated;   /* NEXT-2 (reading A29): > 0 keeps a local segment and grows the context -- up to
                                 this many generated tokens per (sequence, layer) appended with
-                                sentencekv_decode_append; 0 = off.  Device residency, without Quest pages
-                                (else UNSUPPORTED).  With retention (obs_window > 0) the buckets start as
+                                sentencekv_decode_append; 0 = off.  Either residency (the generated
+                                rows stay in HBM; in host residency the context rows go through the
+                                working set), without Quest pages (else UNSUPPORTED).  With retention (obs_window > 0) the buckets start as
                                 the retained buckets and the observation window's rows start the local
                                 segment (they close with the first generated sentence). */
 } skv_config;

@@ -218,9 +218,8 @@ SKV_API skv_status sentencekv_create(const skv_config* cfg_in, skv_ctx** out) {
         return SKV_ERR_INVALID_ARGUMENT;
     if (cfg.obs_window > 0 && cfg.bucket_mode == SKV_BUCKETS_QUEST) return SKV_ERR_UNSUPPORTED;
     if (cfg.max_generated < 0) return SKV_ERR_INVALID_ARGUMENT;
-    // NEXT-2 local segment: device residency, sentence / equal buckets, no retention (this build)
-    if (cfg.max_generated > 0 && (cfg.residency != SKV_KV_DEVICE || cfg.bucket_mode == SKV_BUCKETS_QUEST))
-        return SKV_ERR_UNSUPPORTED;
+    // NEXT-2 local segment: sentence / equal buckets (either residency; generated rows stay in HBM)
+    if (cfg.max_generated > 0 && cfg.bucket_mode == SKV_BUCKETS_QUEST) return SKV_ERR_UNSUPPORTED;
     if ((cfg.head_dim != 64 && cfg.head_dim != 128) || (grp != 1 && grp != 2 && grp != 4 && grp != 8) ||
         (cfg.obs_window > 0 && !skv::retain_supported(cfg.head_dim, cfg.obs_window, grp)))
         return SKV_ERR_UNSUPPORTED;
@@ -350,8 +349,8 @@ static LayerView layer_view(const skv_ctx* c, const skv::LayerState& ls) {
         return {ls.roff, ls.ret_m + 1, ls.rS, ls.PK, ls.PV, ls.ret_m, ls.rsid, ls.ret_m, false,
                 skv::GenSrc{ls.winK, ls.winV, ls.wstat, c->cfg.obs_window, ls.ret_m, c->cfg.obs_window,
                             c->cfg.obs_window}};
-    if (ls.genK)
-        return {ls.goff, c->Smax + 1, ls.gS, ls.K, ls.V, c->L, nullptr, 0, false,
+    if (ls.genK)  // host residency: context rows through the working set, generated rows in HBM
+        return {ls.goff, c->Smax + 1, ls.gS, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST,
                 skv::GenSrc{ls.genK, ls.genV, ls.gstat, c->cfg.max_generated, c->L, 0, c->tau}};
     return {c->off, c->off_stride, c->S_dev, ls.K, ls.V, c->L, nullptr, 0, c->cfg.residency == SKV_KV_HOST, none};
 }

@@ -32,6 +32,7 @@ using MmaSmem = mma::MergeSmem<D, kMW>;
 // HOST == false: rows come from kv (device residency, rows = context tokens).
 // HOST == true:  srcs[i] >= 0 -> host row (mapped pinned store), < 0 -> row -(src+1) of the
 //                previous working-set slot; every loaded row is written through to the current slot.
+//                Rows >= L are generated rows (NEXT-2, HBM): never in the working set.
 template <int D, int GRP, bool HOST>
 __global__ void __cluster_dims__(kMCL, 1, 1) __launch_bounds__(kMT, 2)
 attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bfloat16* Khost,
@@ -87,13 +88,13 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
                 const int mid = (lo + hi) >> 1;
                 if (pids[mid] < id) lo = mid + 1; else hi = mid;
             }
-            if (lo < pcount && pids[lo] == id) srcs[i] = -(ptok[lo] + 1);
+            if (lo < pcount && pids[lo] == id && srcs[i] < L) srcs[i] = -(ptok[lo] + 1);
         }
     }
     __syncthreads();
     SKV_TRACE_POINT(2);
     const int ntok = tok[count];
-    // NEXT-2 local segment (device residency): the generated sentence's tokens follow the selection
+    // NEXT-2 local segment: the generated sentence's tokens follow the selection
     int hot0 = 0, nhot = 0;
     if (gen.Kg) {
         hot0 = gen.gstat[b * 4 + 1];
@@ -137,10 +138,12 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
     const __nv_bfloat16* Vgu = gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr;
     auto rowK = [&](int r) -> const __nv_bfloat16* {
         if (!HOST) return (gen.Kg && r >= gen.L) ? Kgu + (size_t)(r - gen.L) * D : Kd + (size_t)r * D;
+        if (Kgu && r >= L) return Kgu + (size_t)(r - L) * D;  // generated row (gen.L == L)
         return r >= 0 ? Kh + (size_t)r * D : Kp + (size_t)(-(r + 1)) * D;
     };
     auto rowV = [&](int r) -> const __nv_bfloat16* {
         if (!HOST) return (gen.Kg && r >= gen.L) ? Vgu + (size_t)(r - gen.L) * D : Vd + (size_t)r * D;
+        if (Vgu && r >= L) return Vgu + (size_t)(r - L) * D;
         return r >= 0 ? Vh + (size_t)r * D : Vp + (size_t)(-(r + 1)) * D;
     };
 
@@ -169,24 +172,25 @@ attend_mma_kernel(const __nv_bfloat16* __restrict__ q, KvSrc kv, const __nv_bflo
         if (tile == tb + kMW) SKV_TRACE_POINT(7);
         if (HOST) {
             constexpr int NU = D / 32, NVP = D / 64;
-            // write the tile's rows through to the current working-set slot (gathered order)
+            // write the tile's context rows through to the current working-set slot (gathered order;
+            // generated rows stay in their HBM store)
 #pragma unroll
             for (int u = 0; u < NU; ++u) {
-                if (rk0 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq) * D + mma::kseg(cq, u)) = tr.kA[u];
-                if (rk1 != kInvalid) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq + 8) * D + mma::kseg(cq, u)) = tr.kB[u];
+                if (rk0 != kInvalid && rk0 < L) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq) * D + mma::kseg(cq, u)) = tr.kA[u];
+                if (rk1 != kInvalid && rk1 < L) *reinterpret_cast<uint4*>(Kc + (size_t)(t0 + gq + 8) * D + mma::kseg(cq, u)) = tr.kB[u];
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k)
 #pragma unroll
                 for (int pp = 0; pp < NVP; ++pp)
-                    if (rv[k] != kInvalid)
+                    if (rv[k] != kInvalid && rv[k] < L)
                         *reinterpret_cast<uint4*>(Vc + (size_t)(t0 + 2 * cq + (k & 1) + 8 * (k >> 1)) * D + 8 * gq + 64 * pp) =
                             tr.vv[k][pp];
             // host bytes: K rows (counted once per row by cq == 0 lanes) + V rows (gq == 0 lanes)
-            if (cq == 0) host_bytes += (rk0 >= 0 ? D * 2 : 0) + (rk1 >= 0 ? D * 2 : 0);
+            if (cq == 0) host_bytes += (rk0 >= 0 && rk0 < L ? D * 2 : 0) + (rk1 >= 0 && rk1 < L ? D * 2 : 0);
             if (gq == 0)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) host_bytes += (rv[k] >= 0 && rv[k] != kInvalid) ? D * 2 : 0;
+                for (int k = 0; k < 4; ++k) host_bytes += (rv[k] >= 0 && rv[k] < L) ? D * 2 : 0;
         }
     }
     if (HOST) {

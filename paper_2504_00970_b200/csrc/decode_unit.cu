@@ -220,10 +220,11 @@ __device__ __forceinline__ bool crossing_bin(const uint32_t* hist, uint32_t rem,
 // mma.sync fragments -> per-warp online softmax -> CTA partial in `msm`.  Not inlined: the caller's
 // state lives across this phase, and inlined it pushed the tile registers into local memory (spills
 // in the tile loop, measured slower); across a call it is saved once.
-//   Kd / Vd: device residency: the unit's context rows (generated rows >= genL in Kgu / Vgu);
-//            host residency: the unit's working-set rows (r >= 0), host row -(r+1) in Khu / Vhu
+//   Kd / Vd: device residency: the unit's context rows; host residency: the unit's working-set rows
+//            (r >= 0), host row -(r+1) in Khu / Vhu; rows >= genL: generated rows in Kgu / Vgu (NEXT-2)
 //   MISS:    some rows of this CTA come from host (they are written through into the working set)
-template <int D, int GRP, bool HOST, bool MISS>
+//   GEN:     generated rows may exist (NEXT-2: when Kgu / Vgu are set)
+template <int D, int GRP, bool HOST, bool MISS, bool GEN>
 __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int tb, int te, int T0, int T1,
                                           const __nv_bfloat16* __restrict__ qg, const __nv_bfloat16* Kd,
                                           const __nv_bfloat16* Vd, const __nv_bfloat16* Khu, const __nv_bfloat16* Vhu,
@@ -232,18 +233,19 @@ __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int t
                                           USmemMerge<D>& msm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int gq = lane >> 2, cq = lane & 3;
-    auto rowK = [&](int r) -> const __nv_bfloat16* {
-        return (HOST && r < 0) ? Khu + (size_t)(-(r + 1)) * D : Kd + (size_t)r * D;
-    };
-    auto rowV = [&](int r) -> const __nv_bfloat16* {
-        return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : Vd + (size_t)r * D;
-    };
-    // device rows: context rows < L, generated rows (NEXT-2) >= L
+    // HBM rows: r < genL context (device residency) or working-set (host residency) rows, r >= genL
+    // generated rows (NEXT-2) when Kgu is set; host residency: r < 0 host row -(r+1)
     auto devK = [&](int r) -> const __nv_bfloat16* {
-        return (!HOST && Kgu && r >= genL) ? Kgu + (size_t)(r - genL) * D : Kd + (size_t)r * D;
+        return (GEN && Kgu && r >= genL) ? Kgu + (size_t)(r - genL) * D : Kd + (size_t)r * D;
     };
     auto devV = [&](int r) -> const __nv_bfloat16* {
-        return (!HOST && Vgu && r >= genL) ? Vgu + (size_t)(r - genL) * D : Vd + (size_t)r * D;
+        return (GEN && Vgu && r >= genL) ? Vgu + (size_t)(r - genL) * D : Vd + (size_t)r * D;
+    };
+    auto rowK = [&](int r) -> const __nv_bfloat16* {
+        return (HOST && r < 0) ? Khu + (size_t)(-(r + 1)) * D : devK(r);
+    };
+    auto rowV = [&](int r) -> const __nv_bfloat16* {
+        return (HOST && r < 0) ? Vhu + (size_t)(-(r + 1)) * D : devV(r);
     };
     unsigned long long host_bytes = 0;
     uint4 qseg[D / 32];
@@ -303,7 +305,8 @@ __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int t
 
 }  // namespace
 
-template <int D, int GRP, bool HOST>
+// HGEN (host residency only): NEXT-2 generated rows exist (device residency checks gen.Kg at run time)
+template <int D, int GRP, bool HOST, bool HGEN>
 __global__ void __cluster_dims__(kUC, 1, 1) __launch_bounds__(kUT, 2)
 unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
                  const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq, int32_t* __restrict__ cnt,
@@ -1113,6 +1116,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     const int per = (ntl + kUC - 1) / kUC;
     const int tb = min(ntl, rank * per), te = min(ntl, tb + per);
     const int T0 = tb * kTile, T1 = min(natt, te * kTile);
+    // first row index of the generated rows in the attention's row encoding: after the context rows
+    // (device residency) or after the working-set rows (host residency)
+    const int gbase = HOST ? hc.slots * kPage : gen.L;
     // Host residency (D3 host): the HBM working set is a page cache (pages of kPage context
     // rows); a page-table entry holds the page's slot and the mask of its rows already in HBM.  A
     // selected row is read from its slot if the row is there, else from the mapped host store.  When
@@ -1148,6 +1154,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         SKV_USTAMP(26);
         for (int i = tid; i < count; i += kUT) {  // pages of the selection
             const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
+            if (HGEN && r0 >= hc.L) continue;  // a generated sentence (NEXT-2): not in the page cache
             for (int p = r0 / kPage; p <= r1 / kPage; ++p) atomicOr(&pbits[p >> 5], 1u << (p & 31));
         }
         __syncthreads();
@@ -1205,6 +1212,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         }
         for (int i = tid; i < count; i += kUT) {  // the selected rows of every page
             const int r0 = sel_src[i], r1 = r0 + (sel_tok[i + 1] - sel_tok[i]) - 1;
+            if (HGEN && r0 >= hc.L) continue;  // a generated sentence (NEXT-2): not in the page cache
             for (int p = r0 / kPage; p <= r1 / kPage; ++p) {
                 const int j = page_rank(p);
                 const int lo = max(r0, p * kPage) - p * kPage, hi = min(r1, p * kPage + kPage - 1) - p * kPage;
@@ -1258,8 +1266,8 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
         if (t < T1 && t >= ntok) {
-            const int x = t - ntok;  // local segment (device residency only)
-            r.x = gen.L + (x < gen.fixed ? x : hot0 + (x - gen.fixed));
+            const int x = t - ntok;  // local segment: generated rows
+            r.x = gbase + (x < gen.fixed ? x : hot0 + (x - gen.fixed));
         } else if (t < T1) {
             int lo2 = 0, hi2 = count - 1;  // largest i with sel_tok[i] <= t
             while (lo2 < hi2) {
@@ -1268,7 +1276,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
             const int row = sel_src[lo2] + (t - sel_tok[lo2]);
             r.x = row;
-            if constexpr (HOST) {
+            if (HGEN && row >= gen.L) {
+                r.x = gbase + (row - gen.L);  // a generated sentence (NEXT-2): its rows are in HBM
+            } else if constexpr (HOST) {
                 const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + row / kPage];
                 const int w = row % kPage;
                 if (e != kEmpty && ((e >> (16 + w)) & 1u)) {
@@ -1351,13 +1361,13 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     // pdl_wait, i.e. after this grid has completed)
     pdl_trigger();
     auto attend = [&](auto miss_tag) {
-        attend_phase<D, GRP, HOST, decltype(miss_tag)::value>(
-        rowtab, tb, te, T0, T1, q + ((size_t)b * Hq + g * GRP) * D,
-        HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D,
-        HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D,
-        HOST ? hc.Kh + (size_t)unit * hc.L * D : nullptr, HOST ? hc.Vh + (size_t)unit * hc.L * D : nullptr,
-        gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr, gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr,
-        gen.L, hc.ledger, scale_log2, msm);
+        attend_phase<D, GRP, HOST, decltype(miss_tag)::value, !HOST || HGEN>(
+            rowtab, tb, te, T0, T1, q + ((size_t)b * Hq + g * GRP) * D,
+            HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D,
+            HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D,
+            HOST ? hc.Kh + (size_t)unit * hc.L * D : nullptr, HOST ? hc.Vh + (size_t)unit * hc.L * D : nullptr,
+            gen.Kg ? gen.Kg + (size_t)unit * gen.stride * D : nullptr,
+            gen.Kg ? gen.Vg + (size_t)unit * gen.stride * D : nullptr, gbase, hc.ledger, scale_log2, msm);
     };
     if (HOST && any_miss) attend(std::true_type{});
     else attend(std::false_type{});
@@ -1417,13 +1427,13 @@ static int band_width() { return 1 << 19; }  // half-width of the band in ordere
 
 static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
 
-template <int D, int GRP, bool HOST>
+template <int D, int GRP, bool HOST, bool HGEN>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     const size_t smem = unit_smem_bytes(D, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0));
-    cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST>, smem);
+    cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST, HGEN>, smem);
     if (e != cudaSuccess) return e;
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
-    return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
+    return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST, HGEN>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, band_width(), a.out, a.out_ids,
@@ -1433,7 +1443,9 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
     const bool host = a.hc.Kh != nullptr;
-#define SKV_UN(DV, GV) return host ? launch_unit_t<DV, GV, true>(a, st) : launch_unit_t<DV, GV, false>(a, st)
+#define SKV_UN(DV, GV)                                                                                  \
+    return host ? (a.gen.Kg ? launch_unit_t<DV, GV, true, true>(a, st) : launch_unit_t<DV, GV, true, false>(a, st)) \
+                : launch_unit_t<DV, GV, false, false>(a, st)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_UN(128, 1);

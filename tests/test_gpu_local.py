@@ -14,14 +14,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(mode, seed=0, B=2, M=1, Hq=8, G=2, d=64, L=3000, tau=128, steps=40, mean_sentence=6.0, max_generated=64,
-         graph=False):
+         graph=False, residency="device"):
     import paper_2504_00970_b200 as skvlib
 
     dev = torch.device("cuda:0")
     toks, topics = synth.prompts(seed, B, L, median=20.0)
     Ks, Vs = zip(*(synth.kv_layer(seed, l, topics, G, d) for l in range(M)))
     skv = skvlib.SentenceKV(batch=B, layers=M, q_heads=Hq, kv_heads=G, head_dim=d, max_context=L, token_budget=tau,
-                            max_generated=max_generated)
+                            max_generated=max_generated,
+                            residency=skvlib.SKV_KV_HOST if residency == "host" else skvlib.SKV_KV_DEVICE)
     orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, M, Hq, G, d, max_generated=max_generated)
     Kd = [from_bits(K, dev) for K in Ks]
     Vd = [from_bits(V, dev) for V in Vs]
@@ -75,6 +76,18 @@ def _run(mode, seed=0, B=2, M=1, Hq=8, G=2, d=64, L=3000, tau=128, steps=40, mea
 def test_local_segment_and_growth(cuda_device, mode):
     worst, grown = _run(mode)
     assert grown >= 3  # several generated sentences became buckets
+
+
+@pytest.mark.parametrize("mode", ["split", "step"])
+def test_local_segment_host_residency(cuda_device, mode):
+    """The same with the prompt's K/V offloaded to pinned host memory (P3): context rows through the
+    working set / page cache, generated rows (local segment and generated buckets) from HBM."""
+    worst, grown = _run(mode, seed=4, residency="host")
+    assert grown >= 3
+
+
+def test_local_host_residency_d128_two_layers(cuda_device):
+    _run("step", seed=5, B=1, M=2, Hq=16, G=4, d=128, L=2500, tau=64, steps=40, mean_sentence=12.0, residency="host")
 
 
 @pytest.mark.parametrize("mode", ["split", "step"])
