@@ -8,5 +8,5 @@ for tool in memcheck racecheck synccheck; do
   echo "smoke $tool rc=$? $(tail -2 $O/smoke_$tool.txt | tr '\n' ' ')"
 done
 timeout -s KILL 900 compute-sanitizer --tool memcheck --error-exitcode 99 --print-limit 20 \
-  python -m pytest -q -x tests/test_gpu_retention.py -k "unambiguous and 64" tests/test_gpu_local.py -k "growth and step" > $O/next_memcheck.txt 2>&1
+  python -m pytest -q -x tests/test_gpu_retention.py tests/test_gpu_local.py -k "(unambiguous and 64) or (growth and step) or (host and d128)" > $O/next_memcheck.txt 2>&1
 echo "next rows memcheck rc=$? $(tail -2 $O/next_memcheck.txt | tr '\n' ' ')"
