@@ -549,21 +549,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             atomicAdd(&ctl.wnar, wnar);
         }
         if (tid == 0) ctl.bn = (int)total;
-#ifdef SKV_PF_ABOVE
-        // device residency: the K/V runs of this CTA's sentences above the previous step's band are
-        // (almost always) selected -- ask L2 for them now, while the cluster selects (HBM idle)
-        if constexpr (!HOST) {
-            const char* Kb = reinterpret_cast<const char*>(kv.K + (size_t)unit * kv.unit_stride * D);
-            const char* Vb = reinterpret_cast<const char*>(kv.V + (size_t)unit * kv.unit_stride * D);
-            for (int i = i0; i < i1; ++i)
-                if (keys[i] > khi && (!gen.Kg || offs[i + 1] <= gen.L)) {  // context rows only
-                    const size_t o0 = (size_t)offs[i] * D * 2;
-                    const uint32_t nb2 = (uint32_t)(offs[i + 1] - offs[i]) * D * 2;
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Kb + o0), "r"(nb2) : "memory");
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Vb + o0), "r"(nb2) : "memory");
-                }
-        }
-#endif
     }
     __syncthreads();
     SKV_USTAMP(1);
