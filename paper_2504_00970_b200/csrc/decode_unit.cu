@@ -344,13 +344,12 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     int* need = reinterpret_cast<int*>(keys);                            // [kNeedCap] pages of the selection
     uint32_t* pslot = reinterpret_cast<uint32_t*>(need + kNeedCap);     // [kNeedCap] their page-table entries
     int* slotof = reinterpret_cast<int*>(pslot + kNeedCap);             // [kNeedCap] slot this step (-1 none)
-    int* oldof = slotof + kNeedCap;                                     // [kNeedCap] page evicted for it
-    uint32_t* rowbits = reinterpret_cast<uint32_t*>(oldof + kNeedCap);  // [kNeedCap] selected rows
+    uint32_t* rowbits = reinterpret_cast<uint32_t*>(slotof + kNeedCap); // [kNeedCap] selected rows
     int* newj = reinterpret_cast<int*>(rowbits + kNeedCap);             // [kNeedCap] non-resident pages
     int* frees = newj + kNeedCap;                                       // [kNeedCap] their slots
     uint32_t* pbits = reinterpret_cast<uint32_t*>(frees + kNeedCap);    // [kMaxPageWords] pages of the selection
     uint32_t* pbase = pbits + kMaxPageWords;                            // [kMaxPageWords] rank of each word's first page
-    static_assert(kNeedCap * 28 + kMaxPageWords * 8 <= kULocalCap * 8, "plan fits the keys + offsets area");
+    static_assert(kNeedCap * 24 + kMaxPageWords * 8 <= kULocalCap * 8, "plan fits the keys + offsets area");
 
     __shared__ uint64_t bar[kUStages];
     __shared__ float qt[D];
@@ -1119,18 +1118,9 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         return (int)pbase[p >> 5] + __popc(pbits[p >> 5] & ((1u << (p & 31)) - 1u));
     };
     auto cache_plan = [&]() {
-        uint32_t* ownc = hist;  // slot -> page, copied (the histogram is idle now)
-        static_assert(kUBins >= kMaxSlots, "slot table fits the histogram");
-        // the slot owners and the clock hand are loaded first and consumed late (their latency hides
-        // under the bitmap and the scan); the page-table entries of the selection are read in ONE
-        // round, once the pages are ranked
-        constexpr int kOwnPer = kMaxSlots / kUT;
-        int32_t own_r[kOwnPer];
-#pragma unroll
-        for (int k = 0; k < kOwnPer; ++k) {
-            const int j = tid + k * kUT;
-            own_r[k] = j < hc.slots ? hc.own[(size_t)unit * hc.slots + j] : -1;
-        }
+        // the clock hand is loaded first and consumed late; the page-table entries of the selection are
+        // read in ONE round, once the pages are ranked.  A slot is free iff no page of this selection
+        // is in it (empty slots included); its owner is read only by the CTA that applies the plan.
         const int hand = hc.hand[unit];
         const int nwords = (hc.pages + 31) >> 5;
         for (int w = tid; w < nwords; w += kUT) pbits[w] = 0u;
@@ -1182,17 +1172,11 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 m &= m - 1u;
             }
         }
-#pragma unroll
-        for (int k = 0; k < kOwnPer; ++k) {
-            const int j = tid + k * kUT;
-            if (j < hc.slots) ownc[j] = (uint32_t)own_r[k];
-        }
         __syncthreads();
         for (int j = tid; j < n_need; j += kUT) {
             const uint32_t e = (uint32_t)hc.pt[(size_t)unit * hc.pages + need[j]];
             pslot[j] = e;
             slotof[j] = e == kEmpty ? -1 : (int)(e & 0xffffu);
-            oldof[j] = -1;
             if (e != kEmpty) atomicOr(&inuse[(e & 0xffffu) >> 5], 1u << (e & 31u));
         }
         for (int i = tid; i < count; i += kUT) {  // the selected rows of every page
@@ -1215,7 +1199,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             nn += (j < n_need && pslot[j] == kEmpty) ? 1u : 0u;
             int sl = hand + 2 * tid + k;
             sl = sl >= hc.slots ? sl - hc.slots : sl;
-            nf += (2 * tid + k < hc.slots && ((int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u))) ? 1u : 0u;
+            nf += (2 * tid + k < hc.slots && !((inuse[sl >> 5] >> (sl & 31)) & 1u)) ? 1u : 0u;
         }
         // (the clock scan looks at the first 2 * kUT = 512 slots from the hand; the new pages are at most kNeedCap)
         static_assert(2 * kUT >= kNeedCap, "two entries per thread cover the new pages");
@@ -1230,7 +1214,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 if (j < n_need && pslot[j] == kEmpty) newj[pn++] = j;
                 int sl = hand + 2 * tid + k;
                 sl = sl >= hc.slots ? sl - hc.slots : sl;
-                if (2 * tid + k < hc.slots && ((int)ownc[sl] < 0 || !((inuse[sl >> 5] >> (sl & 31)) & 1u))) {
+                if (2 * tid + k < hc.slots && !((inuse[sl >> 5] >> (sl & 31)) & 1u)) {
                     if (pf < (uint32_t)kNeedCap) frees[pf] = sl;
                     ++pf;
                 }
@@ -1241,7 +1225,6 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         for (int k = tid; k < n_asg; k += kUT) {
             const int j = newj[k], sl = frees[k];
             slotof[j] = sl;
-            oldof[j] = (int)ownc[sl];
         }
         if (tid == 0) last_slot_s = n_asg > 0 ? frees[n_asg - 1] : -1;
         __syncthreads();
@@ -1380,9 +1363,12 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (sl < 0) continue;
             const uint32_t e = pslot[j];
             const uint32_t mask = (e == kEmpty ? 0u : (e >> 16)) | rowbits[j];
+            if (e == kEmpty) {  // a new page: the slot's previous page (not in this selection) leaves
+                const int old = hc.own[(size_t)unit * hc.slots + sl];
+                if (old >= 0) pt[old] = (int32_t)kEmpty;
+                hc.own[(size_t)unit * hc.slots + sl] = need[j];
+            }
             pt[need[j]] = (int32_t)((uint32_t)sl | (mask << 16));
-            hc.own[(size_t)unit * hc.slots + sl] = need[j];
-            if (oldof[j] >= 0) pt[oldof[j]] = (int32_t)kEmpty;
         }
         if (tid == 0 && last_slot_s >= 0) hc.hand[unit] = (last_slot_s + 1) % hc.slots;
     }
