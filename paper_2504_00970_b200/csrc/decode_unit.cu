@@ -119,7 +119,7 @@ constexpr int kUBins = 1024;
 // point falls below the band far more often than above it (the scores of the sentences at the
 // budget's edge drift down as Q_s grows); a 4x wider lower margin cut the general-path fallbacks
 // and the step time 0.887 -> 0.866 ms (8x: lists overflow, 1.05 ms).
-constexpr int kBandLoShift = 2;
+constexpr int kBandLoShift = 2;  // (r02, with the upper-part ranking: 8x / 16x measured 0.6 % / 4 % slower)
 constexpr int kUExact = kUT;             // crossing-bin candidates ranked exactly per refinement level
 constexpr int kUGather = kUStages * kUTileBytes / 16;  // candidates gathered into the (idle) ring
 constexpr int kUBandCap = 256;           // band-path list entries per CTA
@@ -1132,6 +1132,18 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             if (HGEN && r0 >= hc.L) continue;  // a generated sentence (NEXT-2): not in the page cache
             for (int p = r0 / kPage; p <= r1 / kPage; ++p) atomicOr(&pbits[p >> 5], 1u << (p & 31));
         }
+        if (ok && ctl.kc_set) {
+            // band path: also give slots to the pages of the sentences just below the crossing point
+            // (within w of it; no rows loaded): drift into them at the next steps then only fills rows in
+            // (4w instead of w: more evictions of pages still in use later, +23 % host bytes, slower)
+            const uint32_t kc = ctl.kc, klw = kc > (uint32_t)band_w ? kc - (uint32_t)band_w : 0u;
+            const int* flg = reinterpret_cast<const int*>(gath + kUC * kUBandCap) + kUC * kUBandCap;
+            for (int i = tid; i < ctl.base[kUC]; i += kUT) {
+                const int4 e = gath[i];
+                if (flg[i] || (uint32_t)e.x < klw || (uint32_t)e.x > kc || (HGEN && e.z >= hc.L)) continue;
+                for (int p = e.z / kPage; p <= (e.z + e.w - 1) / kPage; ++p) atomicOr(&pbits[p >> 5], 1u << (p & 31));
+            }
+        }
         __syncthreads();
         SKV_USTAMP(27);
         uint32_t total;
@@ -1230,7 +1242,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         __syncthreads();
         SKV_USTAMP(29);
     };
-    int my_miss = 0;
+    int my_miss = 0, my_new = 0;  // host rows read / of them in pages with no slot yet
     for (int t = T0 + tid; t < te * kTile; t += kUT) {
         int2 r = make_int2(kInvalid, -1);
         if (t < T1 && t >= ntok) {
@@ -1254,17 +1266,22 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
                 } else {
                     r.x = -(row + 1);
                     my_miss = 1;
+                    if (e != kEmpty) r.y = (int)(e & 0xffffu) * kPage + w;  // its page has a slot: fill the row in
+                    else my_new = 1;
                 }
             }
         }
         rowtab[t - T0] = r;
     }
     const bool any_miss = __syncthreads_or(my_miss) != 0;  // (always false in device residency)
+    // a plan is needed only for pages without a slot; rows missing from a page that has one are
+    // written into it and published after barrier #2 (every CTA has done its lookups by then)
+    const bool any_new = HOST && any_miss && __syncthreads_or(my_new) != 0;
 #ifdef SKV_TRACE
     SKV_USTAMP(25);
     if (tid == 0 && unit * kUC + rank < 1024) g_unit_t[unit * kUC + rank][24] = any_miss ? 1 : 0;
 #endif
-    if (HOST && any_miss) {
+    if (HOST && any_new) {
         cache_plan();
         // write-through targets of the rows read from host
         const int n_need = n_need_s;
@@ -1345,7 +1362,19 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     // host residency: the lowest rank that met a miss applies its plan (the same in every CTA that
     // computed one) after barrier #3 -- no other CTA recomputes it, and nobody waits for the update
     bool upd = false;
-    if constexpr (HOST) upd = any_miss && *cluster.map_shared_rank(&ctl.miss_rank, 0) == rank;
+    if constexpr (HOST) {
+        upd = any_new && *cluster.map_shared_rank(&ctl.miss_rank, 0) == rank;
+        if (any_miss && !any_new) {  // no plan here: publish the rows this CTA wrote into resident pages
+            int32_t* pt = hc.pt + (size_t)unit * hc.pages;
+            for (int t = T0 + tid; t < T1; t += kUT) {
+                const int2 r = rowtab[t - T0];
+                if (r.x < 0 && r.y >= 0) {
+                    const int row = -(r.x + 1);
+                    atomicOr(&pt[row / kPage], (int32_t)(1u << (16 + row % kPage)));
+                }
+            }
+        }
+    }
     mma::merge_cluster<D, GRP, kUW, kUC>(cluster, msm, rank, out + ((size_t)b * Hq + g * GRP) * D, kUT, &peers,
                                          ((size_t)b * Hq + g * GRP) * D);
     cluster.sync();  // #3: remote reads done before any CTA of the cluster exits
