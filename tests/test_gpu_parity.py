@@ -285,6 +285,53 @@ def test_host_residency_transfer_ledger(cuda_device):
     assert skv.host_fetch_bytes(0) > first
 
 
+def test_host_residency_drift_fetches_each_row_once(cuda_device):
+    """Drift within a topic (Q_s grows, qbar moves, sentences enter the selection step by step): with a
+    page cache large enough to hold every selection of the run (r = 8), each step fetches from host
+    exactly the rows of its selection never selected before -- rows that enter a page already holding
+    a slot (filled in without a cache plan) or a page reserved for the sentences just below the
+    crossing point (slot, no rows) included: nothing is fetched twice, nothing unselected is fetched.
+    Selected ids equal the oracle's at every step."""
+    import paper_2504_00970_b200 as skvlib
+
+    B, Hq, G, d, L, tau, steps = 2, 8, 2, 64, 6000, 256, 12
+    toks, topics = synth.prompts(5, B, L, median=12.0)
+    K, V = synth.kv_layer(5, 0, topics, G, d)
+    skv = _skv(B, 1, Hq, G, d, L, tau, residency=skvlib.SKV_KV_HOST, semantic_factor=8.0)
+    orc = oracle.Oracle(toks, synth.BOUNDARY_IDS, tau, 1, Hq, G, d)
+    skv.prefill_compress(0, from_bits(K, cuda_device), from_bits(V, cuda_device),
+                         torch.from_numpy(toks).to(cuda_device), synth.BOUNDARY_IDS)
+    orc.prefill_layer(0, K, V)
+    off = skv.offsets().cpu().numpy()
+    tgt = np.array([4, 11], np.int32)
+    no_b = np.full((B,), 300, np.int32)
+    ids = torch.empty((B, G, tau), dtype=torch.int32, device=cuda_device)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=cuda_device)
+    seen = [[set() for _ in range(G)] for _ in range(B)]
+    row = d * 2 * 2  # K + V bytes per token
+    changed = 0
+    for s in range(steps):
+        q = synth.queries(5, 0, s, tgt, Hq, G, d)
+        before = skv.host_fetch_bytes(0)
+        skv.decode_step(0, from_bits(q, cuda_device), torch.from_numpy(no_b).to(cuda_device), out, sel_ids=ids)
+        _, ids_o, _ = orc.decode_select(0, q, no_b)
+        got = ids.cpu().numpy()
+        expect = 0
+        for b in range(B):
+            for g in range(G):
+                n = len(ids_o[b][g])
+                assert np.array_equal(got[b, g, :n], ids_o[b][g]), f"ids s={s} b={b} g={g}"
+                rows = set()
+                for sid in ids_o[b][g]:
+                    rows.update(range(int(off[b, sid]), int(off[b, sid + 1])))
+                new = rows - seen[b][g]
+                changed += 1 if (s > 0 and new) else 0
+                expect += len(new) * row
+                seen[b][g] |= rows
+        assert skv.host_fetch_bytes(0) - before == expect, f"step {s}"
+    assert changed >= 2  # the selection did drift
+
+
 @pytest.mark.parametrize("mode", ["split", "step"])
 @pytest.mark.parametrize("L,tau,median", [
     (40000, 4096, 25.0),   # configs[3]'s budget: ~400 pages of 16 rows per selection
