@@ -593,6 +593,9 @@ def main():
                 "duration": "graph replays' device time in the timed region / (steps x layers)",
                 "per_unit": "per layer (all units): G*S*d*2 B (bf16 E; Quest pages: min + max) + sum(ntok)*d*2*2 B "
                             "(selected K,V rows) + G*S*4*2 (scores written, offsets read) + B*Hq*d*14 (q, Sq r/w, O)"}
+    if host:  # the HBM fraction alone understates a step whose topic switches wait on PCIe
+        roofline["note"] = ("host residency: part of the selected K/V comes over the host link (see "
+                            "host_residency.link_roofline, the serial HBM + link bound)")
 
     # ---------------- the split call pair of SURVEY 8(b): decode_select + decode_attend per layer
     split = None
