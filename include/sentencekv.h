@@ -114,9 +114,10 @@ typedef struct {
                                 this many generated tokens per (sequence, layer) appended with
                                 sentencekv_decode_append; 0 = off.  Either residency (the generated
                                 rows stay in HBM; in host residency the context rows go through the
-                                working set), without Quest pages (else UNSUPPORTED).  With retention (obs_window > 0) the buckets start as
-                                the retained buckets and the observation window's rows start the local
-                                segment (they close with the first generated sentence). */
+                                working set), without Quest pages (else UNSUPPORTED).  With retention
+                                (obs_window > 0) the buckets start as the retained buckets and the
+                                observation window's rows start the local segment (they close with the
+                                first generated sentence). */
 } skv_config;
 
 /* Fills cfg with defaults (shard = everything, device residency, r = 2, obs_window = 0). */
