@@ -335,6 +335,12 @@ typedef enum {
 
 skv_status sentencekv_set_profiling(skv_ctx* ctx, int32_t on);
 
+/* Tuning of sentencekv_decode_step's selection (performance only -- results are exact for any value):
+ * the one-launch kernel first ranks a band of ordered-key width 2^log2 around the previous step's
+ * crossing point and falls back to its general path when the crossing point left it.
+ * log2 in [0, 29]; default 19.  INVALID_ARGUMENT outside the range. */
+skv_status sentencekv_set_band_log2(skv_ctx* ctx, int32_t log2);
+
 /* Synchronises, then adds the elapsed time of every profiled launch since the last read:
  * ms_out host double [SKV_K_COUNT] (total milliseconds per kind), n_out host int64 [SKV_K_COUNT]
  * (launches per kind).  Both are accumulated into (not overwritten). */

@@ -81,6 +81,7 @@ def _load():
         "sentencekv_copy_scores": (i32, [P, i32, P, P]),
         "sentencekv_launch_count": (i64, [P]),
         "sentencekv_set_profiling": (i32, [P, i32]),
+        "sentencekv_set_band_log2": (i32, [P, i32]),
         "sentencekv_host_fetch_bytes": (i32, [P, i32, P]),
         "sentencekv_profile_read": (i32, [P, P, P]),
         "sentencekv_retained_tokens": (i32, [P, i32]),
@@ -316,6 +317,10 @@ class SentenceKV:
 
     def set_profiling(self, on: bool):
         _check(self.ctx, lib.sentencekv_set_profiling(self.ctx, 1 if on else 0))
+
+    def set_band_log2(self, log2: int):
+        """Selection band width of decode_step (tuning; results are exact for any value)."""
+        _check(self.ctx, lib.sentencekv_set_band_log2(self.ctx, int(log2)))
 
     def profile_read(self):
         """{kernel: (total_ms, launches)} of the profiled launches since the last read."""

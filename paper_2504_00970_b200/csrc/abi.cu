@@ -773,6 +773,7 @@ SKV_API skv_status sentencekv_decode_step(skv_ctx* c, int32_t layer, const void*
         a.kv = skv::KvSrc{v.K, v.V, v.stride, 0};
         a.cand = c->unit_cand;
         a.hint = ls.unit_hint;
+        a.band_w = 1 << c->band_log2;
         // the step kernel reads prefill outputs (S, offsets, E) before its programmatic-launch wait:
         // never overlap it with a prefill kernel
         a.pdl = !c->after_prefill;
@@ -987,6 +988,12 @@ SKV_API skv_status sentencekv_host_fetch_bytes(skv_ctx* c, int32_t layer, uint64
     unsigned long long v = 0;
     SKV_CUDA(c, cudaMemcpy(&v, c->layer[layer].ledger, sizeof(v), cudaMemcpyDeviceToHost));
     *bytes_out = v;
+    return SKV_OK;
+}
+
+SKV_API skv_status sentencekv_set_band_log2(skv_ctx* c, int32_t log2) {
+    if (!c || log2 < 0 || log2 > 29) return SKV_ERR_INVALID_ARGUMENT;
+    c->band_log2 = log2;
     return SKV_OK;
 }
 

@@ -1423,8 +1423,6 @@ bool unit_supported(int d, int grp, int Smax, int tau, int slots, int pages, int
 size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
 
 
-static int band_width() { return 1 << 19; }  // half-width of the band in ordered-key units
-
 static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
 
 template <int D, int GRP, bool HOST, bool HGEN>
@@ -1436,7 +1434,7 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST, HGEN>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
-                      a.cand, a.hint, band_width(), a.out, a.out_ids,
+                      a.cand, a.hint, a.band_w, a.out, a.out_ids,
                       a.out_count, a.out_tokens, a.sid, a.sid_stride, a.qmode, a.gen, a.peers, scale_log2,
                       trace_counter++);
 }

@@ -133,6 +133,7 @@ struct skv_ctx {
     std::string err;
     skv_status sticky = SKV_OK;
     int64_t launches = 0;
+    int band_log2 = 19;                // half-width of the step kernel's selection band (ordered-key units)
 
     // prompt state
     int L = 0;
@@ -283,6 +284,7 @@ struct UnitArgs {
     int4* cand;                    // [unit_cand_entries] overflow scratch of the candidate lists
     uint2* hint;                   // [units] selection band of the previous step (klo, khi ordered keys)
     bool pdl;                      // launch with programmatic stream serialization
+    int band_w;                    // half-width of the selection band (ordered-key units)
     float* out;                    // [B][Hq][d]
     int32_t* out_ids;              // optional [B][G][tau]
     int32_t* out_count;            // optional [B][G]

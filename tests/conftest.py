@@ -19,3 +19,25 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(autouse=True)
+def _band_width_under_test(monkeypatch):
+    """SKV_TEST_BAND_LOG2=n (set by test_step_kernel_selection_paths_subprocess for its child pytest):
+    every context the tests create ranks with a selection band of width 2^n (sentencekv_set_band_log2),
+    so that narrow or very wide bands drive the step kernel through mode 2, the general path and list
+    overflows.  A test hook: the library itself reads no environment."""
+    n = os.environ.get("SKV_TEST_BAND_LOG2")
+    if n is None:
+        yield
+        return
+    import paper_2504_00970_b200 as skvlib
+
+    init = skvlib.SentenceKV.__init__
+
+    def patched(self, *a, **kw):
+        init(self, *a, **kw)
+        self.set_band_log2(int(n))
+
+    monkeypatch.setattr(skvlib.SentenceKV, "__init__", patched)
+    yield

@@ -85,5 +85,6 @@ def test_null_arguments_are_rejected():
     assert skv.lib.sentencekv_create(None, None) == 1
     assert skv.lib.sentencekv_prefill_compress(None, 0, None, 1, None, 0, None, None, 2.0, 1, None, None) == 1
     assert skv.lib.sentencekv_decode_select(None, 0, None, None, None, None, None, None) == 1
+    assert skv.lib.sentencekv_set_band_log2(None, 19) == 1
     assert skv.lib.sentencekv_decode_attend(None, 0, None, None, None) == 1
     assert skv.lib.sentencekv_destroy(None) == 0

@@ -165,18 +165,18 @@ def test_one_token_sentences_zero_query(cuda_device, L):
     _custom_case(cuda_device, toks, K, V, [q0, q0, q1], np.array([[300], [13], [300]], np.int32), tau, Hq, G, d)
 
 
-@pytest.mark.parametrize("band_log2", ["0", "12", "30"])
+@pytest.mark.parametrize("band_log2", ["0", "12", "29"])
 def test_step_kernel_selection_paths_subprocess(cuda_device, band_log2):
     """The one-launch step kernel ranks either the band around the previous crossing point or, when
     the crossing left the band, the entries above it (mode 2) or the union of the local candidate
-    lists (general path).  A zero-width or narrow band (SKV_BAND_LOG2=0, 12) sends most steps through
-    mode 2 and the general path, a very wide one (30) overflows the
-    band lists: all must give the oracle's selections and outputs."""
+    lists (general path).  A narrow band (sentencekv_set_band_log2 0 or 12, applied to every context of
+    the child pytest by tests/conftest.py) sends most steps through mode 2 and the general path, a very
+    wide one (29) overflows the band lists: all must give the oracle's selections and outputs."""
     import os
     import subprocess
     import sys
 
-    env = dict(os.environ, SKV_BAND_LOG2=band_log2)
+    env = dict(os.environ, SKV_TEST_BAND_LOG2=band_log2)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "tests/test_gpu_parity.py",
                         "tests/test_gpu_fullsize.py",
