@@ -144,6 +144,7 @@ struct Ctl {
     int ok, nsel, nband, count, ntok, reset, cnt0, kc_set;
     int miss_rank;      // host residency (rank 0's copy): lowest rank of the cluster that met a miss
     int mode;           // band-list ranking mode (see step 2), -1 = general path
+    int below;          // general path because the crossing point fell below the band (no list overflowed)
     uint32_t WHI, WB, WN, ks, kc;
     uint32_t lo, hi, cb, rem, ncand;
     unsigned long long thr;
@@ -595,6 +596,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             }
             ctl.mode = mode;
             ctl.ok = mode >= 0;
+            ctl.below = (!ovf && mode < 0) ? 1 : 0;  // (then WHI + WB <= tau and klo > 0)
 #ifdef SKV_TRACE
             if (unit * kUC + rank < 1024) {
                 g_unit_t[unit * kUC + rank][10] = (ovf ? 1 : 0) | (WHI > (uint32_t)tau ? 2 : 0) |
@@ -847,18 +849,30 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     SKV_USTAMP(3);
     if (!ok) {
         // ------------------------------------------------------------ general path
-        // 2a. local candidates
+        // 2a. local candidates.  When the crossing point fell below the band (no list overflowed), every
+        // sentence at or above klo is selected (they weigh WHI + WB <= tau and rank above the rest):
+        // the problem shrinks to the keys below klo with the budget left, rem0 = tau - (WHI + WB) --
+        // the same cut and exact ranking over them; the sentences at or above klo join the lists
+        // (selected by the compaction's key64 > thr like any entry ranked above the crossing)
+        const bool below = ctl.below != 0;
+        const uint32_t rem0 = below ? (uint32_t)tau - (ctl.WHI + ctl.WB) : (uint32_t)tau;
         for (int i = tid; i < kUBins; i += kUT) hist[i] = 0u;
         __syncthreads();
         {
-            const Binner bin(ctl.lo, ctl.hi);
-            for (int i = i0; i < i1; ++i) atomicAdd(&hist[bin(keys[i])], (uint32_t)(offs[i + 1] - offs[i]));
+            const uint32_t hi_b = below ? min(ctl.hi, klo - 1u) : ctl.hi;  // ranked keys: [ctl.lo, hi_b]
+            const bool any_b = n > 0 && ctl.lo <= hi_b;
+            const Binner bin(ctl.lo, any_b ? hi_b : ctl.lo);
+            auto ranked = [&](uint32_t k) { return any_b && k <= hi_b; };
+            for (int i = i0; i < i1; ++i)
+                if (ranked(keys[i])) atomicAdd(&hist[bin(keys[i])], (uint32_t)(offs[i + 1] - offs[i]));
             __syncthreads();
             uint32_t cb = 0, rem_unused;
-            const bool cross = crossing_bin(hist, (uint32_t)tau, ws32, ctl, &cb, &rem_unused);
-            // keep bins >= cb (all sentences if the CTA's total fits), in ascending sentence order
+            const bool cross = crossing_bin(hist, rem0, ws32, ctl, &cb, &rem_unused);
+            // keep bins >= cb (all sentences if the CTA's total fits) and (below) every key >= klo, in
+            // ascending sentence order
+            auto keep = [&](uint32_t k) { return !ranked(k) || !cross || bin(k) >= cb; };
             uint32_t mine = 0;
-            for (int i = i0; i < i1; ++i) mine += (!cross || bin(keys[i]) >= cb) ? 1u : 0u;
+            for (int i = i0; i < i1; ++i) mine += keep(keys[i]) ? 1u : 0u;
             uint32_t total;
             const uint32_t excl = block_incl_sum<uint32_t>(mine, ws32, &total) - mine;
             const bool to_global = total > (uint32_t)kUOwnCap;
@@ -866,7 +880,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             uint32_t pos = excl;
             for (int i = i0; i < i1; ++i) {
                 const uint32_t k = keys[i];
-                if (!cross || bin(k) >= cb) dst[pos++] = make_int4((int)k, s0 + i, offs[i], offs[i + 1] - offs[i]);
+                if (keep(k)) dst[pos++] = make_int4((int)k, s0 + i, offs[i], offs[i + 1] - offs[i]);
             }
             if (tid == 0) {
                 ctl.own_count = (int)total;
@@ -937,6 +951,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
             uint32_t mn = 0xffffffffu, mx = 0u;
             for (int i = c0; i < c1; ++i) {
                 const uint32_t k = (uint32_t)cand(i).x;
+                if (below && k >= klo) continue;  // selected; not ranked
                 mn = min(mn, k);
                 mx = max(mx, k);
             }
@@ -951,10 +966,10 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
         SKV_USTAMP(20);
 
         // 2c. exact selection over the union of the lists
-        uint32_t lo = ctl.lo, hi = ctl.hi, rem = (uint32_t)tau;
-        bool all_fit = false;
+        uint32_t lo = ctl.lo, hi = ctl.hi, rem = rem0;
+        bool all_fit = lo > hi;  // (below: nothing under klo -- everything listed is selected)
         unsigned long long thr = 0;  // select key64 > thr
-        for (int level = 0;; ++level) {
+        for (int level = 0; !all_fit; ++level) {
             if (lo == hi) {
                 // the remaining contenders all carry key lo: ascending sentence order decides (A14)
                 uint32_t tw = 0;
