@@ -225,7 +225,9 @@ __device__ __forceinline__ bool crossing_bin(const uint32_t* hist, uint32_t rem,
 //            (r >= 0), host row -(r+1) in Khu / Vhu; rows >= genL: generated rows in Kgu / Vgu (NEXT-2)
 //   MISS:    some rows of this CTA come from host (they are written through into the working set)
 //   GEN:     generated rows may exist (NEXT-2: when Kgu / Vgu are set)
-template <int D, int GRP, bool HOST, bool MISS, bool GEN>
+//   PIPE:    a warp's next tile is loaded while it computes the current one (two tiles of fragment
+//            registers: only when one CTA per SM leaves the kernel the registers, e.g. tau = 4096)
+template <int D, int GRP, bool HOST, bool MISS, bool GEN, bool PIPE>
 __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int tb, int te, int T0, int T1,
                                           const __nv_bfloat16* __restrict__ qg, const __nv_bfloat16* Kd,
                                           const __nv_bfloat16* Vd, const __nv_bfloat16* Khu, const __nv_bfloat16* Vhu,
@@ -253,7 +255,69 @@ __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int t
     mma::load_q<D, GRP>(qseg, qg, lane);
     mma::WarpAcc<D> wacc;
     wacc.init();
-    {
+    // issue: the loads of a tile's rows (K: tokens gq, gq+8; V: tokens 2cq, 2cq+1, 2cq+8, 2cq+9)
+    auto issue = [&](int tile, mma::TileRegs<D>& tr) {
+        const int t0 = tile * kTile;
+        const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+        const __nv_bfloat16* pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int2 rv = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+            pv[k] = rv.x != kInvalid ? (MISS ? rowV(rv.x) : devV(rv.x)) : nullptr;
+        }
+        if constexpr (MISS)
+            mma::load_tile<D>(tr, rk0.x != kInvalid ? rowK(rk0.x) : nullptr,
+                              rk1.x != kInvalid ? rowK(rk1.x) : nullptr, pv, lane);
+        else
+            mma::load_tile<D>(tr, rk0.x != kInvalid ? devK(rk0.x) : nullptr,
+                              rk1.x != kInvalid ? devK(rk1.x) : nullptr, pv, lane);
+    };
+    // finish: QK, online softmax, PV of a loaded tile (+ host residency write-through)
+    auto finish = [&](int tile, const mma::TileRegs<D>& tr) {
+        const int t0 = tile * kTile;
+        mma::compute_tile<D, GRP>(wacc, tr, qseg, t0 + gq < T1, t0 + gq + 8 < T1, scale_log2, lane);
+        if constexpr (MISS) {
+            // write-through of the rows read from host into their working-set slot
+            const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
+            int2 rv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rv[k] = rowtab[t0 + 2 * cq + (k & 1) + 8 * (k >> 1) - T0];
+            constexpr int NU = D / 32, NVP = D / 64;
+            __nv_bfloat16* Kw = const_cast<__nv_bfloat16*>(Kd);  // (host residency: the working set)
+            __nv_bfloat16* Vw = const_cast<__nv_bfloat16*>(Vd);
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+                if (rk0.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk0.y * D + mma::kseg(cq, u)) = tr.kA[u];
+                if (rk1.y >= 0) *reinterpret_cast<uint4*>(Kw + (size_t)rk1.y * D + mma::kseg(cq, u)) = tr.kB[u];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int pp = 0; pp < NVP; ++pp)
+                    if (rv[k].y >= 0) *reinterpret_cast<uint4*>(Vw + (size_t)rv[k].y * D + 8 * gq + 64 * pp) = tr.vv[k][pp];
+            // host bytes: K rows (counted by the cq == 0 lanes) + V rows (gq == 0 lanes)
+            if (cq == 0) host_bytes += (rk0.x != kInvalid && rk0.x < 0 ? D * 2 : 0) + (rk1.x != kInvalid && rk1.x < 0 ? D * 2 : 0);
+            if (gq == 0)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) host_bytes += (rv[k].x != kInvalid && rv[k].x < 0) ? D * 2 : 0;
+        }
+    };
+    if constexpr (PIPE) {
+        mma::TileRegs<D> ta, tc;  // two tiles in flight per warp
+        int tile = tb + warp;
+        if (tile < te) issue(tile, ta);
+        while (tile < te) {
+            int nx = tile + kUW;
+            if (nx < te) issue(nx, tc);
+            finish(tile, ta);
+            tile = nx;
+            if (tile >= te) break;
+            nx = tile + kUW;
+            if (nx < te) issue(nx, ta);
+            finish(tile, tc);
+            tile = nx;
+        }
+    } else {  // (the same work, written out: as lambdas the host miss variant spilled more)
         for (int tile = tb + warp; tile < te; tile += kUW) {
             const int t0 = tile * kTile;
             const int2 rk0 = rowtab[t0 + gq - T0], rk1 = rowtab[t0 + gq + 8 - T0];
@@ -307,8 +371,8 @@ __device__ __noinline__ void attend_phase(const int2* __restrict__ rowtab, int t
 }  // namespace
 
 // HGEN (host residency only): NEXT-2 generated rows exist (device residency checks gen.Kg at run time)
-template <int D, int GRP, bool HOST, bool HGEN>
-__global__ void __cluster_dims__(kUC, 1, 1) __launch_bounds__(kUT, 2)
+template <int D, int GRP, bool HOST, bool HGEN, int MINB>
+__global__ void __cluster_dims__(kUC, 1, 1) __launch_bounds__(kUT, MINB)
 unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ input_token,
                  const int32_t* __restrict__ bset, int nb, float* __restrict__ Sq, int32_t* __restrict__ cnt,
                  const __nv_bfloat16* __restrict__ E, const int32_t* __restrict__ S, const int32_t* __restrict__ off,
@@ -1361,7 +1425,7 @@ unit_step_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict_
     // pdl_wait, i.e. after this grid has completed)
     pdl_trigger();
     auto attend = [&](auto miss_tag) {
-        attend_phase<D, GRP, HOST, decltype(miss_tag)::value, !HOST || HGEN>(
+        attend_phase<D, GRP, HOST, decltype(miss_tag)::value, !HOST || HGEN, MINB == 1>(
             rowtab, tb, te, T0, T1, q + ((size_t)b * Hq + g * GRP) * D,
             HOST ? hc.wsK + (size_t)unit * hc.slots * kPage * D : kv.K + (size_t)unit * kv.unit_stride * D,
             HOST ? hc.wsV + (size_t)unit * hc.slots * kPage * D : kv.V + (size_t)unit * kv.unit_stride * D,
@@ -1440,13 +1504,13 @@ size_t unit_cand_entries(int units) { return (size_t)units * kUC * kULocalCap; }
 
 static int trace_counter = 0;  // launch index for the trace build's per-launch stamps
 
-template <int D, int GRP, bool HOST, bool HGEN>
+template <int D, int GRP, bool HOST, bool HGEN, int MINB>
 static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
     const size_t smem = unit_smem_bytes(D, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0));
-    cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST, HGEN>, smem);
+    cudaError_t e = ensure_smem((const void*)unit_step_kernel<D, GRP, HOST, HGEN, MINB>, smem);
     if (e != cudaSuccess) return e;
     const float scale_log2 = (float)(1.0 / sqrt((double)D) * 1.4426950408889634);
-    return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST, HGEN>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
+    return launch_pdl_if(a.pdl, unit_step_kernel<D, GRP, HOST, HGEN, MINB>, dim3(kUC, a.G, a.B), dim3(kUT), smem, st,
                       a.q, a.input_token,
                       a.bset, a.nb, a.Sq, a.cnt, a.E, a.S, a.off, a.off_stride, a.G, a.Smax, a.scores, a.sel, a.kv, a.hc,
                       a.cand, a.hint, a.band_w, a.out, a.out_ids,
@@ -1456,9 +1520,14 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
 
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
     const bool host = a.hc.Kh != nullptr;
-#define SKV_UN(DV, GV)                                                                                  \
-    return host ? (a.gen.Kg ? launch_unit_t<DV, GV, true, true>(a, st) : launch_unit_t<DV, GV, true, false>(a, st)) \
-                : launch_unit_t<DV, GV, false, false>(a, st)
+    // one CTA per SM anyway (large tau): the kernel may take the SM's registers (two tiles in flight)
+    const bool one = unit_smem_bytes(d, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0)) > 100 * 1024;
+#define SKV_UN1(DV, GV, MB)                                                                                  \
+    return host ? (a.gen.Kg ? launch_unit_t<DV, GV, true, true, MB>(a, st) : launch_unit_t<DV, GV, true, false, MB>(a, st)) \
+                : launch_unit_t<DV, GV, false, false, MB>(a, st)
+#define SKV_UN(DV, GV)            \
+    if (one) SKV_UN1(DV, GV, 1);  \
+    else SKV_UN1(DV, GV, 2)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_UN(128, 1);
@@ -1475,6 +1544,7 @@ cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
         }
     }
 #undef SKV_UN
+#undef SKV_UN1
     return cudaErrorInvalidValue;
 }
 
