@@ -1518,16 +1518,39 @@ static cudaError_t launch_unit_t(const UnitArgs& a, cudaStream_t st) {
                       trace_counter++);
 }
 
+// Two CTAs per SM fit the selection's shared memory (the kernel's static + dynamic + the per-CTA
+// reservation, twice, within the SM's): then the kernel keeps <= 128 registers per thread (two
+// CTAs' worth); else the instantiation with launch bounds (256, 1) may use the SM's registers for
+// two attention tiles in flight per warp.
+template <int D, int GRP, bool HOST, bool HGEN>
+static bool unit_two_per_sm(size_t smem) {
+    static const size_t fixed = [] {
+        cudaFuncAttributes fa{};
+        int dev = 0, resv = 0;
+        cudaGetDevice(&dev);
+        cudaFuncGetAttributes(&fa, (const void*)unit_step_kernel<D, GRP, HOST, HGEN, 2>);
+        cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        return fa.sharedSizeBytes + (size_t)resv;
+    }();
+    static const size_t per_sm = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        return (size_t)v;
+    }();
+    return 2 * (smem + fixed) <= per_sm;
+}
+
 cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
     const bool host = a.hc.Kh != nullptr;
-    // one CTA per SM anyway (large tau): the kernel may take the SM's registers (two tiles in flight)
-    const bool one = unit_smem_bytes(d, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0)) > 100 * 1024;
-#define SKV_UN1(DV, GV, MB)                                                                                  \
-    return host ? (a.gen.Kg ? launch_unit_t<DV, GV, true, true, MB>(a, st) : launch_unit_t<DV, GV, true, false, MB>(a, st)) \
-                : launch_unit_t<DV, GV, false, false, MB>(a, st)
-#define SKV_UN(DV, GV)            \
-    if (one) SKV_UN1(DV, GV, 1);  \
-    else SKV_UN1(DV, GV, 2)
+    const size_t smem = unit_smem_bytes(d, a.sel.tau, a.sel.tau + (a.gen.Kg ? a.gen.max_att : 0));
+#define SKV_UN2(DV, GV, H, HG)                                                                    \
+    return unit_two_per_sm<DV, GV, H, HG>(smem) ? launch_unit_t<DV, GV, H, HG, 2>(a, st)        \
+                                                : launch_unit_t<DV, GV, H, HG, 1>(a, st)
+#define SKV_UN(DV, GV)                                   \
+    if (!host) SKV_UN2(DV, GV, false, false);            \
+    else if (a.gen.Kg) SKV_UN2(DV, GV, true, true);      \
+    else SKV_UN2(DV, GV, true, false)
     if (d == 128) {
         switch (grp) {
             case 1: SKV_UN(128, 1);
@@ -1544,7 +1567,7 @@ cudaError_t launch_unit(const UnitArgs& a, int grp, int d, cudaStream_t st) {
         }
     }
 #undef SKV_UN
-#undef SKV_UN1
+#undef SKV_UN2
     return cudaErrorInvalidValue;
 }
 
