@@ -21,7 +21,7 @@ for res in device host; do
   timeout -s KILL 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
      -k regex:"segment|compress|unit_step|score|select|attend" -c 200 --csv --log-file $O/launches_$res.csv \
      python bench.py --residency $res $A > /dev/null 2>&1; echo "launches $res rc=$?"
-  timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:unit_step -s 40 -c 1 \
+  [ -n "$NO_FULL" ] || timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:unit_step -s 40 -c 1 \
      -o $O/prof_step_$res python bench.py --residency $res $A > $O/ncu_step_$res.log 2>&1; echo "full $res rc=$?"
 done
 TAG=$TAG/san bash scripts/gpu_sanitize.sh
