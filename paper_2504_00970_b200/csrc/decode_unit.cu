@@ -36,6 +36,11 @@
 //      to global memory for the unit's last CTA to combine, with a split cluster barrier so that
 //      CTAs exit early, was measured slower on B200: with programmatic launch the next layer's
 //      clusters then fill the freed SMs unevenly and part of the grid runs as a second wave.)
+//      This phase is the non-inlined attend_phase; where one CTA per SM is all the shared memory
+//      allows, the kernel is instantiated with launch bounds (256, 1) and a warp keeps two tiles in
+//      flight.
+// Host residency: see the page-cache comment at the row-table step (fill-in without a plan for pages
+// that have a slot; the plan for pages that have none, applied by the lowest planning rank).
 #include <cooperative_groups.h>
 
 #include <algorithm>
